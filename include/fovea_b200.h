@@ -1,0 +1,145 @@
+/*
+ * fovea_b200.h -- C ABI of the B200 (sm_100a) image-transformation path.
+ *
+ * Drop-in boundary for the reference's hot path (`fovea`, a Python/NumPy
+ * package; paths below are relative to /root/reference/pkg/src/fovea/):
+ * every entry point replaces one reference function and keeps its semantics
+ * (HWC interleaved images, same dtypes, rounding, interpolation and border).
+ * The Python mirror `paper_2505_12425_b200` binds these with ctypes
+ * (INTEGRATION.md shows the binding).
+ *
+ * Conventions shared by every entry point
+ *   - All image pointers are caller-owned DEVICE memory; nothing is allocated
+ *     or freed inside (the reference's preallocated-dst discipline,
+ *     imgproc.py:1-6, bench.py:139-148).
+ *   - Images are batches of N HWC images. Strides are in BYTES:
+ *       *_img_stride  distance between consecutive images,
+ *       *_row_pitch   distance between consecutive rows (>= width*C*elem;
+ *                     crop views keep their parent's pitch, image.py:66-75).
+ *     Pixels are C interleaved elements; channel stride is one element.
+ *   - Small per-call parameters (warp matrices, normalisation LUT) are HOST
+ *     pointers; they are copied into the kernel parameter block, so no device
+ *     allocation or H2D copy happens per call.
+ *   - `stream` is a cudaStream_t (0 = legacy default stream). Calls are
+ *     asynchronous on that stream and deterministic (bit-identical reruns).
+ *   - Return: FV_OK (0) on success; FV_EINVAL for a bad argument (checked
+ *     before any launch; message in fv_last_error()); FV_ECUDA when the
+ *     launch failed (cudaGetLastError text in fv_last_error()).
+ *   - n == 0 is a valid no-op (empty batch).
+ *   - Argument *validation in the reference's order* (SizeMismatch,
+ *     UnsupportedDtype, AliasedBuffers) is done by the host mirror before it
+ *     calls here; the ABI checks only what it needs to be memory-safe.
+ */
+#ifndef FOVEA_B200_H
+#define FOVEA_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define FV_OK 0
+#define FV_EINVAL (-1)
+#define FV_ECUDA (-2)
+
+/* ABI version (major*100 + minor). */
+int fv_version(void);
+
+/* Thread-local text of the last failure ("" if none). */
+const char* fv_last_error(void);
+
+/* Number of kernel launches issued by this library since load (all threads).
+ * Used by bench.py to report `gpu_launches`. */
+uint64_t fv_launch_count(void);
+
+/* ---- a1: imgproc.gray_from_rgb (imgproc.py:43-64) ------------------------
+ * u8: floor((f64(r)*0.299 + f64(g)*0.587) + f64(b)*0.114 + 0.5), exact.
+ * f32: the same f64 sum narrowed to f32. src has 3 channels, dst 1. */
+int fv_gray_from_rgb_u8(const uint8_t* src, int64_t src_img_stride, int64_t src_row_pitch,
+                        uint8_t* dst, int64_t dst_img_stride, int64_t dst_row_pitch,
+                        int32_t n, int32_t height, int32_t width, void* stream);
+int fv_gray_from_rgb_f32(const float* src, int64_t src_img_stride, int64_t src_row_pitch,
+                         float* dst, int64_t dst_img_stride, int64_t dst_row_pitch,
+                         int32_t n, int32_t height, int32_t width, void* stream);
+
+/* ---- a4: image.to_float_scaled (image.py:150-160) -------------------------
+ * dst = f32(src) / f32(255), IEEE division, any channel count. */
+int fv_to_float_scaled(const uint8_t* src, int64_t src_img_stride, int64_t src_row_pitch,
+                       float* dst, int64_t dst_img_stride, int64_t dst_row_pitch,
+                       int32_t n, int32_t height, int32_t width, int32_t channels, void* stream);
+
+/* ---- a3: imgproc.resize_bilinear (imgproc.py:100-123) ---------------------
+ * f32 bilinear, pixel-centre mapping sx=(x+0.5)*(src_w/dst_w)-0.5 in f64,
+ * clamp before floor, blend in the reference's f32 op order (no FMA). */
+int fv_resize_bilinear_f32(const float* src, int64_t src_img_stride, int64_t src_row_pitch,
+                           int32_t src_height, int32_t src_width,
+                           float* dst, int64_t dst_img_stride, int64_t dst_row_pitch,
+                           int32_t dst_height, int32_t dst_width,
+                           int32_t channels, int32_t n, void* stream);
+
+/* ---- a6: service.app._resize_u8 bilinear (app.py:64-78) -----
+ * to_float_scaled -> resize_bilinear -> x f32(255) -> Tensor.cast(u8)
+ * (tensor.py:265-282: round half away from zero, saturate), bit-exact,
+ * fused in one pass (no f32 intermediate in HBM). */
+int fv_resize_bilinear_u8(const uint8_t* src, int64_t src_img_stride, int64_t src_row_pitch,
+                          int32_t src_height, int32_t src_width,
+                          uint8_t* dst, int64_t dst_img_stride, int64_t dst_row_pitch,
+                          int32_t dst_height, int32_t dst_width,
+                          int32_t channels, int32_t n, void* stream);
+
+/* ---- a10: fused resize -> normalise -> HWC-to-CHW (builder contract) -----
+ * The a6 u8 result u at (dst_height, dst_width), then
+ * lut[c*256 + u] = ((f32(u)/f32(255)) - mean[c]) / std[c] (host-built table,
+ * C*256 floats, channels <= 4), written planar: dst + n*dst_img_stride +
+ * c*dst_plane_stride + y*dst_row_pitch + x*4. Replaces the composition
+ * _resize_u8 (app.py:64-78) + to_float_scaled (image.py:150-160). */
+int fv_resize_normalize_chw(const uint8_t* src, int64_t src_img_stride, int64_t src_row_pitch,
+                            int32_t src_height, int32_t src_width,
+                            float* dst, int64_t dst_img_stride, int64_t dst_plane_stride,
+                            int64_t dst_row_pitch, int32_t dst_height, int32_t dst_width,
+                            int32_t channels, int32_t n, const float* lut_host, void* stream);
+
+/* ---- a8: warp_affine (absent from the reference) -------------
+ * Inverse-mapped bilinear warp. minv_host: n * 6 doubles, the per-image
+ * INVERSE (dst->src) 2x3 matrix, row-major. sx = m0*x + (m1*y + m2),
+ * sy = m3*x + (m4*y + m5) in f64; per-tap constant border; blend as a3;
+ * u8 images use the a6 recipe. */
+int fv_warp_affine_f32(const float* src, int64_t src_img_stride, int64_t src_row_pitch,
+                       int32_t src_height, int32_t src_width,
+                       float* dst, int64_t dst_img_stride, int64_t dst_row_pitch,
+                       int32_t dst_height, int32_t dst_width, int32_t channels, int32_t n,
+                       const double* minv_host, float border, void* stream);
+int fv_warp_affine_u8(const uint8_t* src, int64_t src_img_stride, int64_t src_row_pitch,
+                      int32_t src_height, int32_t src_width,
+                      uint8_t* dst, int64_t dst_img_stride, int64_t dst_row_pitch,
+                      int32_t dst_height, int32_t dst_width, int32_t channels, int32_t n,
+                      const double* minv_host, uint8_t border, void* stream);
+
+/* ---- a9: warp_perspective (absent from the reference) --------
+ * hinv_host: n * 9 doubles, per-image INVERSE homography, row-major.
+ * X = h0*x + (h1*y + h2), Y = h3*x + (h4*y + h5), W = h6*x + (h7*y + h8);
+ * W == 0 or non-finite coordinate -> raw border; else r = 1/W,
+ * sx = X*r, sy = Y*r and the warp_affine sampler. */
+int fv_warp_perspective_u8(const uint8_t* src, int64_t src_img_stride, int64_t src_row_pitch,
+                           int32_t src_height, int32_t src_width,
+                           uint8_t* dst, int64_t dst_img_stride, int64_t dst_row_pitch,
+                           int32_t dst_height, int32_t dst_width, int32_t channels, int32_t n,
+                           const double* hinv_host, uint8_t border, void* stream);
+int fv_warp_perspective_f32(const float* src, int64_t src_img_stride, int64_t src_row_pitch,
+                            int32_t src_height, int32_t src_width,
+                            float* dst, int64_t dst_img_stride, int64_t dst_row_pitch,
+                            int32_t dst_height, int32_t dst_width, int32_t channels, int32_t n,
+                            const double* hinv_host, float border, void* stream);
+
+/* ---- tuning / introspection ---------------------------------------------
+ * Force the generic direct-gather resize kernel instead of the staged
+ * (TMA-bulk) strip kernel: 0 = auto (default), 1 = always gather.
+ * Exposed so the parity tests can cover both GPU paths. */
+void fv_set_resize_path(int32_t mode);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* FOVEA_B200_H */

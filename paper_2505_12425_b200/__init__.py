@@ -1,0 +1,39 @@
+"""fovea-b200: the kornia-rs / `fovea` image-transformation hot path on B200.
+
+Public API (drop-in for the reference's `fovea.imgproc` / `fovea.image`
+functions on torch CUDA tensors):
+
+    gray_from_rgb(src, dst)                    imgproc.py:43-64
+    resize_bilinear(src, dst)                  imgproc.py:100-123 (f32)
+    resize_bilinear_u8(src, dst)               service/app.py:64-78 (_resize_u8)
+    to_float_scaled(src, dst)                  image.py:150-160
+    warp_affine(src, dst, m, border=0)         builder contract
+    warp_perspective(src, dst, h, border=0)    builder contract
+    resize_normalize_chw(src, dst, mean, std)  fused preprocessing
+
+Every call is one sm_100a kernel launch through the C ABI in
+include/fovea_b200.h; there is no CPU fallback.
+"""
+from .errors import (  # noqa: F401
+    AliasedBuffers,
+    FoveaError,
+    NativeError,
+    NonContiguous,
+    ShapeMismatch,
+    SingularTransform,
+    SizeMismatch,
+    UnsupportedDevice,
+    UnsupportedDtype,
+)
+from .image import to_float_scaled  # noqa: F401
+from .imgproc import (  # noqa: F401
+    gray_from_rgb,
+    normalize_lut,
+    resize_bilinear,
+    resize_bilinear_u8,
+    resize_normalize_chw,
+    warp_affine,
+    warp_perspective,
+)
+
+__version__ = "0.1.0"

@@ -1,0 +1,78 @@
+"""ctypes binding of the C ABI declared in include/fovea_b200.h.
+
+The library is the product: there is no CPU fallback. Loading fails loudly
+(`NativeError`) when `lib/libfovea_b200.so` is missing; build it with
+`python -m paper_2505_12425_b200._build` (or `__graft_entry__.build()`).
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import threading
+
+from .errors import NativeError
+
+LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "lib", "libfovea_b200.so")
+
+_c = ctypes
+_I64, _I32, _P, _D = _c.c_int64, _c.c_int32, _c.c_void_p, _c.c_double
+
+# symbol -> argtypes; mirrors include/fovea_b200.h one to one
+_IMG2 = [_P, _I64, _I64, _P, _I64, _I64]
+SIGNATURES = {
+    "fv_version": ([], _c.c_int),
+    "fv_last_error": ([], _c.c_char_p),
+    "fv_launch_count": ([], _c.c_uint64),
+    "fv_set_resize_path": ([_I32], None),
+    "fv_gray_from_rgb_u8": (_IMG2 + [_I32, _I32, _I32, _P], _c.c_int),
+    "fv_gray_from_rgb_f32": (_IMG2 + [_I32, _I32, _I32, _P], _c.c_int),
+    "fv_to_float_scaled": (_IMG2 + [_I32, _I32, _I32, _I32, _P], _c.c_int),
+    "fv_resize_bilinear_f32": ([_P, _I64, _I64, _I32, _I32, _P, _I64, _I64, _I32, _I32, _I32, _I32, _P], _c.c_int),
+    "fv_resize_bilinear_u8": ([_P, _I64, _I64, _I32, _I32, _P, _I64, _I64, _I32, _I32, _I32, _I32, _P], _c.c_int),
+    "fv_resize_normalize_chw": ([_P, _I64, _I64, _I32, _I32, _P, _I64, _I64, _I64, _I32, _I32, _I32, _I32, _P, _P],
+                                _c.c_int),
+    "fv_warp_affine_f32": ([_P, _I64, _I64, _I32, _I32, _P, _I64, _I64, _I32, _I32, _I32, _I32, _P, _c.c_float, _P],
+                           _c.c_int),
+    "fv_warp_affine_u8": ([_P, _I64, _I64, _I32, _I32, _P, _I64, _I64, _I32, _I32, _I32, _I32, _P, _c.c_uint8, _P],
+                          _c.c_int),
+    "fv_warp_perspective_u8": ([_P, _I64, _I64, _I32, _I32, _P, _I64, _I64, _I32, _I32, _I32, _I32, _P, _c.c_uint8,
+                                _P], _c.c_int),
+    "fv_warp_perspective_f32": ([_P, _I64, _I64, _I32, _I32, _P, _I64, _I64, _I32, _I32, _I32, _I32, _P, _c.c_float,
+                                 _P], _c.c_int),
+}
+
+_lib = None
+_lock = threading.Lock()
+
+
+def lib():
+    """The loaded library (loaded on first use)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    with _lock:
+        if _lib is None:
+            if not os.path.exists(LIB_PATH):
+                raise NativeError(
+                    f"CUDA library not built: {LIB_PATH} is missing "
+                    "(run `python -m paper_2505_12425_b200._build`); there is no CPU fallback")
+            import torch  # noqa: F401  -- loads the shared libcudart the library binds to
+            handle = ctypes.CDLL(LIB_PATH)
+            for name, (args, res) in SIGNATURES.items():
+                fn = getattr(handle, name)
+                fn.argtypes = args
+                fn.restype = res
+            _lib = handle
+    return _lib
+
+
+def call(name: str, *args) -> None:
+    """Call an ABI entry point and raise `NativeError` on a non-zero return."""
+    rc = getattr(lib(), name)(*args)
+    if rc != 0:
+        msg = lib().fv_last_error().decode(errors="replace")
+        raise NativeError(f"{name} failed ({rc}): {msg}")
+
+
+def launch_count() -> int:
+    return int(lib().fv_launch_count())

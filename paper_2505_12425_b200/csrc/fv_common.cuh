@@ -1,0 +1,144 @@
+// fv_common.cuh -- shared device helpers for the sm_100a image kernels.
+//
+// Exact-arithmetic building blocks. Every helper reproduces one rounding step
+// of the reference (NumPy, IEEE round-to-nearest per op, no FMA contraction):
+// the float ops below are written with explicit __f*_rn / __d*_rn intrinsics,
+// which nvcc never contracts into FMAs.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/fovea_b200.h"
+
+namespace fv {
+
+// ---------------------------------------------------------------------------
+// error / launch bookkeeping (fv_util.cu)
+// ---------------------------------------------------------------------------
+int set_error(int code, const char* fmt, ...);
+int check_launch(const char* what);
+void count_launch();
+
+// ---------------------------------------------------------------------------
+// u8 <-> unit float
+// ---------------------------------------------------------------------------
+
+// RN(f32(u) / f32(255)) for u in [0, 255] -- image.py:159-160.
+// f32(u) via the 2^23 magic (exact, no I2F), then a two-term reciprocal:
+// RN(u*RHI + RN(u*RLO)) equals the IEEE quotient for all 256 inputs
+// (checked exhaustively on the host and in tests/test_gpu_parity.py).
+__device__ __forceinline__ float u8_to_unit(uint32_t u) {
+  const float RHI = __uint_as_float(0x3B808081u);  // f32(1/255)
+  const float RLO = __uint_as_float(0xAF7EFEFFu);  // f32(1/255 - RHI) = -2.3191758e-10
+  float f = __fsub_rn(__uint_as_float(0x4B000000u | u), 8388608.0f);
+  return __fmaf_rn(f, RHI, __fmul_rn(f, RLO));
+}
+
+// app.py:75 then tensor.py:273-276 for a non-negative blend result v <= 1:
+// y = RN(v*255); t = RN(y + 0.5); q = floor(t); q <= 255 (see DESIGN.md §4:
+// bilinear weights sum to <= 1 in f32, so no clamp can trigger).
+// floor(t) for 0 <= t < 2^23 is one round-down add of 2^23.
+__device__ __forceinline__ uint32_t unit_to_u8(float v) {
+  float y = __fmul_rn(v, 255.0f);
+  float t = __fadd_rn(y, 0.5f);
+  float r = __fadd_rd(t, 8388608.0f);
+  return __float_as_uint(r) - 0x4B000000u;
+}
+
+// Same as unit_to_u8 but with explicit saturation; used where the input is
+// not a convex blend of unit values.
+__device__ __forceinline__ uint32_t unit_to_u8_sat(float v) {
+  float y = __fmul_rn(v, 255.0f);
+  float t = __fadd_rn(y, 0.5f);
+  t = fminf(fmaxf(t, 0.0f), 255.0f);
+  float r = __fadd_rd(t, 8388608.0f);
+  return __float_as_uint(r) - 0x4B000000u;
+}
+
+// imgproc.py:118-123: top = a00*(1-fx) + a01*fx, etc. -- every product and
+// sum separately rounded. w0 = RN(1 - f), w1 = f.
+__device__ __forceinline__ float lerp_ref(float a, float b, float w0, float w1) {
+  return __fadd_rn(__fmul_rn(a, w0), __fmul_rn(b, w1));
+}
+
+// ---------------------------------------------------------------------------
+// resize coordinate map -- imgproc.py:76-78, 109-116
+// s = clip((i + 0.5) * scale - 0.5, 0, n - 1) in f64, scale = src_n / dst_n;
+// i0 = floor(s); i1 = min(i0 + 1, n - 1); f = f32(s - i0).
+// ---------------------------------------------------------------------------
+struct AxisTap {
+  int i0, i1;
+  float w0, w1;  // RN(1 - f), f
+};
+
+__device__ __forceinline__ AxisTap axis_tap(int i, double scale, int src_n) {
+  double s = __dadd_rn(__dmul_rn(__dadd_rn((double)i, 0.5), scale), -0.5);
+  s = fmin(fmax(s, 0.0), (double)(src_n - 1));
+  double fl = floor(s);
+  AxisTap t;
+  t.i0 = (int)fl;
+  t.i1 = min(t.i0 + 1, src_n - 1);
+  t.w1 = __double2float_rn(__dadd_rn(s, -fl));
+  t.w0 = __fsub_rn(1.0f, t.w1);
+  return t;
+}
+
+// ---------------------------------------------------------------------------
+// element load / store helpers
+// ---------------------------------------------------------------------------
+template <typename T>
+__device__ __forceinline__ const T* row_ptr(const void* base, int64_t img_stride, int64_t pitch,
+                                            int n, int y) {
+  return reinterpret_cast<const T*>(reinterpret_cast<const char*>(base) + n * img_stride + y * pitch);
+}
+template <typename T>
+__device__ __forceinline__ T* row_ptr_mut(void* base, int64_t img_stride, int64_t pitch, int n, int y) {
+  return reinterpret_cast<T*>(reinterpret_cast<char*>(base) + n * img_stride + y * pitch);
+}
+
+// tap value as the blend operand: u8 -> unit float, f32 -> itself
+__device__ __forceinline__ float tap_value(uint8_t u) { return u8_to_unit(u); }
+__device__ __forceinline__ float tap_value(float f) { return f; }
+
+// ---------------------------------------------------------------------------
+// mbarrier + TMA bulk copy (cp.async.bulk) PTX wrappers
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void fence_mbar_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+// 1-D bulk copy global -> shared, completion signalled on `bar` (TMA unit,
+// SASS UBLKCP). dst/src 16-byte aligned, bytes a multiple of 16.
+__device__ __forceinline__ void tma_bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+}  // namespace fv
