@@ -109,8 +109,9 @@ __global__ void __launch_bounds__(128) resize_gather_kernel(const __grid_constan
 // staged strip kernel
 // ---------------------------------------------------------------------------
 
-// Sorted distinct source rows a band needs: the merge of y0(y), y1(y) over
-// the band's destination rows (both non-decreasing in y). Consumer and
+// Sorted distinct source rows a band needs: the union of y0(y), y1(y) over
+// the band's destination rows. Both are non-decreasing in y and y1 <= y0 + 1,
+// so a row not yet seen is always above every row seen so far. Consumer and
 // producer walk the same sequence.
 struct RowSeq {
   int y, k, last;
@@ -125,7 +126,7 @@ __device__ __forceinline__ int next_row(RowSeq& s, int ye, double scale_y, int s
     } else {
       s.k = 1;
     }
-    if (r != s.last) {
+    if (r > s.last) {  // y0(y+1) may be below y1(y): emit each row once, in order
       s.last = r;
       return r;
     }

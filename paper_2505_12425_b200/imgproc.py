@@ -157,21 +157,17 @@ def _matrices(m, n: int, rows: int, inverse: bool) -> np.ndarray:
         a = np.broadcast_to(a, (n, rows, 3))
     if a.shape != (n, rows, 3):
         raise ShapeMismatch(f"expected a {rows}x3 matrix or {n}x{rows}x3 matrices, got {a.shape}")
-    out = np.empty((n, rows, 3), np.float64)
-    for i in range(n):
-        if inverse:
-            out[i] = a[i]
-            continue
-        full = np.eye(3)
-        full[:rows] = a[i]
-        try:
-            inv = np.linalg.inv(full)
-        except np.linalg.LinAlgError as e:
-            raise SingularTransform(f"warp matrix {i} is singular") from e
-        if not np.all(np.isfinite(inv)):
-            raise SingularTransform(f"warp matrix {i} is singular")
-        out[i] = inv[:rows]
-    return np.ascontiguousarray(out)
+    if inverse:
+        return np.ascontiguousarray(a)
+    full = np.broadcast_to(np.eye(3), (n, 3, 3)).copy()
+    full[:, :rows] = a
+    try:
+        inv = np.linalg.inv(full)  # batched f64 LAPACK getrf/getri, same per-matrix result as the oracle's
+    except np.linalg.LinAlgError as e:
+        raise SingularTransform("warp matrix is singular") from e
+    if not np.all(np.isfinite(inv)):
+        raise SingularTransform("warp matrix is singular")
+    return np.ascontiguousarray(inv[:, :rows])
 
 
 def _warp(src, dst, m, border, inverse, perspective):
