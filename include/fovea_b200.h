@@ -133,9 +133,10 @@ int fv_warp_perspective_f32(const float* src, int64_t src_img_stride, int64_t sr
                             const double* hinv_host, float border, void* stream);
 
 /* ---- tuning / introspection ---------------------------------------------
- * Force the generic direct-gather resize kernel instead of the staged
- * (TMA-bulk) strip kernel: 0 = auto (default), 1 = always gather.
- * Exposed so the parity tests can cover both GPU paths. */
+ * Resize kernel selection: 0 = auto (default: exact 2:1 / 1:2 fast paths,
+ * else the staged TMA strip kernel, else the direct-gather kernel),
+ * 1 = always the direct-gather kernel, 2 = never the integer-ratio fast
+ * paths. Exposed so the parity tests cover every GPU path. */
 void fv_set_resize_path(int32_t mode);
 
 #ifdef __cplusplus

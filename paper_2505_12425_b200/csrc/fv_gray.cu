@@ -43,9 +43,9 @@ __global__ void __launch_bounds__(128) gray_u8_vec_kernel(const uint8_t* __restr
     if (x0 + 16 <= w) {
       uint4 v[3];
       const uint4* s4 = reinterpret_cast<const uint4*>(s);
-      v[0] = __ldcs(s4);
-      v[1] = __ldcs(s4 + 1);
-      v[2] = __ldcs(s4 + 2);
+      v[0] = __ldg(s4);
+      v[1] = __ldg(s4 + 1);
+      v[2] = __ldg(s4 + 2);
       const uint32_t* wd = reinterpret_cast<const uint32_t*>(v);
       uint32_t out[4] = {0, 0, 0, 0};
 #pragma unroll

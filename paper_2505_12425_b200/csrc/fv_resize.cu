@@ -30,7 +30,6 @@
 namespace fv {
 
 enum { MODE_U8 = 0, MODE_F32 = 1, MODE_CHW = 2 };
-constexpr int RING = 4;
 constexpr int MAX_LUT = 4 * 256;
 constexpr int kMaxStripSmem = 96 * 1024;
 
@@ -50,24 +49,6 @@ struct ResizeArgs {
 
 struct LutArg {
   float v[MAX_LUT];
-};
-
-// ---------------------------------------------------------------------------
-// output stage
-// ---------------------------------------------------------------------------
-template <typename InT, int MODE>
-struct OutT;
-template <>
-struct OutT<uint8_t, MODE_U8> {
-  using T = uint8_t;
-};
-template <>
-struct OutT<float, MODE_F32> {
-  using T = float;
-};
-template <>
-struct OutT<uint8_t, MODE_CHW> {
-  using T = float;
 };
 
 // ---------------------------------------------------------------------------
@@ -109,255 +90,260 @@ __global__ void __launch_bounds__(128) resize_gather_kernel(const __grid_constan
 // staged strip kernel
 // ---------------------------------------------------------------------------
 
-// Sorted distinct source rows a band needs: the union of y0(y), y1(y) over
-// the band's destination rows. Both are non-decreasing in y and y1 <= y0 + 1,
-// so a row not yet seen is always above every row seen so far. Consumer and
-// producer walk the same sequence.
-struct RowSeq {
-  int y, k, last;
+template <typename InT, int C, int MODE>
+struct StripCfg {
+  // consumer warps; the tile must hold whole pixels (C = 3 -> multiple of 3)
+  static constexpr int NCW = (C == 3) ? 6 : 4;
+  // lane ownership: groups of V contiguous elements (u8: 4 bytes -> one
+  // 32-bit store) or V = 1 element / pixel, G groups per lane, groups of a
+  // warp interleaved so that a warp's taps and stores are contiguous
+  static constexpr int V = MODE == MODE_U8 ? 4 : 1;
+  static constexpr int G = MODE == MODE_U8 ? 2 : (MODE == MODE_F32 ? 8 : 4);
+  static constexpr int EPT = MODE == MODE_CHW ? G * C : G * V;  // elements per thread
+  static constexpr int TW_PX = MODE == MODE_CHW ? NCW * 32 * G : NCW * 32 * G * V / C;
+  static constexpr int RING = 8;
+  static constexpr int NT = (NCW + 1) * 32;  // + one producer warp
+  static_assert(MODE == MODE_CHW || (NCW * 32 * G * V) % C == 0, "tile must hold whole pixels");
 };
-__device__ __forceinline__ int next_row(RowSeq& s, int ye, double scale_y, int sh) {
-  while (s.y < ye) {
-    const AxisTap t = axis_tap(s.y, scale_y, sh);
-    const int r = s.k == 0 ? t.i0 : t.i1;
-    if (s.k == 1) {
-      s.k = 0;
-      ++s.y;
-    } else {
-      s.k = 1;
-    }
-    if (r > s.last) {  // y0(y+1) may be below y1(y): emit each row once, in order
-      s.last = r;
-      return r;
-    }
-  }
-  return -1;
+
+// Weights whose products are exact for every operand of this mode: any
+// power of two for unit-range operands (u8/255 blends are never subnormal),
+// only 0 and 1 for arbitrary f32 operands.
+template <int MODE>
+__device__ __forceinline__ bool exact_weight(float w) {
+  return MODE == MODE_F32 ? (w == 0.0f || w == 1.0f) : pow2_or_zero(w);
 }
 
-template <typename InT, int C, int E, int MODE, int NT>
-__global__ void __launch_bounds__(NT, 2) resize_strip_kernel(const __grid_constant__ ResizeArgs a,
-                                                             const __grid_constant__ LutArg lut_arg) {
+template <typename InT, int C, int MODE>
+__global__ void __launch_bounds__(StripCfg<InT, C, MODE>::NT, 3)
+    resize_strip_kernel(const __grid_constant__ ResizeArgs a, const __grid_constant__ LutArg lut_arg) {
+  using Cfg = StripCfg<InT, C, MODE>;
+  constexpr int NCW = Cfg::NCW, V = Cfg::V, G = Cfg::G, EPT = Cfg::EPT, RING = Cfg::RING;
   extern __shared__ __align__(128) uint8_t smem[];
   uint64_t* full = reinterpret_cast<uint64_t*>(smem);
-  float* lut = reinterpret_cast<float*>(smem + 64);
-  uint8_t* slots = smem + 64 + (MODE == MODE_CHW ? C * 256 * 4 : 0);
+  uint64_t* empty = full + RING;
+  int4* rowtab = reinterpret_cast<int4*>(smem + 16 * RING);
+  float* lut = reinterpret_cast<float*>(smem + 16 * RING + 16 * a.band_rows);
+  uint8_t* slots = smem + 16 * RING + 16 * a.band_rows + (MODE == MODE_CHW ? C * 256 * 4 : 0);
 
   const int tid = threadIdx.x;
+  const int warp = tid >> 5, lane = tid & 31;
   const int n = blockIdx.z;
-  const int tile = blockIdx.x;
-  const int p0 = tile * a.tile_px;
-  const int p1 = min(p0 + a.tile_px, a.dw);
+  const int p0 = blockIdx.x * Cfg::TW_PX;
+  const int p1 = min(p0 + Cfg::TW_PX, a.dw);
   const int yb = blockIdx.y * a.band_rows;
-  const int ye = min(yb + a.band_rows, a.dh);
+  const int nrows = min(a.band_rows, a.dh - yb);
 
-  // source footprint of the tile: columns [xs_lo, xs_hi]
+  // source footprint of the tile: columns [xs_lo, xs_hi], one TMA bulk copy per row
   const int xs_lo = axis_tap(p0, a.scale_x, a.sw).i0;
   const int xs_hi = axis_tap(p1 - 1, a.scale_x, a.sw).i1;
   const int seg_byte = xs_lo * C * (int)sizeof(InT);
   const int shift = seg_byte & 15;
-  const int gstart = seg_byte - shift;
   const uint32_t nbytes = (uint32_t)((shift + (xs_hi + 1 - xs_lo) * C * (int)sizeof(InT) + 15) & ~15);
-  const char* src_img = reinterpret_cast<const char*>(a.src) + n * a.s_is + gstart;
 
-  RowSeq ps = {yb, 0, -1};
   if (tid == 0) {
 #pragma unroll
-    for (int s = 0; s < RING; ++s) mbar_init(&full[s], 1);
+    for (int s = 0; s < RING; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], NCW);
+    }
     fence_mbar_init();
   }
+  // destination-row table of the band: y0, y1, RN(1 - fy), fy (imgproc.py:109-116)
+  for (int i = tid; i < nrows; i += blockDim.x) {
+    const AxisTap t = axis_tap(yb + i, a.scale_y, a.sh);
+    rowtab[i] = make_int4(t.i0, t.i1, __float_as_int(t.w0), __float_as_int(t.w1));
+  }
   if (MODE == MODE_CHW) {
-    for (int i = tid; i < C * 256; i += NT) lut[i] = lut_arg.v[i];
-  }
-  __syncthreads();
-  if (tid == 0) {
-#pragma unroll 1
-    for (int s = 0; s < RING; ++s) {
-      const int r = next_row(ps, ye, a.scale_y, a.sh);
-      if (r < 0) break;
-      mbar_expect_tx(&full[s], nbytes);
-      tma_bulk_g2s(slots + s * a.slot_bytes, src_img + r * a.s_rp, nbytes, &full[s]);
-    }
+    for (int i = tid; i < C * 256; i += blockDim.x) lut[i] = lut_arg.v[i];
   }
 
-  // per-element horizontal taps (loop-invariant over the band)
-  const int shift_el = shift / (int)sizeof(InT);
-  int o0[E], o1[E];
-  float w0[E], w1[E];
-  bool valid[E];
+  // ------------------------------------------------------------------ producer
+  if (warp == NCW) {
+    __syncthreads();
+    (void)__syncthreads_and(1);  // pairs with the consumers' tile-uniform vote
+    if (lane == 0) {
+      const char* src_img = reinterpret_cast<const char*>(a.src) + n * a.s_is + (seg_byte - shift);
+      int last = -1, k = 0;
+      for (int i = 0; i < nrows; ++i) {
+        const int4 rt = rowtab[i];
 #pragma unroll
-  for (int e = 0; e < E; ++e) {
-    const int idx = tid * E + e;
-    const int px = p0 + idx / C;
-    const int ch = idx % C;
-    valid[e] = px < p1;
-    const AxisTap t = axis_tap(valid[e] ? px : p0, a.scale_x, a.sw);
-    o0[e] = shift_el + (t.i0 - xs_lo) * C + ch;
-    o1[e] = shift_el + (t.i1 - xs_lo) * C + ch;
-    w0[e] = t.w0;
-    w1[e] = t.w1;
+        for (int q = 0; q < 2; ++q) {
+          const int r = q == 0 ? rt.x : rt.y;
+          if (r <= last) continue;  // rows are non-decreasing; each is fetched once
+          last = r;
+          const int slot = k % RING;
+          if (k >= RING) mbar_wait_sleep(&empty[slot], (uint32_t)(((k / RING) - 1) & 1));
+          mbar_expect_tx(&full[slot], nbytes);
+          tma_bulk_g2s(slots + slot * a.slot_bytes, src_img + (int64_t)r * a.s_rp, nbytes, &full[slot]);
+          ++k;
+        }
+      }
+    }
+    return;
   }
 
-  float ha[E], hb[E];
-  int ra = -1, rb = -1;
-  int k = 0;  // source rows consumed
+  // ------------------------------------------------------------------ consumers
+  // per-element horizontal taps, loop-invariant over the band
+  const int shift_el = shift / (int)sizeof(InT);
+  int oa[EPT], ob[EPT];
+  float wa[EPT], wb[EPT];
+  bool hfma = true;
+#pragma unroll
+  for (int e = 0; e < EPT; ++e) {
+    int px, ch;
+    if (MODE == MODE_CHW) {
+      px = p0 + warp * 32 * G + (e / C) * 32 + lane;
+      ch = e % C;
+    } else {
+      const int idx = warp * (32 * G * V) + (e / V) * (32 * V) + lane * V + (e % V);
+      px = p0 + idx / C;
+      ch = idx % C;
+    }
+    const AxisTap t = axis_tap(px < p1 ? px : p0, a.scale_x, a.sw);
+    const int o0 = shift_el + (t.i0 - xs_lo) * C + ch;
+    const int o1 = shift_el + (t.i1 - xs_lo) * C + ch;
+    // order the taps so that the second product is the exact one, if any
+    const bool swap = !exact_weight<MODE>(t.w1) && exact_weight<MODE>(t.w0);
+    oa[e] = swap ? o1 : o0;
+    ob[e] = swap ? o0 : o1;
+    wa[e] = swap ? t.w1 : t.w0;
+    wb[e] = swap ? t.w0 : t.w1;
+    hfma = hfma && exact_weight<MODE>(wb[e]);
+  }
+  __syncthreads();  // row table, LUT and barriers ready
+  hfma = __syncthreads_and(hfma) != 0;  // tile-uniform choice of blend form (producer passed 1 above)
 
-  auto consume = [&](float (&h)[E]) {
+  float ha[EPT], hb[EPT];
+  int ra = -1, rb = -1, k = 0;
+
+  auto consume = [&](float (&h)[EPT]) {
     const int slot = k % RING;
     mbar_wait(&full[slot], (uint32_t)((k / RING) & 1));
     const InT* seg = reinterpret_cast<const InT*>(slots + slot * a.slot_bytes);
+    if (hfma) {
 #pragma unroll
-    for (int e = 0; e < E; ++e) h[e] = lerp_ref(tap_value(seg[o0[e]]), tap_value(seg[o1[e]]), w0[e], w1[e]);
-    __syncthreads();  // every thread is done with this slot
-    if (tid == 0) {
-      const int r = next_row(ps, ye, a.scale_y, a.sh);
-      if (r >= 0) {
-        fence_proxy_async();
-        mbar_expect_tx(&full[slot], nbytes);
-        tma_bulk_g2s(slots + slot * a.slot_bytes, src_img + r * a.s_rp, nbytes, &full[slot]);
-      }
+      for (int e = 0; e < EPT; ++e) h[e] = lerp_fma(tap_value(seg[oa[e]]), tap_value(seg[ob[e]]), wa[e], wb[e]);
+    } else {
+#pragma unroll
+      for (int e = 0; e < EPT; ++e) h[e] = lerp_ref(tap_value(seg[oa[e]]), tap_value(seg[ob[e]]), wa[e], wb[e]);
     }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[slot]);
     ++k;
   };
 
-  using OT = typename OutT<InT, MODE>::T;
 #pragma unroll 1
-  for (int y = yb; y < ye; ++y) {
-    const AxisTap ty = axis_tap(y, a.scale_y, a.sh);
-    if (ty.i0 != ra) {
-      if (ty.i0 == rb) {
+  for (int i = 0; i < nrows; ++i) {
+    const int4 rt = rowtab[i];
+    if (rt.x != ra) {
+      if (rt.x == rb) {
 #pragma unroll
-        for (int e = 0; e < E; ++e) ha[e] = hb[e];
+        for (int e = 0; e < EPT; ++e) ha[e] = hb[e];
       } else {
         consume(ha);
       }
-      ra = ty.i0;
+      ra = rt.x;
     }
-    if (ty.i1 != rb) {
-      if (ty.i1 == ra) {
+    if (rt.y != rb) {
+      if (rt.y == ra) {
 #pragma unroll
-        for (int e = 0; e < E; ++e) hb[e] = ha[e];
+        for (int e = 0; e < EPT; ++e) hb[e] = ha[e];
       } else {
         consume(hb);
       }
-      rb = ty.i1;
+      rb = rt.y;
+    }
+    const float wy0 = __int_as_float(rt.z), wy1 = __int_as_float(rt.w);
+    float o[EPT];
+    if (exact_weight<MODE>(wy1)) {
+#pragma unroll
+      for (int e = 0; e < EPT; ++e) o[e] = lerp_fma(ha[e], hb[e], wy0, wy1);
+    } else if (exact_weight<MODE>(wy0)) {
+#pragma unroll
+      for (int e = 0; e < EPT; ++e) o[e] = lerp_fma(hb[e], ha[e], wy1, wy0);
+    } else {
+#pragma unroll
+      for (int e = 0; e < EPT; ++e) o[e] = lerp_ref(ha[e], hb[e], wy0, wy1);
     }
 
+    const int y = yb + i;
     if constexpr (MODE == MODE_U8) {
-      uint8_t* drow = row_ptr_mut<uint8_t>(a.dst, a.d_is, a.d_rp, n, y) + p0 * C + tid * E;
-      uint32_t q[E];
+      uint8_t* drow = row_ptr_mut<uint8_t>(a.dst, a.d_is, a.d_rp, n, y) + p0 * C;
+      const int row_el = (p1 - p0) * C;
 #pragma unroll
-      for (int e = 0; e < E; ++e) q[e] = unit_to_u8(lerp_ref(ha[e], hb[e], ty.w0, ty.w1));
-      if (a.vec_store && valid[E - 1]) {
-        static_assert(E % 16 == 0, "u8 strip stores 16-byte vectors");
+      for (int j = 0; j < G; ++j) {
+        const int idx = warp * (32 * G * V) + j * (32 * V) + lane * V;
+        uint32_t q[V];
 #pragma unroll
-        for (int v = 0; v < E / 16; ++v) {
-          uint32_t wd[4];
-#pragma unroll
-          for (int j = 0; j < 4; ++j) {
-            const int b = v * 16 + j * 4;
-            wd[j] = __byte_perm(__byte_perm(q[b], q[b + 1], 0x0040), __byte_perm(q[b + 2], q[b + 3], 0x0040),
-                                0x5410);
-          }
-          __stcs(reinterpret_cast<uint4*>(drow) + v, make_uint4(wd[0], wd[1], wd[2], wd[3]));
-        }
-      } else {
-#pragma unroll
-        for (int e = 0; e < E; ++e)
-          if (valid[e]) drow[e] = (uint8_t)q[e];
-      }
-    } else if constexpr (MODE == MODE_F32) {
-      float* drow = row_ptr_mut<float>(a.dst, a.d_is, a.d_rp, n, y) + p0 * C + tid * E;
-      float o[E];
-#pragma unroll
-      for (int e = 0; e < E; ++e) o[e] = lerp_ref(ha[e], hb[e], ty.w0, ty.w1);
-      if (a.vec_store && valid[E - 1]) {
-        static_assert(E % 4 == 0, "f32 strip stores 16-byte vectors");
-#pragma unroll
-        for (int v = 0; v < E / 4; ++v)
-          __stcs(reinterpret_cast<float4*>(drow) + v, make_float4(o[4 * v], o[4 * v + 1], o[4 * v + 2], o[4 * v + 3]));
-      } else {
-#pragma unroll
-        for (int e = 0; e < E; ++e)
-          if (valid[e]) drow[e] = o[e];
-      }
-    } else {  // MODE_CHW: thread owns pixels [p0 + 4*tid, +4), all C channels
-      static_assert(E == 4 * C, "CHW strip: 4 pixels per thread");
-      char* img = reinterpret_cast<char*>(a.dst) + n * a.d_is + y * a.d_rp;
-      const int px = p0 + tid * 4;
-#pragma unroll
-      for (int ch = 0; ch < C; ++ch) {
-        float o[4];
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          const int e = j * C + ch;
-          o[j] = lut[ch * 256 + unit_to_u8(lerp_ref(ha[e], hb[e], ty.w0, ty.w1))];
-        }
-        float* dp = reinterpret_cast<float*>(img + ch * a.d_ps) + px;
-        if (a.vec_store && valid[E - 1]) {
-          __stcs(reinterpret_cast<float4*>(dp), make_float4(o[0], o[1], o[2], o[3]));
+        for (int v = 0; v < V; ++v) q[v] = unit_to_u8(o[j * V + v]);
+        if (a.vec_store && idx + V <= row_el) {
+          const uint32_t wd = __byte_perm(__byte_perm(q[0], q[1], 0x0040), __byte_perm(q[2], q[3], 0x0040), 0x5410);
+          __stcs(reinterpret_cast<uint32_t*>(drow + idx), wd);
         } else {
 #pragma unroll
-          for (int j = 0; j < 4; ++j)
-            if (valid[j * C]) dp[j] = o[j];
+          for (int v = 0; v < V; ++v)
+            if (idx + v < row_el) drow[idx + v] = (uint8_t)q[v];
+        }
+      }
+    } else if constexpr (MODE == MODE_F32) {
+      float* drow = row_ptr_mut<float>(a.dst, a.d_is, a.d_rp, n, y) + p0 * C;
+      const int row_el = (p1 - p0) * C;
+#pragma unroll
+      for (int j = 0; j < G; ++j) {
+        const int idx = warp * (32 * G) + j * 32 + lane;
+        if (idx < row_el) __stcs(drow + idx, o[j]);
+      }
+    } else {
+      char* img = reinterpret_cast<char*>(a.dst) + n * a.d_is + (int64_t)y * a.d_rp;
+#pragma unroll
+      for (int j = 0; j < G; ++j) {
+        const int px = p0 + warp * 32 * G + j * 32 + lane;
+        if (px < p1) {
+#pragma unroll
+          for (int ch = 0; ch < C; ++ch)
+            __stcs(reinterpret_cast<float*>(img + ch * a.d_ps) + px, lut[ch * 256 + unit_to_u8(o[j * C + ch])]);
         }
       }
     }
   }
-  (void)sizeof(OT);
 }
 
 // ---------------------------------------------------------------------------
 // host dispatch
 // ---------------------------------------------------------------------------
-static int g_resize_path = 0;  // 0 auto, 1 force gather
+static int g_resize_path = 0;  // 0 auto, 1 force gather, 2 force strip (no integer-ratio fast path)
 
-template <typename InT, int C, int MODE>
-struct StripCfg;
-// u8 HWC: 16 bytes per thread
-template <int C>
-struct StripCfg<uint8_t, C, MODE_U8> {
-  static constexpr int NT = (C == 3) ? 192 : 128;
-  static constexpr int E = 16;
-};
-template <int C>
-struct StripCfg<float, C, MODE_F32> {
-  static constexpr int NT = (C == 3) ? 192 : 128;
-  static constexpr int E = 4;
-};
-template <int C>
-struct StripCfg<uint8_t, C, MODE_CHW> {
-  static constexpr int NT = (C == 3) ? 192 : 128;
-  static constexpr int E = 4 * C;
-};
+int resize_u8_fast(const uint8_t* src, int64_t s_is, int64_t s_rp, int sh, int sw, uint8_t* dst, int64_t d_is,
+                   int64_t d_rp, int dh, int dw, int c, int n, cudaStream_t st, bool* taken);
 
 static inline bool al16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
 
 template <typename InT, int C, int MODE>
 static int launch_strip(ResizeArgs a, int n, const LutArg& lut, cudaStream_t st, bool* launched) {
   using Cfg = StripCfg<InT, C, MODE>;
-  constexpr int NT = Cfg::NT, E = Cfg::E;
-  a.tile_px = NT * E / C;
+  a.tile_px = Cfg::TW_PX;
   a.tiles_x = (a.dw + a.tile_px - 1) / a.tile_px;
   // source footprint of one tile, upper bound: tile_px * scale_x + 3 px
   const double fp = (double)a.tile_px * a.scale_x;
   const int64_t fp_px = std::min<int64_t>((int64_t)fp + 3, (int64_t)a.sw);
   const int64_t slot = ((fp_px * C * (int64_t)sizeof(InT) + 16 + 15) / 16) * 16;
+  // band height 16..64 rows, aiming at >= 8 CTAs per SM over the whole batch
+  const int64_t rows_total = (int64_t)a.dh * a.tiles_x * n;
+  a.band_rows = (int)std::max<int64_t>(16, std::min<int64_t>(64, rows_total / (8 * 148)));
   const int lut_bytes = MODE == MODE_CHW ? C * 256 * 4 : 0;
-  const int64_t smem = 64 + lut_bytes + RING * slot;
+  const int64_t smem = 16 * Cfg::RING + 16 * a.band_rows + lut_bytes + Cfg::RING * slot;
   if (smem > kMaxStripSmem) return FV_OK;  // not eligible: caller falls back to gather
   a.slot_bytes = (int)slot;
-  // band height 8..64 rows, aiming at >= 8 CTAs per SM over the whole batch
-  const int64_t rows_total = (int64_t)a.dh * a.tiles_x * n;
-  a.band_rows = (int)std::max<int64_t>(8, std::min<int64_t>(64, rows_total / (8 * 148)));
   const int bands = (a.dh + a.band_rows - 1) / a.band_rows;
-  auto kern = resize_strip_kernel<InT, C, E, MODE, NT>;
+  auto kern = resize_strip_kernel<InT, C, MODE>;
   static bool attr_set = false;
   if (!attr_set) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxStripSmem);
     attr_set = true;
   }
   dim3 grid(a.tiles_x, bands, n);
-  kern<<<grid, NT, (size_t)smem, st>>>(a, lut);
+  kern<<<grid, Cfg::NT, (size_t)smem, st>>>(a, lut);
   *launched = true;
   return check_launch("resize_strip_kernel");
 }
@@ -366,7 +352,7 @@ template <typename InT, int MODE>
 static int launch_resize(ResizeArgs a, int n, const LutArg& lut, cudaStream_t st) {
   const bool src_al = al16(a.src) && (a.s_is & 15) == 0 && (a.s_rp & 15) == 0;
   bool launched = false;
-  if (g_resize_path == 0 && src_al && a.c >= 1 && a.c <= 4) {
+  if (g_resize_path != 1 && src_al && a.c >= 1 && a.c <= 4) {
     int rc = FV_OK;
     switch (a.c) {
       case 1: rc = launch_strip<InT, 1, MODE>(a, n, lut, st, &launched); break;
@@ -408,7 +394,7 @@ static ResizeArgs make_args(const void* src, int64_t s_is, int64_t s_rp, int sh,
   a.c = c;
   a.scale_x = (double)sw / (double)dw;  // imgproc.py:77, IEEE f64 division
   a.scale_y = (double)sh / (double)dh;
-  const bool dst_al = al16(dst) && (d_is & 15) == 0 && (d_rp & 15) == 0 && (d_ps & 15) == 0;
+  const bool dst_al = (reinterpret_cast<uintptr_t>(dst) & 3) == 0 && (d_is & 3) == 0 && (d_rp & 3) == 0;
   a.vec_store = dst_al ? 1 : 0;
   (void)out_elem;
   return a;
@@ -436,6 +422,12 @@ int fv_resize_bilinear_u8(const uint8_t* src, int64_t s_is, int64_t s_rp, int32_
                           int64_t d_is, int64_t d_rp, int32_t dh, int32_t dw, int32_t c, int32_t n, void* stream) {
   int rc = check_resize(src, dst, n, sh, sw, dh, dw, c, "fv_resize_bilinear_u8");
   if (rc || n == 0) return rc;
+  if (g_resize_path == 0) {  // exact 2:1 / 1:2 fast paths (fv_resize_fast.cu)
+    bool taken = false;
+    rc = resize_u8_fast(src, s_is, s_rp, sh, sw, dst, d_is, d_rp, dh, dw, c, n, static_cast<cudaStream_t>(stream),
+                        &taken);
+    if (rc || taken) return rc;
+  }
   ResizeArgs a = make_args(src, s_is, s_rp, sh, sw, dst, d_is, d_rp, 0, dh, dw, c, 1);
   static LutArg none;
   return launch_resize<uint8_t, MODE_U8>(a, n, none, static_cast<cudaStream_t>(stream));

@@ -44,7 +44,7 @@ def assert_exact(got, ref):
         pytest.fail(f"{len(bad)} elements differ (within gate), first at {bad[0].tolist()}")
 
 
-@pytest.fixture(params=[0, 1], ids=["strip", "gather"])
+@pytest.fixture(params=[0, 1, 2], ids=["auto", "gather", "strip"])
 def resize_path(request):
     _native.lib().fv_set_resize_path(request.param)
     yield request.param
@@ -170,6 +170,20 @@ class TestResize:
         expect = np.stack([O.resize_u8(parent[i, 3:41, 5:74], 60, 25) for i in range(3)])
         assert_exact(host(dst), expect)
         assert not host(dst_parent)[:, :2].any()  # nothing written outside the view
+
+    @pytest.mark.parametrize("c", [1, 3, 4])
+    @pytest.mark.parametrize("geom", [(74, 10, 37, 5), (128, 70, 64, 35), (12, 5, 24, 10), (40, 70, 80, 140),
+                                      (8, 1, 16, 2), (2, 2, 1, 1)])
+    def test_u8_integer_ratio_paths(self, resize_path, rng, c, geom):
+        """Exact 2:1 / 1:2 shapes (fast paths under 'auto'): ragged tail groups,
+        band boundaries (>32 source rows), 1-row sources, batches."""
+        sw, sh, dw, dh = geom
+        a = rng.integers(0, 256, (2, sh, sw, c), dtype=np.uint8)
+        dst = torch.zeros((2, dh, dw, c), dtype=torch.uint8, device=DEV)
+        fv.resize_bilinear_u8(cu(a), dst)
+        out = host(dst)
+        for i in range(2):
+            assert_exact(out[i], O.resize_u8(a[i], dw, dh))
 
     def test_cfg1_downscale_full_image(self):
         a = synth.seeded_u8_image(3840, 2160, 3, seed=synth.SEED_RESIZE)
