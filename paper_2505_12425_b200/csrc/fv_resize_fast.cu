@@ -113,11 +113,10 @@ struct Up2 {
   static constexpr int NW = (4 + 5 * C + 3) / 4;   // source words per row window [4Ct-4, ...)
 };
 
-// h for the thread's 8 destination pixels from one source row
+// the thread's source window of one row: bytes [4Ct - 4, 4Ct + 5C) as words
 template <int C>
-__device__ __forceinline__ void up2_row(const uint8_t* row, int t, int last_t, int sw, float (&h)[8 * C]) {
+__device__ __forceinline__ void up2_load(const uint8_t* row, int t, int sw, uint32_t (&w)[Up2<C>::NW]) {
   constexpr int NW = Up2<C>::NW;
-  uint32_t w[NW];
   const int ws = 4 * C * t - 4;  // window start byte (4-aligned)
   const uint32_t* rw = reinterpret_cast<const uint32_t*>(row + ws);
   const int row_bytes = sw * C;
@@ -126,6 +125,11 @@ __device__ __forceinline__ void up2_row(const uint8_t* row, int t, int last_t, i
     const int b = ws + 4 * i;
     w[i] = (b >= 0 && b < row_bytes) ? __ldg(rw + i) : 0u;
   }
+}
+
+// h for the thread's 8 destination pixels from one source row's window
+template <int C>
+__device__ __forceinline__ void up2_h(const uint32_t (&w)[Up2<C>::NW], int t, int last_t, float (&h)[8 * C]) {
   // v[m] for source pixels m = -1..4 relative to 4t, byte offset 4 + C*m in the window
   float P[4 * C];
 #pragma unroll
@@ -182,14 +186,17 @@ __device__ __forceinline__ void up2_emit_copy(uint8_t* drow, const float (&h)[8 
   }
 }
 
-// Source row k: hn = h_k from the row, then destination rows
+// Source row k (window wc already loaded): hn = h_k, prefetch row k+1 into
+// wn, then destination rows
 //   2k-1 = fma(h_k, 0.25, Q_{k-1})   (rows k-1 @ 0.75, k @ 0.25)
 //   2k   = fma(h_{k-1}, 0.25, Q_k)   (rows k-1 @ 0.25, k @ 0.75)
 // q holds Q_{k-1} on entry and Q_k on exit; hp = h_{k-1}.
 template <int C>
-__device__ __forceinline__ void up2_step(const uint8_t* img, uint8_t* dimg, const FastArgs& a, int t, int k,
+__device__ __forceinline__ void up2_step(const uint8_t* img, uint8_t* dimg, const FastArgs& a, int t, int k, int k1,
+                                         const uint32_t (&wc)[Up2<C>::NW], uint32_t (&wn)[Up2<C>::NW],
                                          const float (&hp)[8 * C], float (&q)[8 * C], float (&hn)[8 * C]) {
-  up2_row<C>(img + (int64_t)k * a.s_rp, t, a.groups - 1, a.sw, hn);
+  up2_h<C>(wc, t, a.groups - 1, hn);
+  if (k + 1 < k1) up2_load<C>(img + (int64_t)(k + 1) * a.s_rp, t, a.sw, wn);
   if (k == 0) {
     up2_emit_copy<C>(dimg, hn);
   } else {
@@ -202,7 +209,7 @@ __device__ __forceinline__ void up2_step(const uint8_t* img, uint8_t* dimg, cons
 
 template <int C>
 __global__ void __launch_bounds__(128, 4) resize_up2_kernel(const __grid_constant__ FastArgs a) {
-  constexpr int E = Up2<C>::E;
+  constexpr int E = Up2<C>::E, NW = Up2<C>::NW;
   const int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int64_t total = (int64_t)a.n * a.bands * a.groups;
   if (gid >= total) return;
@@ -215,21 +222,26 @@ __global__ void __launch_bounds__(128, 4) resize_up2_kernel(const __grid_constan
   const uint8_t* img = a.src + n * a.s_is;
   uint8_t* dimg = a.dst + n * a.d_is + t * 8 * C;
 
-  // two h buffers used alternately (no register copies between rows)
+  // two h buffers and two source windows used alternately (no register copies)
   float h0[E], h1[E], q[E];
+  uint32_t w0[NW], w1[NW];
   if (k0 > 0) {
-    up2_row<C>(img + (int64_t)(k0 - 1) * a.s_rp, t, a.groups - 1, a.sw, h0);
+    up2_load<C>(img + (int64_t)(k0 - 1) * a.s_rp, t, a.sw, w1);
+    up2_load<C>(img + (int64_t)k0 * a.s_rp, t, a.sw, w0);
+    up2_h<C>(w1, t, a.groups - 1, h0);
 #pragma unroll
     for (int e = 0; e < E; ++e) q[e] = __fmul_rn(h0[e], 0.75f);
+  } else {
+    up2_load<C>(img, t, a.sw, w0);
   }
   int k = k0;
 #pragma unroll 1
   for (; k + 1 < k1; k += 2) {
-    up2_step<C>(img, dimg, a, t, k, h0, q, h1);
-    up2_step<C>(img, dimg, a, t, k + 1, h1, q, h0);
+    up2_step<C>(img, dimg, a, t, k, k1, w0, w1, h0, q, h1);
+    up2_step<C>(img, dimg, a, t, k + 1, k1, w1, w0, h1, q, h0);
   }
   if (k < k1) {
-    up2_step<C>(img, dimg, a, t, k, h0, q, h1);
+    up2_step<C>(img, dimg, a, t, k, k1, w0, w1, h0, q, h1);
     if (k1 == a.sh) up2_emit_copy<C>(dimg + (int64_t)(2 * a.sh - 1) * a.d_rp, h1);
   } else if (k1 == a.sh) {
     up2_emit_copy<C>(dimg + (int64_t)(2 * a.sh - 1) * a.d_rp, h0);

@@ -35,64 +35,173 @@ struct WarpMats {
 };
 
 template <typename T>
-__device__ __forceinline__ void store_out(T* p, float v);
+__device__ __forceinline__ T to_out(float v);
 template <>
-__device__ __forceinline__ void store_out<float>(float* p, float v) {
-  *p = v;
+__device__ __forceinline__ float to_out<float>(float v) {
+  return v;
 }
 template <>
-__device__ __forceinline__ void store_out<uint8_t>(uint8_t* p, float v) {
-  *p = (uint8_t)unit_to_u8(v);
+__device__ __forceinline__ uint8_t to_out<uint8_t>(float v) {
+  return (uint8_t)unit_to_u8(v);
 }
 
-template <typename InT, bool PERSP>
-__global__ void __launch_bounds__(128) warp_kernel(const __grid_constant__ WarpArgs a,
+// Inverse map of destination pixel (x, y) and its bilinear taps.
+struct WarpTap {
+  int x0, y0;
+  float wx0, wx1, wy0, wy1;
+  bool finite;
+};
+
+template <bool PERSP>
+__device__ __forceinline__ WarpTap warp_tap(const double (&m)[9], double rx, double ry, double rw, int x, int sw,
+                                            int sh) {
+  WarpTap t;
+  const double xd = (double)x;
+  double sx = __dadd_rn(__dmul_rn(m[0], xd), rx);
+  double sy = __dadd_rn(__dmul_rn(m[3], xd), ry);
+  t.finite = true;
+  if (PERSP) {
+    const double w = __dadd_rn(__dmul_rn(m[6], xd), rw);
+    if (w == 0.0) {
+      t.finite = false;
+    } else {
+      const double r = __drcp_rn(w);
+      sx = __dmul_rn(sx, r);
+      sy = __dmul_rn(sy, r);
+    }
+  }
+  t.finite = t.finite && isfinite(sx) && isfinite(sy);
+  if (!t.finite) {
+    sx = 0.0;
+    sy = 0.0;
+  }
+  const double fx = floor(sx), fy = floor(sy);
+  t.wx1 = __double2float_rn(__dadd_rn(sx, -fx));
+  t.wy1 = __double2float_rn(__dadd_rn(sy, -fy));
+  t.wx0 = __fsub_rn(1.0f, t.wx1);
+  t.wy0 = __fsub_rn(1.0f, t.wy1);
+  // cvt.rmi saturates out-of-range values; clamping keeps every out-of-range
+  // tap out of range (the oracle clips the float the same way)
+  t.x0 = min(max(__double2int_rd(sx), -2), sw + 1);
+  t.y0 = min(max(__double2int_rd(sy), -2), sh + 1);
+  return t;
+}
+
+// Taps of the two source pixels (x0, x0+1) of one row, all C channels.
+// u8, C = 3, interior: three aligned 32-bit loads + two funnel shifts
+// instead of six byte loads.
+template <typename InT, int C>
+__device__ __forceinline__ void load_pair(const InT* row, int x0, int row_elems, float (&t0)[C], float (&t1)[C]) {
+  if constexpr (sizeof(InT) == 1 && C == 3) {
+    const uintptr_t p = reinterpret_cast<uintptr_t>(row) + 3 * x0;
+    const uintptr_t al = p & ~(uintptr_t)3;
+    if (al + 12 <= reinterpret_cast<uintptr_t>(row) + row_elems) {
+      const uint32_t* w = reinterpret_cast<const uint32_t*>(al);
+      const uint32_t w0 = __ldg(w), w1 = __ldg(w + 1), w2 = __ldg(w + 2);
+      const int sh = (int)(p & 3) * 8;
+      uint32_t v[2];
+      v[0] = __funnelshift_r(w0, w1, sh);
+      v[1] = __funnelshift_r(w1, w2, sh);
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        t0[c] = unit_of(v, c);
+        t1[c] = unit_of(v, 3 + c);
+      }
+      return;
+    }
+  }
+#pragma unroll
+  for (int c = 0; c < C; ++c) {
+    t0[c] = tap_value(__ldg(row + x0 * C + c));
+    t1[c] = tap_value(__ldg(row + (x0 + 1) * C + c));
+  }
+}
+
+// Fixed-C kernel (C = 1, 3, 4): a 32 x 8 tile of destination pixels per CTA,
+// one pixel per thread. The row terms m1*y + m2 etc. are computed once per
+// thread; interior pixels (all four taps inside) take unguarded loads.
+template <typename InT, bool PERSP, int C>
+__global__ void __launch_bounds__(256) warp_kernel(const __grid_constant__ WarpArgs a,
                                                    const __grid_constant__ WarpMats mats) {
   const int n = blockIdx.z;
-  const int x = blockIdx.x * blockDim.x + threadIdx.x;
-  if (x >= a.dw) return;
-  const double* m = mats.m[n];
-  const double xd = (double)x;
-  for (int y = blockIdx.y; y < a.dh; y += gridDim.y) {
-    const double yd = (double)y;
-    double sx = __dadd_rn(__dmul_rn(m[0], xd), __dadd_rn(__dmul_rn(m[1], yd), m[2]));
-    double sy = __dadd_rn(__dmul_rn(m[3], xd), __dadd_rn(__dmul_rn(m[4], yd), m[5]));
-    bool finite = true;
-    if (PERSP) {
-      const double w = __dadd_rn(__dmul_rn(m[6], xd), __dadd_rn(__dmul_rn(m[7], yd), m[8]));
-      if (w == 0.0) {
-        finite = false;
-      } else {
-        const double r = __drcp_rn(w);
-        sx = __dmul_rn(sx, r);
-        sy = __dmul_rn(sy, r);
-      }
+  const int x = blockIdx.x * 32 + threadIdx.x;
+  const int y = blockIdx.y * 8 + threadIdx.y;
+  if (x >= a.dw || y >= a.dh) return;
+  double m[9];
+#pragma unroll
+  for (int i = 0; i < 9; ++i) m[i] = mats.m[n][i];
+  const double yd = (double)y;
+  const double rx = __dadd_rn(__dmul_rn(m[1], yd), m[2]);
+  const double ry = __dadd_rn(__dmul_rn(m[4], yd), m[5]);
+  const double rw = PERSP ? __dadd_rn(__dmul_rn(m[7], yd), m[8]) : 0.0;
+  const WarpTap t = warp_tap<PERSP>(m, rx, ry, rw, x, a.sw, a.sh);
+  InT* d = row_ptr_mut<InT>(a.dst, a.d_is, a.d_rp, n, y) + x * C;
+  if (!t.finite) {
+#pragma unroll
+    for (int c = 0; c < C; ++c) d[c] = (InT)a.border_raw;
+    return;
+  }
+  float t00[C], t01[C], t10[C], t11[C];
+  const bool inx = t.x0 >= 0 && t.x0 + 1 < a.sw, iny = t.y0 >= 0 && t.y0 + 1 < a.sh;
+  if (inx && iny) {
+    const InT* r0 = row_ptr<InT>(a.src, a.s_is, a.s_rp, n, t.y0);
+    const InT* r1 = row_ptr<InT>(a.src, a.s_is, a.s_rp, n, t.y0 + 1);
+    load_pair<InT, C>(r0, t.x0, a.sw * C, t00, t01);
+    load_pair<InT, C>(r1, t.x0, a.sw * C, t10, t11);
+  } else {
+    const bool ix0 = t.x0 >= 0 && t.x0 < a.sw, ix1 = t.x0 + 1 >= 0 && t.x0 + 1 < a.sw;
+    const bool iy0 = t.y0 >= 0 && t.y0 < a.sh, iy1 = t.y0 + 1 >= 0 && t.y0 + 1 < a.sh;
+    const InT* r0 = row_ptr<InT>(a.src, a.s_is, a.s_rp, n, iy0 ? t.y0 : 0);
+    const InT* r1 = row_ptr<InT>(a.src, a.s_is, a.s_rp, n, iy1 ? t.y0 + 1 : 0);
+#pragma unroll
+    for (int c = 0; c < C; ++c) {
+      t00[c] = (iy0 && ix0) ? tap_value(__ldg(r0 + t.x0 * C + c)) : a.border_f;
+      t01[c] = (iy0 && ix1) ? tap_value(__ldg(r0 + (t.x0 + 1) * C + c)) : a.border_f;
+      t10[c] = (iy1 && ix0) ? tap_value(__ldg(r1 + t.x0 * C + c)) : a.border_f;
+      t11[c] = (iy1 && ix1) ? tap_value(__ldg(r1 + (t.x0 + 1) * C + c)) : a.border_f;
     }
-    finite = finite && isfinite(sx) && isfinite(sy);
-    InT* d = row_ptr_mut<InT>(a.dst, a.d_is, a.d_rp, n, y) + x * a.c;
-    if (!finite) {
-      for (int ch = 0; ch < a.c; ++ch) d[ch] = (InT)a.border_raw;
-      continue;
-    }
-    const double x0f = floor(sx), y0f = floor(sy);
-    const float wx1 = __double2float_rn(__dadd_rn(sx, -x0f));
-    const float wy1 = __double2float_rn(__dadd_rn(sy, -y0f));
-    const float wx0 = __fsub_rn(1.0f, wx1), wy0 = __fsub_rn(1.0f, wy1);
-    const int x0 = (int)fmin(fmax(x0f, -2.0), (double)a.sw + 1.0);
-    const int y0 = (int)fmin(fmax(y0f, -2.0), (double)a.sh + 1.0);
-    const bool ix0 = x0 >= 0 && x0 < a.sw, ix1 = x0 + 1 >= 0 && x0 + 1 < a.sw;
-    const bool iy0 = y0 >= 0 && y0 < a.sh, iy1 = y0 + 1 >= 0 && y0 + 1 < a.sh;
-    const InT* r0 = iy0 ? row_ptr<InT>(a.src, a.s_is, a.s_rp, n, y0) : nullptr;
-    const InT* r1 = iy1 ? row_ptr<InT>(a.src, a.s_is, a.s_rp, n, y0 + 1) : nullptr;
-    for (int ch = 0; ch < a.c; ++ch) {
-      const float t00 = (iy0 && ix0) ? tap_value(__ldg(r0 + x0 * a.c + ch)) : a.border_f;
-      const float t01 = (iy0 && ix1) ? tap_value(__ldg(r0 + (x0 + 1) * a.c + ch)) : a.border_f;
-      const float t10 = (iy1 && ix0) ? tap_value(__ldg(r1 + x0 * a.c + ch)) : a.border_f;
-      const float t11 = (iy1 && ix1) ? tap_value(__ldg(r1 + (x0 + 1) * a.c + ch)) : a.border_f;
-      const float top = lerp_ref(t00, t01, wx0, wx1);
-      const float bot = lerp_ref(t10, t11, wx0, wx1);
-      store_out<InT>(d + ch, lerp_ref(top, bot, wy0, wy1));
-    }
+  }
+#pragma unroll
+  for (int c = 0; c < C; ++c) {
+    const float top = lerp_ref(t00[c], t01[c], t.wx0, t.wx1);
+    const float bot = lerp_ref(t10[c], t11[c], t.wx0, t.wx1);
+    d[c] = to_out<InT>(lerp_ref(top, bot, t.wy0, t.wy1));
+  }
+}
+
+// Any channel count: same sampler, channel loop at run time.
+template <typename InT, bool PERSP>
+__global__ void __launch_bounds__(256) warp_kernel_any(const __grid_constant__ WarpArgs a,
+                                                       const __grid_constant__ WarpMats mats) {
+  const int n = blockIdx.z;
+  const int x = blockIdx.x * 32 + threadIdx.x;
+  const int y = blockIdx.y * 8 + threadIdx.y;
+  if (x >= a.dw || y >= a.dh) return;
+  double m[9];
+#pragma unroll
+  for (int i = 0; i < 9; ++i) m[i] = mats.m[n][i];
+  const double yd = (double)y;
+  const double rx = __dadd_rn(__dmul_rn(m[1], yd), m[2]);
+  const double ry = __dadd_rn(__dmul_rn(m[4], yd), m[5]);
+  const double rw = PERSP ? __dadd_rn(__dmul_rn(m[7], yd), m[8]) : 0.0;
+  const WarpTap t = warp_tap<PERSP>(m, rx, ry, rw, x, a.sw, a.sh);
+  InT* d = row_ptr_mut<InT>(a.dst, a.d_is, a.d_rp, n, y) + x * a.c;
+  if (!t.finite) {
+    for (int c = 0; c < a.c; ++c) d[c] = (InT)a.border_raw;
+    return;
+  }
+  const bool ix0 = t.x0 >= 0 && t.x0 < a.sw, ix1 = t.x0 + 1 >= 0 && t.x0 + 1 < a.sw;
+  const bool iy0 = t.y0 >= 0 && t.y0 < a.sh, iy1 = t.y0 + 1 >= 0 && t.y0 + 1 < a.sh;
+  const InT* r0 = row_ptr<InT>(a.src, a.s_is, a.s_rp, n, iy0 ? t.y0 : 0);
+  const InT* r1 = row_ptr<InT>(a.src, a.s_is, a.s_rp, n, iy1 ? t.y0 + 1 : 0);
+  for (int c = 0; c < a.c; ++c) {
+    const float t00 = (iy0 && ix0) ? tap_value(__ldg(r0 + t.x0 * a.c + c)) : a.border_f;
+    const float t01 = (iy0 && ix1) ? tap_value(__ldg(r0 + (t.x0 + 1) * a.c + c)) : a.border_f;
+    const float t10 = (iy1 && ix0) ? tap_value(__ldg(r1 + t.x0 * a.c + c)) : a.border_f;
+    const float t11 = (iy1 && ix1) ? tap_value(__ldg(r1 + (t.x0 + 1) * a.c + c)) : a.border_f;
+    const float top = lerp_ref(t00, t01, t.wx0, t.wx1);
+    const float bot = lerp_ref(t10, t11, t.wx0, t.wx1);
+    d[c] = to_out<InT>(lerp_ref(top, bot, t.wy0, t.wy1));
   }
 }
 
@@ -102,6 +211,7 @@ static int launch_warp(const InT* src, int64_t s_is, int64_t s_rp, int sh, int s
                        float border_f, float border_raw, cudaStream_t st, const char* fn) {
   if (n < 0 || sh < 1 || sw < 1 || dh < 1 || dw < 1 || c < 1)
     return set_error(FV_EINVAL, "%s: bad shape n=%d src=%dx%d dst=%dx%d c=%d", fn, n, sh, sw, dh, dw, c);
+  if ((int64_t)(dh + 7) / 8 > 65535) return set_error(FV_EINVAL, "%s: destination height %d too large", fn, dh);
   if (n == 0) return FV_OK;
   if (!src || !dst || !mats_host) return set_error(FV_EINVAL, "%s: null pointer", fn);
   if (sizeof(InT) == 4 && ((s_is | s_rp | d_is | d_rp) & 3))
@@ -125,9 +235,14 @@ static int launch_warp(const InT* src, int64_t s_is, int64_t s_rp, int sh, int s
       for (int j = 0; j < 9; ++j) mats.m[i][j] = j < mat_len ? mats_host[(int64_t)(b + i) * mat_len + j] : 0.0;
     a.src = reinterpret_cast<const char*>(src) + (int64_t)b * s_is;
     a.dst = reinterpret_cast<char*>(dst) + (int64_t)b * d_is;
-    const int gy = dh < 65535 ? dh : 65535;
-    dim3 grid((dw + 127) / 128, gy, nb);
-    warp_kernel<InT, PERSP><<<grid, 128, 0, st>>>(a, mats);
+    dim3 grid((dw + 31) / 32, (dh + 7) / 8, nb);
+    dim3 block(32, 8);
+    switch (c) {
+      case 1: warp_kernel<InT, PERSP, 1><<<grid, block, 0, st>>>(a, mats); break;
+      case 3: warp_kernel<InT, PERSP, 3><<<grid, block, 0, st>>>(a, mats); break;
+      case 4: warp_kernel<InT, PERSP, 4><<<grid, block, 0, st>>>(a, mats); break;
+      default: warp_kernel_any<InT, PERSP><<<grid, block, 0, st>>>(a, mats); break;
+    }
     int rc = check_launch(fn);
     if (rc) return rc;
   }
