@@ -77,6 +77,82 @@ __device__ __forceinline__ float unit_of(const uint32_t (&w)[N], int i) {
   return __fmaf_rn(f, RHI, __fmul_rn(f, RLO));
 }
 
+// ---------------------------------------------------------------------------
+// Packed f32x2 arithmetic (sm_100: FADD2 / FMUL2 / FFMA2, two IEEE f32 ops per
+// instruction, each lane rounded separately).
+//
+// CAUTION (ptxas 12.9): for .f32x2 ptxas contracts a mul.rn whose result is
+// a MULTIPLICAND or a plain ADD operand into an FFMA2, ignoring the explicit
+// rounding modifier (and -fmad=false). Only these shapes are used here:
+//   * mul2 result as the ADDEND of an explicit fma2 (cannot be contracted:
+//     the fma already has a product);
+//   * add2 whose operands are not bare products;
+//   * RN(y + 0.5) of a product y written as fma2(y, one, 0.5) with `one` a
+//     RUNTIME 1.0 (kernel argument), so ptxas cannot fold the product in.
+// tests/test_gpu_parity.py checks every kernel bit-exactly at config sizes.
+// ---------------------------------------------------------------------------
+typedef unsigned long long f2_t;
+
+__device__ __forceinline__ f2_t f2(float lo, float hi) {
+  f2_t r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
+  return r;
+}
+__device__ __forceinline__ f2_t f2u(uint32_t lo, uint32_t hi) {
+  f2_t r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "r"(lo), "r"(hi));
+  return r;
+}
+__device__ __forceinline__ void f2split(f2_t v, uint32_t& lo, uint32_t& hi) {
+  asm("mov.b64 {%0, %1}, %2;" : "=r"(lo), "=r"(hi) : "l"(v));
+}
+__device__ __forceinline__ f2_t fmul2(f2_t a, f2_t b) {
+  f2_t r;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+__device__ __forceinline__ f2_t ffma2(f2_t a, f2_t b, f2_t c) {
+  f2_t r;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
+  return r;
+}
+__device__ __forceinline__ f2_t fadd2(f2_t a, f2_t b) {
+  f2_t r;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+__device__ __forceinline__ f2_t fadd2_rd(f2_t a, f2_t b) {
+  f2_t r;
+  asm("add.rm.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+// two u8_to_unit at once from two magic words 0x4B0000uu
+__device__ __forceinline__ f2_t unit2(uint32_t m_lo, uint32_t m_hi) {
+  const float RHI = __uint_as_float(0x3B808081u);
+  const float RLO = __uint_as_float(0xAF7EFEFFu);
+  const f2_t f = fadd2(f2u(m_lo, m_hi), f2(-8388608.0f, -8388608.0f));
+  return ffma2(f, f2(RHI, RHI), fmul2(f, f2(RLO, RLO)));
+}
+// magic word 0x4B0000uu of byte i of a word array (see unit_of)
+template <int N>
+__device__ __forceinline__ uint32_t magic_of(const uint32_t (&w)[N], int i) {
+  return __byte_perm(w[i >> 2], 0x4B000000u, 0x7440 + (i & 3));
+}
+// y = RN(v * scale) then the u8 epilogue; returns the two float-bit words
+// whose low bytes are the results. `one` must be a runtime 1.0f.
+__device__ __forceinline__ f2_t scale_to_u8_bits2(f2_t v, float scale, float one) {
+  const f2_t y = fmul2(v, f2(scale, scale));
+  const f2_t t = ffma2(y, f2(one, one), f2(0.5f, 0.5f));
+  return fadd2_rd(t, f2(8388608.0f, 8388608.0f));
+}
+// low bytes of two pairs -> one word
+__device__ __forceinline__ uint32_t pack4x2(f2_t a, f2_t b) {
+  uint32_t a0, a1, b0, b1;
+  f2split(a, a0, a1);
+  f2split(b, b0, b1);
+  return pack4(a0, a1, b0, b1);
+}
+
 // Same as unit_to_u8 but with explicit saturation; used where the input is
 // not a convex blend of unit values.
 __device__ __forceinline__ uint32_t unit_to_u8_sat(float v) {

@@ -37,6 +37,8 @@ struct FastArgs {
   int groups;  // column groups per row
   int band;    // up2: source rows per band
   int bands;
+  float one;   // runtime 1.0f (see fv_common.cuh: f32x2 contraction guard)
+  int slot_bytes;
 };
 
 // ---------------------------------------------------------------------------
@@ -72,20 +74,23 @@ __global__ void __launch_bounds__(128) resize_down2_kernel(const __grid_constant
       const uint4 v = __ldg(s1 + i);
       w1[4 * i] = v.x, w1[4 * i + 1] = v.y, w1[4 * i + 2] = v.z, w1[4 * i + 3] = v.w;
     }
+    // element pairs (e, e+1) in packed f32x2: 4 taps, 3 adds, epilogue
     uint32_t out[4 * C];
 #pragma unroll
     for (int q = 0; q < 4 * C; ++q) {
-      uint32_t b[4];
+      f2_t r[2];
 #pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        const int e = 4 * q + j;            // destination byte in the group
-        const int p = e / C, c = e % C;     // pixel, channel
-        const int o = 2 * p * C + c;        // first tap byte in the window
-        const float top = __fadd_rn(unit_of(w0, o), unit_of(w0, o + C));
-        const float bot = __fadd_rn(unit_of(w1, o), unit_of(w1, o + C));
-        b[j] = scaled_to_u8_bits(__fmul_rn(__fadd_rn(top, bot), K));
+      for (int j = 0; j < 2; ++j) {
+        const int e0 = 4 * q + 2 * j, e1 = e0 + 1;  // destination bytes in the group
+        const int o0 = 2 * (e0 / C) * C + e0 % C;   // first tap byte of each
+        const int o1 = 2 * (e1 / C) * C + e1 % C;
+        const f2_t top = fadd2(unit2(magic_of(w0, o0), magic_of(w0, o1)),
+                               unit2(magic_of(w0, o0 + C), magic_of(w0, o1 + C)));
+        const f2_t bot = fadd2(unit2(magic_of(w1, o0), magic_of(w1, o1)),
+                               unit2(magic_of(w1, o0 + C), magic_of(w1, o1 + C)));
+        r[j] = scale_to_u8_bits2(fadd2(top, bot), K, a.one);
       }
-      out[q] = pack4(b[0], b[1], b[2], b[3]);
+      out[q] = pack4x2(r[0], r[1]);
     }
     uint4* dv = reinterpret_cast<uint4*>(d + px0 * C);
 #pragma unroll
@@ -113,138 +118,189 @@ struct Up2 {
   static constexpr int NW = (4 + 5 * C + 3) / 4;   // source words per row window [4Ct-4, ...)
 };
 
-// the thread's source window of one row: bytes [4Ct - 4, 4Ct + 5C) as words
+// h for the thread's 8 destination pixels from one source row's window, as
+// E/2 packed pairs of consecutive destination elements
 template <int C>
-__device__ __forceinline__ void up2_load(const uint8_t* row, int t, int sw, uint32_t (&w)[Up2<C>::NW]) {
-  constexpr int NW = Up2<C>::NW;
-  const int ws = 4 * C * t - 4;  // window start byte (4-aligned)
-  const uint32_t* rw = reinterpret_cast<const uint32_t*>(row + ws);
-  const int row_bytes = sw * C;
+__device__ __forceinline__ void up2_h(const uint32_t (&w)[Up2<C>::NW], int t, int last_t, f2_t (&h)[4 * C]) {
+  // v for source pixels m = -1..4 relative to 4t (window bytes 4-C .. 4+5C-1),
+  // converted two at a time
+  float v[6 * C];
 #pragma unroll
-  for (int i = 0; i < NW; ++i) {
-    const int b = ws + 4 * i;
-    w[i] = (b >= 0 && b < row_bytes) ? __ldg(rw + i) : 0u;
+  for (int j = 0; j < 6 * C; j += 2) {
+    uint32_t lo, hi;
+    f2split(unit2(magic_of(w, 4 - C + j), magic_of(w, 4 - C + j + 1)), lo, hi);
+    v[j] = __uint_as_float(lo);
+    v[j + 1] = __uint_as_float(hi);
   }
-}
-
-// h for the thread's 8 destination pixels from one source row's window
-template <int C>
-__device__ __forceinline__ void up2_h(const uint32_t (&w)[Up2<C>::NW], int t, int last_t, float (&h)[8 * C]) {
-  // v[m] for source pixels m = -1..4 relative to 4t, byte offset 4 + C*m in the window
+  // v[m][c] = v[(m + 1) * C + c]
   float P[4 * C];
 #pragma unroll
-  for (int m = 0; m < 4; ++m)
-#pragma unroll
-    for (int c = 0; c < C; ++c) P[m * C + c] = __fmul_rn(unit_of(w, 4 + C * m + c), 0.75f);
+  for (int i = 0; i < 4 * C; ++i) P[i] = __fmul_rn(v[C + i], 0.75f);
+  float hs[8 * C];
 #pragma unroll
   for (int m = 0; m < 4; ++m)
 #pragma unroll
     for (int c = 0; c < C; ++c) {
-      h[(2 * m) * C + c] = __fmaf_rn(unit_of(w, 4 + C * (m - 1) + c), 0.25f, P[m * C + c]);
-      h[(2 * m + 1) * C + c] = __fmaf_rn(unit_of(w, 4 + C * (m + 1) + c), 0.25f, P[m * C + c]);
+      hs[(2 * m) * C + c] = __fmaf_rn(v[m * C + c], 0.25f, P[m * C + c]);
+      hs[(2 * m + 1) * C + c] = __fmaf_rn(v[(m + 2) * C + c], 0.25f, P[m * C + c]);
     }
   if (t == 0) {  // destination pixel 0: clamped, fx = 0 -> copy
 #pragma unroll
-    for (int c = 0; c < C; ++c) h[c] = unit_of(w, 4 + c);
+    for (int c = 0; c < C; ++c) hs[c] = v[C + c];
   }
   if (t == last_t) {  // destination pixel 2W-1: clamped, fx = 0 -> copy
 #pragma unroll
-    for (int c = 0; c < C; ++c) h[7 * C + c] = unit_of(w, 4 + 3 * C + c);
+    for (int c = 0; c < C; ++c) hs[7 * C + c] = v[4 * C + c];
   }
+#pragma unroll
+  for (int i = 0; i < 4 * C; ++i) h[i] = f2(hs[2 * i], hs[2 * i + 1]);
 }
 
-// one destination row from two h rows: o = fma(hb, 0.25, qa) per element,
-// packed 4 bytes at a time and written as 8-byte stores (8*C bytes)
+// one destination row from two h rows: o = fma(hb, 0.25, qa), epilogue in
+// f32x2, packed 4 bytes at a time and written as 8-byte stores (8*C bytes)
 template <int C>
-__device__ __forceinline__ void up2_emit(uint8_t* drow, const float (&hb)[8 * C], const float (&qa)[8 * C]) {
+__device__ __forceinline__ void up2_emit(uint8_t* drow, const f2_t (&hb)[4 * C], const f2_t (&qa)[4 * C], float one) {
 #pragma unroll
   for (int i = 0; i < C; ++i) {
     uint32_t w[2];
 #pragma unroll
     for (int j = 0; j < 2; ++j) {
-      const int e = 8 * i + 4 * j;
-      w[j] = pack4(unit_to_u8_bits(__fmaf_rn(hb[e], 0.25f, qa[e])), unit_to_u8_bits(__fmaf_rn(hb[e + 1], 0.25f, qa[e + 1])),
-                   unit_to_u8_bits(__fmaf_rn(hb[e + 2], 0.25f, qa[e + 2])),
-                   unit_to_u8_bits(__fmaf_rn(hb[e + 3], 0.25f, qa[e + 3])));
+      const int e = 4 * i + 2 * j;  // pair index
+      const f2_t r0 = scale_to_u8_bits2(ffma2(hb[e], f2(0.25f, 0.25f), qa[e]), 255.0f, one);
+      const f2_t r1 = scale_to_u8_bits2(ffma2(hb[e + 1], f2(0.25f, 0.25f), qa[e + 1]), 255.0f, one);
+      w[j] = pack4x2(r0, r1);
     }
     __stcs(reinterpret_cast<uint2*>(drow) + i, make_uint2(w[0], w[1]));
   }
 }
 // a row that is a plain copy of h (clamped rows 0 and 2H-1, fy = 0)
 template <int C>
-__device__ __forceinline__ void up2_emit_copy(uint8_t* drow, const float (&h)[8 * C]) {
+__device__ __forceinline__ void up2_emit_copy(uint8_t* drow, const f2_t (&h)[4 * C], float one) {
 #pragma unroll
   for (int i = 0; i < C; ++i) {
     uint32_t w[2];
 #pragma unroll
     for (int j = 0; j < 2; ++j) {
-      const int e = 8 * i + 4 * j;
-      w[j] = pack4(unit_to_u8_bits(h[e]), unit_to_u8_bits(h[e + 1]), unit_to_u8_bits(h[e + 2]),
-                   unit_to_u8_bits(h[e + 3]));
+      const int e = 4 * i + 2 * j;
+      w[j] = pack4x2(scale_to_u8_bits2(h[e], 255.0f, one), scale_to_u8_bits2(h[e + 1], 255.0f, one));
     }
     __stcs(reinterpret_cast<uint2*>(drow) + i, make_uint2(w[0], w[1]));
   }
 }
 
-// Source row k (window wc already loaded): hn = h_k, prefetch row k+1 into
-// wn, then destination rows
-//   2k-1 = fma(h_k, 0.25, Q_{k-1})   (rows k-1 @ 0.75, k @ 0.25)
-//   2k   = fma(h_{k-1}, 0.25, Q_k)   (rows k-1 @ 0.25, k @ 0.75)
-// q holds Q_{k-1} on entry and Q_k on exit; hp = h_{k-1}.
+// TMA-staged variant: a CTA = 4 consumer warps (128 column groups = 512
+// source pixels) + 1 producer warp. The producer streams the band's source
+// row segments into an UP2_RING-slot shared-memory ring with 1-D bulk copies
+// (cp.async.bulk, completion on the slot's "full" mbarrier); consumers read
+// their 4-byte aligned windows with LDS (lane stride 12 B: conflict-free) and
+// release the slot on its "empty" mbarrier.
+constexpr int UP2_NCW = 4, UP2_GROUPS = UP2_NCW * 32, UP2_RING = 8;
+
 template <int C>
-__device__ __forceinline__ void up2_step(const uint8_t* img, uint8_t* dimg, const FastArgs& a, int t, int k, int k1,
-                                         const uint32_t (&wc)[Up2<C>::NW], uint32_t (&wn)[Up2<C>::NW],
-                                         const float (&hp)[8 * C], float (&q)[8 * C], float (&hn)[8 * C]) {
-  up2_h<C>(wc, t, a.groups - 1, hn);
-  if (k + 1 < k1) up2_load<C>(img + (int64_t)(k + 1) * a.s_rp, t, a.sw, wn);
-  if (k == 0) {
-    up2_emit_copy<C>(dimg, hn);
-  } else {
-    up2_emit<C>(dimg + (int64_t)(2 * k - 1) * a.d_rp, hn, q);
-  }
+__device__ __forceinline__ void up2_lds(const uint8_t* seg_row_base, int t, uint32_t (&w)[Up2<C>::NW]) {
+  // seg_row_base points at source-row byte 0 inside the slot (may lie before
+  // the slot for t = 0; those bytes feed only the clamped pixel and are unused)
+  const uint32_t* rw = reinterpret_cast<const uint32_t*>(seg_row_base + 4 * C * t - 4);
 #pragma unroll
-  for (int e = 0; e < 8 * C; ++e) q[e] = __fmul_rn(hn[e], 0.75f);
-  if (k > 0) up2_emit<C>(dimg + (int64_t)(2 * k) * a.d_rp, hp, q);
+  for (int i = 0; i < Up2<C>::NW; ++i) w[i] = rw[i];
 }
 
 template <int C>
-__global__ void __launch_bounds__(128, 4) resize_up2_kernel(const __grid_constant__ FastArgs a) {
-  constexpr int E = Up2<C>::E, NW = Up2<C>::NW;
-  const int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  const int64_t total = (int64_t)a.n * a.bands * a.groups;
-  if (gid >= total) return;
-  const int t = (int)(gid % a.groups);
-  const int64_t r = gid / a.groups;
-  const int band = (int)(r % a.bands);
-  const int n = (int)(r / a.bands);
-  const int k0 = band * a.band;
-  const int k1 = min(k0 + a.band, a.sh);
-  const uint8_t* img = a.src + n * a.s_is;
-  uint8_t* dimg = a.dst + n * a.d_is + t * 8 * C;
-
-  // two h buffers and two source windows used alternately (no register copies)
-  float h0[E], h1[E], q[E];
-  uint32_t w0[NW], w1[NW];
-  if (k0 > 0) {
-    up2_load<C>(img + (int64_t)(k0 - 1) * a.s_rp, t, a.sw, w1);
-    up2_load<C>(img + (int64_t)k0 * a.s_rp, t, a.sw, w0);
-    up2_h<C>(w1, t, a.groups - 1, h0);
-#pragma unroll
-    for (int e = 0; e < E; ++e) q[e] = __fmul_rn(h0[e], 0.75f);
+__device__ __forceinline__ void up2_step_s(uint8_t* dimg, const FastArgs& a, int t, int k,
+                                           const uint32_t (&w)[Up2<C>::NW], const f2_t (&hp)[4 * C],
+                                           f2_t (&q)[4 * C], f2_t (&hn)[4 * C]) {
+  up2_h<C>(w, t, a.groups - 1, hn);
+  if (k == 0) {
+    up2_emit_copy<C>(dimg, hn, a.one);
   } else {
-    up2_load<C>(img, t, a.sw, w0);
+    up2_emit<C>(dimg + (int64_t)(2 * k - 1) * a.d_rp, hn, q, a.one);
+  }
+#pragma unroll
+  for (int e = 0; e < 4 * C; ++e) q[e] = fmul2(hn[e], f2(0.75f, 0.75f));
+  if (k > 0) up2_emit<C>(dimg + (int64_t)(2 * k) * a.d_rp, hp, q, a.one);
+}
+
+template <int C>
+__global__ void __launch_bounds__((UP2_NCW + 1) * 32, 3) resize_up2_kernel(const __grid_constant__ FastArgs a) {
+  constexpr int NP = 4 * C, NW = Up2<C>::NW;
+  extern __shared__ __align__(128) uint8_t smem[];
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem);
+  uint64_t* empty = full + UP2_RING;
+  uint8_t* slots = smem + 16 * UP2_RING + 16;  // 16 bytes of slack before slot 0
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int n = blockIdx.z;
+  const int k0 = blockIdx.y * a.band;
+  const int k1 = min(k0 + a.band, a.sh);
+  const int g0 = blockIdx.x * UP2_GROUPS;                 // first column group of the tile
+  const int g1 = min(g0 + UP2_GROUPS, a.groups);
+  // source bytes the tile reads: pixels [4*g0 - 1, 4*g1] clamped, 16-byte aligned superset
+  const int b_lo = max(4 * g0 - 1, 0) * C;
+  const int b_hi = min(4 * g1 + 1, a.sw) * C;
+  const int gstart = b_lo & ~15;
+  const uint32_t nbytes = (uint32_t)((b_hi - gstart + 15) & ~15);
+  const int r_first = k0 > 0 ? k0 - 1 : 0;
+
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int s = 0; s < UP2_RING; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], UP2_NCW);
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+
+  if (warp == UP2_NCW) {  // producer
+    if (lane == 0) {
+      const uint8_t* src = a.src + n * a.s_is + gstart;
+      for (int r = r_first, i = 0; r < k1; ++r, ++i) {
+        const int slot = i % UP2_RING;
+        if (i >= UP2_RING) mbar_wait_sleep(&empty[slot], (uint32_t)(((i / UP2_RING) - 1) & 1));
+        mbar_expect_tx(&full[slot], nbytes);
+        tma_bulk_g2s(slots + slot * a.slot_bytes, src + (int64_t)r * a.s_rp, nbytes, &full[slot]);
+      }
+    }
+    return;
+  }
+
+  const int t = g0 + warp * 32 + lane;  // this thread's column group
+  const bool active = t < g1;
+  uint8_t* dimg = a.dst + n * a.d_is + (int64_t)t * 8 * C;
+  f2_t h0[NP], h1[NP], q[NP];
+  uint32_t w[NW];
+  int i = 0;
+  auto take = [&](int r) {  // window of source row r from the ring
+    const int slot = i % UP2_RING;
+    mbar_wait(&full[slot], (uint32_t)((i / UP2_RING) & 1));
+    up2_lds<C>(slots + slot * a.slot_bytes - gstart, t, w);
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[slot]);
+    ++i;
+    (void)r;
+  };
+  if (k0 > 0) {
+    take(k0 - 1);
+    up2_h<C>(w, t, a.groups - 1, h0);
+#pragma unroll
+    for (int e = 0; e < NP; ++e) q[e] = fmul2(h0[e], f2(0.75f, 0.75f));
   }
   int k = k0;
 #pragma unroll 1
   for (; k + 1 < k1; k += 2) {
-    up2_step<C>(img, dimg, a, t, k, k1, w0, w1, h0, q, h1);
-    up2_step<C>(img, dimg, a, t, k + 1, k1, w1, w0, h1, q, h0);
+    take(k);
+    if (active) up2_step_s<C>(dimg, a, t, k, w, h0, q, h1);
+    take(k + 1);
+    if (active) up2_step_s<C>(dimg, a, t, k + 1, w, h1, q, h0);
   }
   if (k < k1) {
-    up2_step<C>(img, dimg, a, t, k, k1, w0, w1, h0, q, h1);
-    if (k1 == a.sh) up2_emit_copy<C>(dimg + (int64_t)(2 * a.sh - 1) * a.d_rp, h1);
-  } else if (k1 == a.sh) {
-    up2_emit_copy<C>(dimg + (int64_t)(2 * a.sh - 1) * a.d_rp, h0);
+    take(k);
+    if (active) {
+      up2_step_s<C>(dimg, a, t, k, w, h0, q, h1);
+      if (k1 == a.sh) up2_emit_copy<C>(dimg + (int64_t)(2 * a.sh - 1) * a.d_rp, h1, a.one);
+    }
+  } else if (k1 == a.sh && active) {
+    up2_emit_copy<C>(dimg + (int64_t)(2 * a.sh - 1) * a.d_rp, h0, a.one);
   }
 }
 
@@ -264,8 +320,18 @@ static int launch_fast_c(const FastArgs& a0, bool down, cudaStream_t st) {
     a.groups = a.sw / 4;
     a.band = 32;
     a.bands = (a.sh + a.band - 1) / a.band;
-    const int64_t total = (int64_t)a.n * a.bands * a.groups;
-    resize_up2_kernel<C><<<(unsigned)((total + 127) / 128), 128, 0, st>>>(a);
+    // ring slot: the tile's source bytes (+ halo, + alignment), 16-byte padded
+    // on both sides for the unused halo words of the edge groups
+    a.slot_bytes = ((UP2_GROUPS * 4 + 2) * C + 16 + 15) / 16 * 16 + 32;
+    const size_t smem = 16 * UP2_RING + 16 + (size_t)UP2_RING * a.slot_bytes;
+    auto kern = resize_up2_kernel<C>;
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      attr = true;
+    }
+    dim3 grid((a.groups + UP2_GROUPS - 1) / UP2_GROUPS, a.bands, a.n);
+    kern<<<grid, (UP2_NCW + 1) * 32, smem, st>>>(a);
   }
   return check_launch(down ? "resize_down2_kernel" : "resize_up2_kernel");
 }
@@ -283,10 +349,10 @@ int resize_u8_fast(const uint8_t* src, int64_t s_is, int64_t s_rp, int sh, int s
   if (down) {
     if (!aligned(src, 16) || !aligned(dst, 16) || (s_is | s_rp | d_is | d_rp) & 15) return FV_OK;
   } else {
-    if (sw % 4 != 0 || sh < 2 || !aligned(src, 4) || !aligned(dst, 8) || (s_is | s_rp) & 3 || (d_is | d_rp) & 7)
+    if (sw % 4 != 0 || sh < 2 || !aligned(src, 16) || !aligned(dst, 8) || (s_is | s_rp) & 15 || (d_is | d_rp) & 7)
       return FV_OK;
   }
-  FastArgs a{src, s_is, s_rp, sh, sw, dst, d_is, d_rp, dh, dw, n, 0, 0, 0};
+  FastArgs a{src, s_is, s_rp, sh, sw, dst, d_is, d_rp, dh, dw, n, 0, 0, 0, 1.0f, 0};
   *taken = true;
   switch (c) {
     case 1: return launch_fast_c<1>(a, down, st);
