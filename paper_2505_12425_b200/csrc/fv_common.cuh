@@ -265,8 +265,26 @@ __device__ __forceinline__ bool mbar_try(uint64_t* bar, uint32_t parity) {
 }
 // wait with back-off: for a producer that is ahead and must not steal issue
 // slots from the consumer warps while it waits for a free slot
-__device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) {
-  while (!mbar_try(bar, parity)) __nanosleep(100);
+// (the ring is several rows deep, so a late wake-up costs nothing; polling
+// every ~1 us keeps the producer's issue share negligible)
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity, unsigned ns = 1000) {
+  while (!mbar_try(bar, parity)) __nanosleep(ns);
+}
+// blocking wait: the thread is suspended (NANOSLEEP.SYNCS) until the phase
+// completes or the hint (ns) expires, instead of spinning on try_wait
+__device__ __forceinline__ void mbar_wait_block(uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
+  do {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n"
+        "selp.u32 %0, 1, 0, p;\n"
+        "}\n"
+        : "=r"(ok)
+        : "r"(smem_u32(bar)), "r"(parity), "r"(1000000u)
+        : "memory");
+  } while (!ok);
 }
 // 1-D bulk copy global -> shared, completion signalled on `bar` (TMA unit,
 // SASS UBLKCP). dst/src 16-byte aligned, bytes a multiple of 16.

@@ -45,6 +45,7 @@ struct ResizeArgs {
   // strip kernel only
   int tile_px, band_rows, tiles_x, slot_bytes;
   int vec_store;
+  float one;  // runtime 1.0f (f32x2 contraction guard, fv_common.cuh)
 };
 
 struct LutArg {
@@ -93,7 +94,7 @@ __global__ void __launch_bounds__(128) resize_gather_kernel(const __grid_constan
 template <typename InT, int C, int MODE>
 struct StripCfg {
   // consumer warps; the tile must hold whole pixels (C = 3 -> multiple of 3)
-  static constexpr int NCW = (C == 3) ? 6 : 4;
+  static constexpr int NCW = MODE == MODE_CHW ? 5 : ((C == 3) ? 6 : 4);
   // lane ownership: groups of V contiguous elements (u8: 4 bytes -> one
   // 32-bit store) or V = 1 element / pixel, G groups per lane, groups of a
   // warp interleaved so that a warp's taps and stores are contiguous
@@ -161,7 +162,8 @@ __global__ void __launch_bounds__(StripCfg<InT, C, MODE>::NT, 3)
   // ------------------------------------------------------------------ producer
   if (warp == NCW) {
     __syncthreads();
-    (void)__syncthreads_and(1);  // pairs with the consumers' tile-uniform vote
+    (void)__syncthreads_and(1);  // pair with the consumers' two tile-uniform votes
+    (void)__syncthreads_and(1);
     if (lane == 0) {
       const char* src_img = reinterpret_cast<const char*>(a.src) + n * a.s_is + (seg_byte - shift);
       int last = -1, k = 0;
@@ -173,7 +175,7 @@ __global__ void __launch_bounds__(StripCfg<InT, C, MODE>::NT, 3)
           if (r <= last) continue;  // rows are non-decreasing; each is fetched once
           last = r;
           const int slot = k % RING;
-          if (k >= RING) mbar_wait_sleep(&empty[slot], (uint32_t)(((k / RING) - 1) & 1));
+          if (k >= RING) mbar_wait_block(&empty[slot], (uint32_t)(((k / RING) - 1) & 1));
           mbar_expect_tx(&full[slot], nbytes);
           tma_bulk_g2s(slots + slot * a.slot_bytes, src_img + (int64_t)r * a.s_rp, nbytes, &full[slot]);
           ++k;
@@ -184,17 +186,20 @@ __global__ void __launch_bounds__(StripCfg<InT, C, MODE>::NT, 3)
   }
 
   // ------------------------------------------------------------------ consumers
-  // per-element horizontal taps, loop-invariant over the band
+  // horizontal taps, loop-invariant over the band: per element (HWC modes)
+  // or per pixel (CHW: all channels of a pixel share them; element e of
+  // pixel j = e / C reads offset oa[j] + e % C)
+  constexpr int NA = MODE == MODE_CHW ? G : EPT;
   const int shift_el = shift / (int)sizeof(InT);
-  int oa[EPT], ob[EPT];
-  float wa[EPT], wb[EPT];
-  bool hfma = true;
+  int oa[NA], ob[NA];
+  float wa[NA], wb[NA];
+  bool hfma = true, hcopy = true;
 #pragma unroll
-  for (int e = 0; e < EPT; ++e) {
+  for (int e = 0; e < NA; ++e) {
     int px, ch;
     if (MODE == MODE_CHW) {
-      px = p0 + warp * 32 * G + (e / C) * 32 + lane;
-      ch = e % C;
+      px = p0 + warp * 32 * G + e * 32 + lane;
+      ch = 0;
     } else {
       const int idx = warp * (32 * G * V) + (e / V) * (32 * V) + lane * V + (e % V);
       px = p0 + idx / C;
@@ -210,23 +215,45 @@ __global__ void __launch_bounds__(StripCfg<InT, C, MODE>::NT, 3)
     wa[e] = swap ? t.w1 : t.w0;
     wb[e] = swap ? t.w0 : t.w1;
     hfma = hfma && exact_weight<MODE>(wb[e]);
+    hcopy = hcopy && wb[e] == 0.0f && wa[e] == 1.0f;  // fx == 0: h is the tap itself
   }
+  auto OA = [&](int e) { return MODE == MODE_CHW ? oa[e / C] + e % C : oa[e]; };
+  auto OB = [&](int e) { return MODE == MODE_CHW ? ob[e / C] + e % C : ob[e]; };
+  auto WA = [&](int e) { return MODE == MODE_CHW ? wa[e / C] : wa[e]; };
+  auto WB = [&](int e) { return MODE == MODE_CHW ? wb[e / C] : wb[e]; };
   __syncthreads();  // row table, LUT and barriers ready
-  hfma = __syncthreads_and(hfma) != 0;  // tile-uniform choice of blend form (producer passed 1 above)
+  // tile-uniform choice of the horizontal blend form (producer voted 1 above)
+  const int all_copy = __syncthreads_and(hcopy);
+  const int all_fma = __syncthreads_and(hfma);
+  const int hmode = all_copy ? 2 : (all_fma ? 1 : 0);
+  const float one = a.one;
 
-  float ha[EPT], hb[EPT];
+  constexpr int NP = EPT / 2;  // element pairs (packed f32x2)
+  f2_t ha[NP], hb[NP];
   int ra = -1, rb = -1, k = 0;
 
-  auto consume = [&](float (&h)[EPT]) {
+  auto consume = [&](f2_t (&h)[NP]) {
     const int slot = k % RING;
     mbar_wait(&full[slot], (uint32_t)((k / RING) & 1));
     const InT* seg = reinterpret_cast<const InT*>(slots + slot * a.slot_bytes);
-    if (hfma) {
 #pragma unroll
-      for (int e = 0; e < EPT; ++e) h[e] = lerp_fma(tap_value(seg[oa[e]]), tap_value(seg[ob[e]]), wa[e], wb[e]);
-    } else {
-#pragma unroll
-      for (int e = 0; e < EPT; ++e) h[e] = lerp_ref(tap_value(seg[oa[e]]), tap_value(seg[ob[e]]), wa[e], wb[e]);
+    for (int p = 0; p < NP; ++p) {
+      const int e = 2 * p;
+      f2_t va, vb;
+      if constexpr (sizeof(InT) == 1) {
+        va = unit2(0x4B000000u | seg[OA(e)], 0x4B000000u | seg[OA(e + 1)]);
+        if (hmode != 2) vb = unit2(0x4B000000u | seg[OB(e)], 0x4B000000u | seg[OB(e + 1)]);
+      } else {
+        va = f2(seg[OA(e)], seg[OA(e + 1)]);
+        if (hmode != 2) vb = f2(seg[OB(e)], seg[OB(e + 1)]);
+      }
+      if (hmode == 2) {
+        h[p] = va;
+      } else if (hmode == 1) {
+        h[p] = ffma2(vb, f2(WB(e), WB(e + 1)), fmul2(va, f2(WA(e), WA(e + 1))));
+      } else {
+        h[p] = ffma2(fmul2(vb, f2(WB(e), WB(e + 1))), f2(one, one), fmul2(va, f2(WA(e), WA(e + 1))));
+      }
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[slot]);
@@ -239,7 +266,7 @@ __global__ void __launch_bounds__(StripCfg<InT, C, MODE>::NT, 3)
     if (rt.x != ra) {
       if (rt.x == rb) {
 #pragma unroll
-        for (int e = 0; e < EPT; ++e) ha[e] = hb[e];
+        for (int p = 0; p < NP; ++p) ha[p] = hb[p];
       } else {
         consume(ha);
       }
@@ -248,23 +275,24 @@ __global__ void __launch_bounds__(StripCfg<InT, C, MODE>::NT, 3)
     if (rt.y != rb) {
       if (rt.y == ra) {
 #pragma unroll
-        for (int e = 0; e < EPT; ++e) hb[e] = ha[e];
+        for (int p = 0; p < NP; ++p) hb[p] = ha[p];
       } else {
         consume(hb);
       }
       rb = rt.y;
     }
     const float wy0 = __int_as_float(rt.z), wy1 = __int_as_float(rt.w);
-    float o[EPT];
+    const f2_t WY0 = f2(wy0, wy0), WY1 = f2(wy1, wy1);
+    f2_t o[NP];
     if (exact_weight<MODE>(wy1)) {
 #pragma unroll
-      for (int e = 0; e < EPT; ++e) o[e] = lerp_fma(ha[e], hb[e], wy0, wy1);
+      for (int p = 0; p < NP; ++p) o[p] = ffma2(hb[p], WY1, fmul2(ha[p], WY0));
     } else if (exact_weight<MODE>(wy0)) {
 #pragma unroll
-      for (int e = 0; e < EPT; ++e) o[e] = lerp_fma(hb[e], ha[e], wy1, wy0);
+      for (int p = 0; p < NP; ++p) o[p] = ffma2(ha[p], WY0, fmul2(hb[p], WY1));
     } else {
 #pragma unroll
-      for (int e = 0; e < EPT; ++e) o[e] = lerp_ref(ha[e], hb[e], wy0, wy1);
+      for (int p = 0; p < NP; ++p) o[p] = ffma2(fmul2(hb[p], WY1), f2(one, one), fmul2(ha[p], WY0));
     }
 
     const int y = yb + i;
@@ -274,35 +302,41 @@ __global__ void __launch_bounds__(StripCfg<InT, C, MODE>::NT, 3)
 #pragma unroll
       for (int j = 0; j < G; ++j) {
         const int idx = warp * (32 * G * V) + j * (32 * V) + lane * V;
-        uint32_t q[V];
-#pragma unroll
-        for (int v = 0; v < V; ++v) q[v] = unit_to_u8(o[j * V + v]);
+        const f2_t r0 = scale_to_u8_bits2(o[2 * j], 255.0f, one);
+        const f2_t r1 = scale_to_u8_bits2(o[2 * j + 1], 255.0f, one);
         if (a.vec_store && idx + V <= row_el) {
-          const uint32_t wd = __byte_perm(__byte_perm(q[0], q[1], 0x0040), __byte_perm(q[2], q[3], 0x0040), 0x5410);
-          __stcs(reinterpret_cast<uint32_t*>(drow + idx), wd);
+          __stcs(reinterpret_cast<uint32_t*>(drow + idx), pack4x2(r0, r1));
         } else {
+          uint32_t q[4];
+          f2split(r0, q[0], q[1]);
+          f2split(r1, q[2], q[3]);
 #pragma unroll
           for (int v = 0; v < V; ++v)
-            if (idx + v < row_el) drow[idx + v] = (uint8_t)q[v];
+            if (idx + v < row_el) drow[idx + v] = (uint8_t)(q[v] & 0xFF);
         }
       }
     } else if constexpr (MODE == MODE_F32) {
       float* drow = row_ptr_mut<float>(a.dst, a.d_is, a.d_rp, n, y) + p0 * C;
       const int row_el = (p1 - p0) * C;
 #pragma unroll
-      for (int j = 0; j < G; ++j) {
-        const int idx = warp * (32 * G) + j * 32 + lane;
-        if (idx < row_el) __stcs(drow + idx, o[j]);
+      for (int p = 0; p < NP; ++p) {
+        uint32_t lo, hi;
+        f2split(o[p], lo, hi);
+        const int i0 = warp * (32 * G) + (2 * p) * 32 + lane;
+        if (i0 < row_el) __stcs(drow + i0, __uint_as_float(lo));
+        if (i0 + 32 < row_el) __stcs(drow + i0 + 32, __uint_as_float(hi));
       }
     } else {
       char* img = reinterpret_cast<char*>(a.dst) + n * a.d_is + (int64_t)y * a.d_rp;
 #pragma unroll
-      for (int j = 0; j < G; ++j) {
-        const int px = p0 + warp * 32 * G + j * 32 + lane;
-        if (px < p1) {
+      for (int p = 0; p < NP; ++p) {
+        uint32_t q[2];
+        f2split(scale_to_u8_bits2(o[p], 255.0f, one), q[0], q[1]);
 #pragma unroll
-          for (int ch = 0; ch < C; ++ch)
-            __stcs(reinterpret_cast<float*>(img + ch * a.d_ps) + px, lut[ch * 256 + unit_to_u8(o[j * C + ch])]);
+        for (int h = 0; h < 2; ++h) {
+          const int e = 2 * p + h, j = e / C, ch = e % C;
+          const int px = p0 + warp * 32 * G + j * 32 + lane;
+          if (px < p1) __stcs(reinterpret_cast<float*>(img + ch * a.d_ps) + px, lut[ch * 256 + (q[h] & 0xFF)]);
         }
       }
     }
@@ -396,6 +430,7 @@ static ResizeArgs make_args(const void* src, int64_t s_is, int64_t s_rp, int sh,
   a.scale_y = (double)sh / (double)dh;
   const bool dst_al = (reinterpret_cast<uintptr_t>(dst) & 3) == 0 && (d_is & 3) == 0 && (d_rp & 3) == 0;
   a.vec_store = dst_al ? 1 : 0;
+  a.one = 1.0f;
   (void)out_elem;
   return a;
 }
