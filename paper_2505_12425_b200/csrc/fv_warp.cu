@@ -28,6 +28,7 @@ struct WarpArgs {
   int c;
   float border_f;     // border as a blend operand (u8: RN(b/255))
   float border_raw;   // border as stored for non-finite coordinates
+  float one;          // runtime 1.0f (f32x2 contraction guard)
 };
 
 struct WarpMats {
@@ -87,11 +88,13 @@ __device__ __forceinline__ WarpTap warp_tap(const double (&m)[9], double rx, dou
   return t;
 }
 
-// Taps of the two source pixels (x0, x0+1) of one row, all C channels.
-// u8, C = 3, interior: three aligned 32-bit loads + two funnel shifts
-// instead of six byte loads.
+// Raw taps of the two source pixels (x0, x0+1) of one row, all C channels:
+// u8 -> magic words 0x4B0000uu (converted later, two at a time), f32 -> bits.
+// u8, C = 3: three aligned 32-bit loads + two funnel shifts instead of six
+// byte loads.
 template <typename InT, int C>
-__device__ __forceinline__ void load_pair(const InT* row, int x0, int row_elems, float (&t0)[C], float (&t1)[C]) {
+__device__ __forceinline__ void load_pair_raw(const InT* row, int x0, int row_elems, uint32_t (&t0)[C],
+                                              uint32_t (&t1)[C]) {
   if constexpr (sizeof(InT) == 1 && C == 3) {
     const uintptr_t p = reinterpret_cast<uintptr_t>(row) + 3 * x0;
     const uintptr_t al = p & ~(uintptr_t)3;
@@ -104,29 +107,79 @@ __device__ __forceinline__ void load_pair(const InT* row, int x0, int row_elems,
       v[1] = __funnelshift_r(w1, w2, sh);
 #pragma unroll
       for (int c = 0; c < 3; ++c) {
-        t0[c] = unit_of(v, c);
-        t1[c] = unit_of(v, 3 + c);
+        t0[c] = magic_of(v, c);
+        t1[c] = magic_of(v, 3 + c);
       }
       return;
     }
   }
 #pragma unroll
   for (int c = 0; c < C; ++c) {
-    t0[c] = tap_value(__ldg(row + x0 * C + c));
-    t1[c] = tap_value(__ldg(row + (x0 + 1) * C + c));
+    if constexpr (sizeof(InT) == 1) {
+      t0[c] = 0x4B000000u | __ldg(row + x0 * C + c);
+      t1[c] = 0x4B000000u | __ldg(row + (x0 + 1) * C + c);
+    } else {
+      t0[c] = __float_as_uint(__ldg(row + x0 * C + c));
+      t1[c] = __float_as_uint(__ldg(row + (x0 + 1) * C + c));
+    }
   }
 }
 
-// Fixed-C kernel (C = 1, 3, 4): a 32 x 8 tile of destination pixels per CTA,
-// one pixel per thread. The row terms m1*y + m2 etc. are computed once per
-// thread; interior pixels (all four taps inside) take unguarded loads.
+template <typename InT, int C>
+__device__ __forceinline__ void gather_raw(const WarpArgs& a, int n, const WarpTap& t, uint32_t bord,
+                                           uint32_t (&t00)[C], uint32_t (&t01)[C], uint32_t (&t10)[C],
+                                           uint32_t (&t11)[C]) {
+  const bool inx = t.x0 >= 0 && t.x0 + 1 < a.sw, iny = t.y0 >= 0 && t.y0 + 1 < a.sh;
+  const bool outside = t.x0 < -1 || t.x0 >= a.sw || t.y0 < -1 || t.y0 >= a.sh || !t.finite;
+  if (inx && iny) {
+    const InT* r0 = row_ptr<InT>(a.src, a.s_is, a.s_rp, n, t.y0);
+    const InT* r1 = row_ptr<InT>(a.src, a.s_is, a.s_rp, n, t.y0 + 1);
+    load_pair_raw<InT, C>(r0, t.x0, a.sw * C, t00, t01);
+    load_pair_raw<InT, C>(r1, t.x0, a.sw * C, t10, t11);
+  } else if (outside) {  // every tap reads the border
+#pragma unroll
+    for (int c = 0; c < C; ++c) t00[c] = t01[c] = t10[c] = t11[c] = bord;
+  } else {
+    const bool ix0 = t.x0 >= 0 && t.x0 < a.sw, ix1 = t.x0 + 1 >= 0 && t.x0 + 1 < a.sw;
+    const bool iy0 = t.y0 >= 0 && t.y0 < a.sh, iy1 = t.y0 + 1 >= 0 && t.y0 + 1 < a.sh;
+    const InT* r0 = row_ptr<InT>(a.src, a.s_is, a.s_rp, n, iy0 ? t.y0 : 0);
+    const InT* r1 = row_ptr<InT>(a.src, a.s_is, a.s_rp, n, iy1 ? t.y0 + 1 : 0);
+    auto raw = [&](const InT* r, int i) -> uint32_t {
+      if constexpr (sizeof(InT) == 1) return 0x4B000000u | __ldg(r + i);
+      else return __float_as_uint(__ldg(r + i));
+    };
+#pragma unroll
+    for (int c = 0; c < C; ++c) {
+      t00[c] = (iy0 && ix0) ? raw(r0, t.x0 * C + c) : bord;
+      t01[c] = (iy0 && ix1) ? raw(r0, (t.x0 + 1) * C + c) : bord;
+      t10[c] = (iy1 && ix0) ? raw(r1, t.x0 * C + c) : bord;
+      t11[c] = (iy1 && ix1) ? raw(r1, (t.x0 + 1) * C + c) : bord;
+    }
+  }
+}
+
+// blend operands from two raw taps (one per pixel of the thread's pair)
+template <typename InT>
+__device__ __forceinline__ f2_t tap2(uint32_t r0, uint32_t r1) {
+  if constexpr (sizeof(InT) == 1) return unit2(r0, r1);
+  else return f2u(r0, r1);
+}
+
+// Fixed-C kernel (C = 1, 3, 4): a 64 x 8 tile of destination pixels per CTA;
+// each thread samples pixels x and x + 32 (a warp covers 64 consecutive
+// pixels, lanes stay contiguous for the gathers). The matrix and the row
+// terms m1*y + m2 etc. are loaded / computed once per thread; tap
+// conversion, blend and the u8 epilogue of the two pixels run as packed
+// f32x2 pairs. Interior pixels take unguarded loads, pixels whose four taps
+// are all outside skip the loads.
 template <typename InT, bool PERSP, int C>
 __global__ void __launch_bounds__(256) warp_kernel(const __grid_constant__ WarpArgs a,
                                                    const __grid_constant__ WarpMats mats) {
   const int n = blockIdx.z;
-  const int x = blockIdx.x * 32 + threadIdx.x;
+  const int x = blockIdx.x * 64 + threadIdx.x;
   const int y = blockIdx.y * 8 + threadIdx.y;
   if (x >= a.dw || y >= a.dh) return;
+  const bool two = x + 32 < a.dw;
   double m[9];
 #pragma unroll
   for (int i = 0; i < 9; ++i) m[i] = mats.m[n][i];
@@ -134,38 +187,36 @@ __global__ void __launch_bounds__(256) warp_kernel(const __grid_constant__ WarpA
   const double rx = __dadd_rn(__dmul_rn(m[1], yd), m[2]);
   const double ry = __dadd_rn(__dmul_rn(m[4], yd), m[5]);
   const double rw = PERSP ? __dadd_rn(__dmul_rn(m[7], yd), m[8]) : 0.0;
-  const WarpTap t = warp_tap<PERSP>(m, rx, ry, rw, x, a.sw, a.sh);
+  WarpTap t[2];
+  t[0] = warp_tap<PERSP>(m, rx, ry, rw, x, a.sw, a.sh);
+  t[1] = warp_tap<PERSP>(m, rx, ry, rw, two ? x + 32 : x, a.sw, a.sh);
+  const uint32_t bord = sizeof(InT) == 1 ? (0x4B000000u | (uint32_t)a.border_raw) : __float_as_uint(a.border_f);
+  uint32_t v00[2][C], v01[2][C], v10[2][C], v11[2][C];
+#pragma unroll
+  for (int k = 0; k < 2; ++k) gather_raw<InT, C>(a, n, t[k], bord, v00[k], v01[k], v10[k], v11[k]);
+
+  const float one = a.one;
+  const f2_t WX0 = f2(t[0].wx0, t[1].wx0), WX1 = f2(t[0].wx1, t[1].wx1);
+  const f2_t WY0 = f2(t[0].wy0, t[1].wy0), WY1 = f2(t[0].wy1, t[1].wy1);
+  const f2_t ONE = f2(one, one);
   InT* d = row_ptr_mut<InT>(a.dst, a.d_is, a.d_rp, n, y) + x * C;
-  if (!t.finite) {
-#pragma unroll
-    for (int c = 0; c < C; ++c) d[c] = (InT)a.border_raw;
-    return;
-  }
-  float t00[C], t01[C], t10[C], t11[C];
-  const bool inx = t.x0 >= 0 && t.x0 + 1 < a.sw, iny = t.y0 >= 0 && t.y0 + 1 < a.sh;
-  if (inx && iny) {
-    const InT* r0 = row_ptr<InT>(a.src, a.s_is, a.s_rp, n, t.y0);
-    const InT* r1 = row_ptr<InT>(a.src, a.s_is, a.s_rp, n, t.y0 + 1);
-    load_pair<InT, C>(r0, t.x0, a.sw * C, t00, t01);
-    load_pair<InT, C>(r1, t.x0, a.sw * C, t10, t11);
-  } else {
-    const bool ix0 = t.x0 >= 0 && t.x0 < a.sw, ix1 = t.x0 + 1 >= 0 && t.x0 + 1 < a.sw;
-    const bool iy0 = t.y0 >= 0 && t.y0 < a.sh, iy1 = t.y0 + 1 >= 0 && t.y0 + 1 < a.sh;
-    const InT* r0 = row_ptr<InT>(a.src, a.s_is, a.s_rp, n, iy0 ? t.y0 : 0);
-    const InT* r1 = row_ptr<InT>(a.src, a.s_is, a.s_rp, n, iy1 ? t.y0 + 1 : 0);
-#pragma unroll
-    for (int c = 0; c < C; ++c) {
-      t00[c] = (iy0 && ix0) ? tap_value(__ldg(r0 + t.x0 * C + c)) : a.border_f;
-      t01[c] = (iy0 && ix1) ? tap_value(__ldg(r0 + (t.x0 + 1) * C + c)) : a.border_f;
-      t10[c] = (iy1 && ix0) ? tap_value(__ldg(r1 + t.x0 * C + c)) : a.border_f;
-      t11[c] = (iy1 && ix1) ? tap_value(__ldg(r1 + (t.x0 + 1) * C + c)) : a.border_f;
-    }
-  }
 #pragma unroll
   for (int c = 0; c < C; ++c) {
-    const float top = lerp_ref(t00[c], t01[c], t.wx0, t.wx1);
-    const float bot = lerp_ref(t10[c], t11[c], t.wx0, t.wx1);
-    d[c] = to_out<InT>(lerp_ref(top, bot, t.wy0, t.wy1));
+    // imgproc.py:118-123 order, each product and sum rounded (the sum is
+    // fma(q, runtime 1, p): see the f32x2 note in fv_common.cuh)
+    const f2_t top = ffma2(fmul2(tap2<InT>(v01[0][c], v01[1][c]), WX1), ONE, fmul2(tap2<InT>(v00[0][c], v00[1][c]), WX0));
+    const f2_t bot = ffma2(fmul2(tap2<InT>(v11[0][c], v11[1][c]), WX1), ONE, fmul2(tap2<InT>(v10[0][c], v10[1][c]), WX0));
+    const f2_t o = ffma2(fmul2(bot, WY1), ONE, fmul2(top, WY0));
+    uint32_t lo, hi;
+    if constexpr (sizeof(InT) == 1) {
+      f2split(scale_to_u8_bits2(o, 255.0f, one), lo, hi);
+      d[c] = t[0].finite ? (InT)(lo & 0xFF) : (InT)a.border_raw;
+      if (two) d[32 * C + c] = t[1].finite ? (InT)(hi & 0xFF) : (InT)a.border_raw;
+    } else {
+      f2split(o, lo, hi);
+      d[c] = t[0].finite ? __uint_as_float(lo) : a.border_raw;
+      if (two) d[32 * C + c] = t[1].finite ? __uint_as_float(hi) : a.border_raw;
+    }
   }
 }
 
@@ -228,6 +279,7 @@ static int launch_warp(const InT* src, int64_t s_is, int64_t s_rp, int sh, int s
   a.c = c;
   a.border_f = border_f;
   a.border_raw = border_raw;
+  a.one = 1.0f;
   WarpMats mats;
   for (int b = 0; b < n; b += MAXW) {
     const int nb = (n - b) < MAXW ? (n - b) : MAXW;
@@ -235,13 +287,14 @@ static int launch_warp(const InT* src, int64_t s_is, int64_t s_rp, int sh, int s
       for (int j = 0; j < 9; ++j) mats.m[i][j] = j < mat_len ? mats_host[(int64_t)(b + i) * mat_len + j] : 0.0;
     a.src = reinterpret_cast<const char*>(src) + (int64_t)b * s_is;
     a.dst = reinterpret_cast<char*>(dst) + (int64_t)b * d_is;
-    dim3 grid((dw + 31) / 32, (dh + 7) / 8, nb);
     dim3 block(32, 8);
+    dim3 grid2((dw + 63) / 64, (dh + 7) / 8, nb);  // two pixels per thread
+    dim3 grid1((dw + 31) / 32, (dh + 7) / 8, nb);
     switch (c) {
-      case 1: warp_kernel<InT, PERSP, 1><<<grid, block, 0, st>>>(a, mats); break;
-      case 3: warp_kernel<InT, PERSP, 3><<<grid, block, 0, st>>>(a, mats); break;
-      case 4: warp_kernel<InT, PERSP, 4><<<grid, block, 0, st>>>(a, mats); break;
-      default: warp_kernel_any<InT, PERSP><<<grid, block, 0, st>>>(a, mats); break;
+      case 1: warp_kernel<InT, PERSP, 1><<<grid2, block, 0, st>>>(a, mats); break;
+      case 3: warp_kernel<InT, PERSP, 3><<<grid2, block, 0, st>>>(a, mats); break;
+      case 4: warp_kernel<InT, PERSP, 4><<<grid2, block, 0, st>>>(a, mats); break;
+      default: warp_kernel_any<InT, PERSP><<<grid1, block, 0, st>>>(a, mats); break;
     }
     int rc = check_launch(fn);
     if (rc) return rc;
