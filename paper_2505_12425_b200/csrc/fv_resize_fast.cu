@@ -194,7 +194,7 @@ __device__ __forceinline__ void up2_emit_copy(uint8_t* drow, const f2_t (&h)[4 *
 // (cp.async.bulk, completion on the slot's "full" mbarrier); consumers read
 // their 4-byte aligned windows with LDS (lane stride 12 B: conflict-free) and
 // release the slot on its "empty" mbarrier.
-constexpr int UP2_NCW = 4, UP2_GROUPS = UP2_NCW * 32, UP2_RING = 8;
+constexpr int UP2_NCW = 3, UP2_GROUPS = UP2_NCW * 32, UP2_RING = 8;
 
 template <int C>
 __device__ __forceinline__ void up2_lds(const uint8_t* seg_row_base, int t, uint32_t (&w)[Up2<C>::NW]) {
@@ -221,7 +221,7 @@ __device__ __forceinline__ void up2_step_s(uint8_t* dimg, const FastArgs& a, int
 }
 
 template <int C>
-__global__ void __launch_bounds__((UP2_NCW + 1) * 32, 3) resize_up2_kernel(const __grid_constant__ FastArgs a) {
+__global__ void __launch_bounds__((UP2_NCW + 1) * 32, 4) resize_up2_kernel(const __grid_constant__ FastArgs a) {
   constexpr int NP = 4 * C, NW = Up2<C>::NW;
   extern __shared__ __align__(128) uint8_t smem[];
   uint64_t* full = reinterpret_cast<uint64_t*>(smem);
