@@ -42,6 +42,16 @@ METRIC = "megapixels/sec per op at 1/2/4/8 B200; achieved HBM GB/s vs peak"
 UNIT = "MP/s"
 
 
+def load_traffic():
+    """DRAM bytes (read + write) per launch of each kernel from the committed
+    `ncu --set full` captures (profiles/traffic.json), or {}."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
+            return json.load(f)
+    except Exception:
+        return {}
+
+
 def load_peaks():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     try:
@@ -462,6 +472,8 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-cores", type=int, default=0)
+    ap.add_argument("--soak", type=float, default=1.0,
+                    help="seconds of untimed cfg1 steps before timing (clock sampler sees a loaded GPU)")
     args = ap.parse_args()
     world, rank, local = dist_env()
 
@@ -506,7 +518,7 @@ def main():
     results = {}
     total_launches = 0
     for name, op in ops.items():
-        soak = 1.0 if name.startswith("cfg1") else 0.0
+        soak = args.soak if name.startswith("cfg1") else 0.0
         ms, per, lc = time_op(op, args.steps, max(3, args.warmup), stream, world, soak_s=soak)
         total_launches += lc if name.startswith("cfg1") else 0
         kern = []
@@ -569,7 +581,9 @@ def main():
                        "l2": "inputs 1.59 GB >> 126 MB L2 (no flush needed)"},
             "roofline": {"bound": "hbm", "kernel": dom["kernel"], "achieved": dom["gbs"], "peak": peak,
                          "peak_source": peak_src, "unit": "GB/s", "frac": dom["gbs"] / peak,
-                         "traffic": None, "algorithmic_bytes_per_launch": dom["algorithmic_bytes"],
+                         "traffic": load_traffic().get(dom["kernel"], {}).get("dram_bytes"),
+                         "traffic_source": load_traffic().get(dom["kernel"], {}).get("source"),
+                         "algorithmic_bytes_per_launch": dom["algorithmic_bytes"],
                          "launch_ms": dom["ms"]},
             "cpu_baseline": cpu,
             "e2e": e2e,
