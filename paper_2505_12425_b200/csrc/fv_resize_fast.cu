@@ -256,7 +256,7 @@ __global__ void __launch_bounds__((UP2_NCW + 1) * 32, 4) resize_up2_kernel(const
       const uint8_t* src = a.src + n * a.s_is + gstart;
       for (int r = r_first, i = 0; r < k1; ++r, ++i) {
         const int slot = i % UP2_RING;
-        if (i >= UP2_RING) mbar_wait_sleep(&empty[slot], (uint32_t)(((i / UP2_RING) - 1) & 1));
+        if (i >= UP2_RING) mbar_wait_block(&empty[slot], (uint32_t)(((i / UP2_RING) - 1) & 1));
         mbar_expect_tx(&full[slot], nbytes);
         tma_bulk_g2s(slots + slot * a.slot_bytes, src + (int64_t)r * a.s_rp, nbytes, &full[slot]);
       }
