@@ -113,6 +113,24 @@ __device__ __forceinline__ void load_pair_raw(const InT* row, int x0, int row_el
       return;
     }
   }
+  if constexpr (sizeof(InT) == 4 && C == 3) {
+    // six consecutive floats at byte 12*x0: four aligned 8-byte loads cover
+    // them for either 8-byte phase (4 LSU requests instead of 6)
+    const uintptr_t p = reinterpret_cast<uintptr_t>(row) + 12 * x0;
+    const uintptr_t al = p & ~(uintptr_t)7;
+    if (al + 32 <= reinterpret_cast<uintptr_t>(row) + 4 * row_elems) {
+      const uint2* w = reinterpret_cast<const uint2*>(al);
+      const uint2 q0 = __ldg(w), q1 = __ldg(w + 1), q2 = __ldg(w + 2), q3 = __ldg(w + 3);
+      const uint32_t v[8] = {q0.x, q0.y, q1.x, q1.y, q2.x, q2.y, q3.x, q3.y};
+      const bool odd = (p & 7) != 0;
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        t0[c] = odd ? v[c + 1] : v[c];
+        t1[c] = odd ? v[c + 4] : v[c + 3];
+      }
+      return;
+    }
+  }
 #pragma unroll
   for (int c = 0; c < C; ++c) {
     if constexpr (sizeof(InT) == 1) {
