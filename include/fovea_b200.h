@@ -132,6 +132,25 @@ int fv_warp_perspective_f32(const float* src, int64_t src_img_stride, int64_t sr
                             int32_t dst_height, int32_t dst_width, int32_t channels, int32_t n,
                             const double* hinv_host, float border, void* stream);
 
+/* ---- the remaining imgproc kernels ---------------------------
+ * imgproc.flip_horizontal (imgproc.py:67-73) and imgproc.resize_nearest
+ * (imgproc.py:81-97, round-half-down pixel-centre index in f64): any element
+ * type of elem_size 1, 2, 4 or 8 bytes, pure indexing (bit-exact).
+ * imgproc.sobel (imgproc.py:126-155): f32, 3x3, replicate border, unnormalised
+ * magnitude, NumPy's f32 op order. */
+int fv_resize_nearest(const void* src, int64_t src_img_stride, int64_t src_row_pitch,
+                      int32_t src_height, int32_t src_width,
+                      void* dst, int64_t dst_img_stride, int64_t dst_row_pitch,
+                      int32_t dst_height, int32_t dst_width,
+                      int32_t channels, int32_t elem_size, int32_t n, void* stream);
+int fv_flip_horizontal(const void* src, int64_t src_img_stride, int64_t src_row_pitch,
+                       void* dst, int64_t dst_img_stride, int64_t dst_row_pitch,
+                       int32_t height, int32_t width, int32_t channels, int32_t elem_size, int32_t n,
+                       void* stream);
+int fv_sobel_f32(const float* src, int64_t src_img_stride, int64_t src_row_pitch,
+                 float* dst, int64_t dst_img_stride, int64_t dst_row_pitch,
+                 int32_t height, int32_t width, int32_t channels, int32_t n, void* stream);
+
 /* ---- tuning / introspection ---------------------------------------------
  * Resize kernel selection: 0 = auto (default: exact 2:1 / 1:2 fast paths,
  * else the staged TMA strip kernel, else the direct-gather kernel),

@@ -29,6 +29,7 @@ __all__ = [
     "invert_affine", "invert_homography", "affine_forward", "perspective_forward",
     "warp_affine", "warp_perspective",
     "gray_scalar", "bilinear_scalar", "warp_scalar", "resize_normalize_chw_scalar",
+    "flip_horizontal", "nearest_indices", "resize_nearest", "sobel",
 ]
 
 # BT.601 luma weights -- imgproc.py:27
@@ -411,3 +412,41 @@ def resize_normalize_chw_scalar(arr: np.ndarray, dst_w: int, dst_h: int, mean, s
                 v = _f32(_f32(u[y, x, ch]) / _f32(255.0))
                 out[ch, y, x] = _f32(_f32(v - m) / s)
     return out
+
+
+# --------------------------------------------------------------------------
+# flip, nearest, sobel -- imgproc.py:67-97, 126-155
+# --------------------------------------------------------------------------
+
+def flip_horizontal(a: np.ndarray) -> np.ndarray:
+    """imgproc.py:73: dst = src[:, ::-1, :]."""
+    return np.ascontiguousarray(a[:, ::-1, :])
+
+
+def nearest_indices(dst_n: int, src_n: int) -> np.ndarray:
+    """imgproc.py:81-86: ceil((i + 0.5) * scale) - 1, clipped (round half down)."""
+    scale = src_n / dst_n
+    z = (np.arange(dst_n, dtype=np.float64) + 0.5) * scale
+    return np.clip(np.ceil(z).astype(np.int64) - 1, 0, src_n - 1)
+
+
+def resize_nearest(a: np.ndarray, dst_w: int, dst_h: int) -> np.ndarray:
+    """imgproc.py:94-97."""
+    xi = nearest_indices(dst_w, a.shape[1])
+    yi = nearest_indices(dst_h, a.shape[0])
+    return np.ascontiguousarray(a[yi[:, None], xi[None, :], :])
+
+
+def sobel(a: np.ndarray) -> np.ndarray:
+    """imgproc.py:139-155: edge-padded 3x3 Sobel magnitude, f32 op order."""
+    p = np.pad(a, ((1, 1), (1, 1), (0, 0)), mode="edge")
+    left, right = p[1:-1, :-2, :], p[1:-1, 2:, :]
+    up, down = p[:-2, 1:-1, :], p[2:, 1:-1, :]
+    ul, ur = p[:-2, :-2, :], p[:-2, 2:, :]
+    dl, dr = p[2:, :-2, :], p[2:, 2:, :]
+    gx = (ur - ul) + 2.0 * (right - left) + (dr - dl)
+    gy = (dl - ul) + 2.0 * (down - up) + (dr - ur)
+    np.multiply(gx, gx, out=gx)
+    np.multiply(gy, gy, out=gy)
+    np.add(gx, gy, out=gx)
+    return np.sqrt(gx).astype(np.float32)

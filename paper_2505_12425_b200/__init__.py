@@ -10,6 +10,9 @@ functions on torch CUDA tensors):
     warp_affine(src, dst, m, border=0)         builder contract
     warp_perspective(src, dst, h, border=0)    builder contract
     resize_normalize_chw(src, dst, mean, std)  fused preprocessing
+    resize_nearest(src, dst)                   imgproc.py:89-97
+    flip_horizontal(src, dst)                  imgproc.py:67-73
+    sobel(src, dst, 3)                         imgproc.py:126-155
 
 Every call is one sm_100a kernel launch through the C ABI in
 include/fovea_b200.h; there is no CPU fallback.
@@ -24,14 +27,18 @@ from .errors import (  # noqa: F401
     SizeMismatch,
     UnsupportedDevice,
     UnsupportedDtype,
+    UnsupportedKernelSize,
 )
 from .image import to_float_scaled  # noqa: F401
 from .imgproc import (  # noqa: F401
+    flip_horizontal,
     gray_from_rgb,
     normalize_lut,
     resize_bilinear,
     resize_bilinear_u8,
+    resize_nearest,
     resize_normalize_chw,
+    sobel,
     warp_affine,
     warp_perspective,
 )

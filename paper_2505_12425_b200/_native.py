@@ -39,6 +39,9 @@ SIGNATURES = {
                                 _P], _c.c_int),
     "fv_warp_perspective_f32": ([_P, _I64, _I64, _I32, _I32, _P, _I64, _I64, _I32, _I32, _I32, _I32, _P, _c.c_float,
                                  _P], _c.c_int),
+    "fv_resize_nearest": ([_P, _I64, _I64, _I32, _I32, _P, _I64, _I64, _I32, _I32, _I32, _I32, _I32, _P], _c.c_int),
+    "fv_flip_horizontal": (_IMG2 + [_I32, _I32, _I32, _I32, _I32, _P], _c.c_int),
+    "fv_sobel_f32": (_IMG2 + [_I32, _I32, _I32, _I32, _P], _c.c_int),
 }
 
 _lib = None

@@ -1,0 +1,144 @@
+// fv_geom.cu -- SURVEY §8(f) rank 1 and 3: the rest of the reference's
+// imgproc kernels on the same boundary.
+//   imgproc.flip_horizontal  (imgproc.py:67-73)   any dtype, pure indexing
+//   imgproc.resize_nearest   (imgproc.py:81-97)   any dtype, pure indexing
+//   imgproc.sobel            (imgproc.py:126-155) f32, 3x3, replicate border
+// Indexing work is bit-exact by construction; sobel reproduces the NumPy op
+// order (each f32 op separately rounded, correctly rounded sqrt).
+#include "fv_common.cuh"
+
+namespace fv {
+
+// _nearest_indices (imgproc.py:81-86): z = (i + 0.5) * (src_n / dst_n) in f64,
+// idx = clip(ceil(z) - 1, 0, src_n - 1)  (round-half-down of the centre)
+__device__ __forceinline__ int nearest_index(int i, double scale, int src_n) {
+  const double z = __dmul_rn(__dadd_rn((double)i, 0.5), scale);
+  const int idx = (int)ceil(z) - 1;
+  return min(max(idx, 0), src_n - 1);
+}
+
+template <typename T>
+__device__ __forceinline__ void copy_px(T* d, const T* s, int c) {
+  for (int k = 0; k < c; ++k) d[k] = s[k];
+}
+
+// one destination pixel per thread; T is the element type (1/2/4/8 bytes)
+template <typename T>
+__global__ void nearest_kernel(const char* __restrict__ src, int64_t s_is, int64_t s_rp, int sh, int sw,
+                               char* __restrict__ dst, int64_t d_is, int64_t d_rp, int dh, int dw, int c,
+                               double scale_x, double scale_y) {
+  const int n = blockIdx.z;
+  const int x = blockIdx.x * blockDim.x + threadIdx.x;
+  if (x >= dw) return;
+  const int sx = nearest_index(x, scale_x, sw);
+  for (int y = blockIdx.y; y < dh; y += gridDim.y) {
+    const int sy = nearest_index(y, scale_y, sh);
+    const T* s = reinterpret_cast<const T*>(src + n * s_is + (int64_t)sy * s_rp) + (int64_t)sx * c;
+    T* d = reinterpret_cast<T*>(dst + n * d_is + (int64_t)y * d_rp) + (int64_t)x * c;
+    copy_px(d, s, c);
+  }
+}
+
+template <typename T>
+__global__ void flip_kernel(const char* __restrict__ src, int64_t s_is, int64_t s_rp, char* __restrict__ dst,
+                            int64_t d_is, int64_t d_rp, int h, int w, int c) {
+  const int n = blockIdx.z;
+  const int x = blockIdx.x * blockDim.x + threadIdx.x;
+  if (x >= w) return;
+  for (int y = blockIdx.y; y < h; y += gridDim.y) {
+    const T* s = reinterpret_cast<const T*>(src + n * s_is + (int64_t)y * s_rp) + (int64_t)(w - 1 - x) * c;
+    T* d = reinterpret_cast<T*>(dst + n * d_is + (int64_t)y * d_rp) + (int64_t)x * c;
+    copy_px(d, s, c);
+  }
+}
+
+// imgproc.py:139-155. p = edge-padded source; for each pixel and channel
+//   gx = ((ur - ul) + 2*(right - left)) + (dr - dl)
+//   gy = ((dl - ul) + 2*(down - up)) + (dr - ur)
+//   out = sqrt(RN(gx*gx) + RN(gy*gy))          (f32, each op rounded)
+__global__ void sobel_kernel(const char* __restrict__ src, int64_t s_is, int64_t s_rp, char* __restrict__ dst,
+                             int64_t d_is, int64_t d_rp, int h, int w, int c) {
+  const int n = blockIdx.z;
+  const int x = blockIdx.x * blockDim.x + threadIdx.x;
+  if (x >= w) return;
+  const int xl = max(x - 1, 0), xr = min(x + 1, w - 1);
+  for (int y = blockIdx.y; y < h; y += gridDim.y) {
+    const int yu = max(y - 1, 0), yd = min(y + 1, h - 1);
+    const float* ru = reinterpret_cast<const float*>(src + n * s_is + (int64_t)yu * s_rp);
+    const float* rm = reinterpret_cast<const float*>(src + n * s_is + (int64_t)y * s_rp);
+    const float* rd = reinterpret_cast<const float*>(src + n * s_is + (int64_t)yd * s_rp);
+    float* d = reinterpret_cast<float*>(dst + n * d_is + (int64_t)y * d_rp) + (int64_t)x * c;
+    for (int k = 0; k < c; ++k) {
+      const float ul = __ldg(ru + xl * c + k), up = __ldg(ru + x * c + k), ur = __ldg(ru + xr * c + k);
+      const float left = __ldg(rm + xl * c + k), right = __ldg(rm + xr * c + k);
+      const float dl = __ldg(rd + xl * c + k), down = __ldg(rd + x * c + k), dr = __ldg(rd + xr * c + k);
+      const float gx = __fadd_rn(__fadd_rn(__fsub_rn(ur, ul), __fmul_rn(2.0f, __fsub_rn(right, left))), __fsub_rn(dr, dl));
+      const float gy = __fadd_rn(__fadd_rn(__fsub_rn(dl, ul), __fmul_rn(2.0f, __fsub_rn(down, up))), __fsub_rn(dr, ur));
+      d[k] = __fsqrt_rn(__fadd_rn(__fmul_rn(gx, gx), __fmul_rn(gy, gy)));
+    }
+  }
+}
+
+static int check_geom(const void* src, const void* dst, int n, int sh, int sw, int dh, int dw, int c, int es,
+                      const char* fn) {
+  if (n < 0 || sh < 1 || sw < 1 || dh < 1 || dw < 1 || c < 1)
+    return set_error(FV_EINVAL, "%s: bad shape n=%d src=%dx%d dst=%dx%d c=%d", fn, n, sh, sw, dh, dw, c);
+  if (es != 1 && es != 2 && es != 4 && es != 8) return set_error(FV_EINVAL, "%s: element size %d", fn, es);
+  if (n > 65535) return set_error(FV_EINVAL, "%s: batch %d exceeds 65535", fn, n);
+  if (n > 0 && (!src || !dst)) return set_error(FV_EINVAL, "%s: null pointer", fn);
+  return FV_OK;
+}
+
+}  // namespace fv
+
+using namespace fv;
+
+extern "C" {
+
+int fv_resize_nearest(const void* src, int64_t s_is, int64_t s_rp, int32_t sh, int32_t sw, void* dst, int64_t d_is,
+                      int64_t d_rp, int32_t dh, int32_t dw, int32_t c, int32_t elem_size, int32_t n, void* stream) {
+  int rc = check_geom(src, dst, n, sh, sw, dh, dw, c, elem_size, "fv_resize_nearest");
+  if (rc || n == 0) return rc;
+  const double sx = (double)sw / (double)dw, sy = (double)sh / (double)dh;  // imgproc.py:83
+  dim3 grid((dw + 127) / 128, dh < 65535 ? dh : 65535, n);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const char* s = static_cast<const char*>(src);
+  char* d = static_cast<char*>(dst);
+  switch (elem_size) {
+    case 1: nearest_kernel<uint8_t><<<grid, 128, 0, st>>>(s, s_is, s_rp, sh, sw, d, d_is, d_rp, dh, dw, c, sx, sy); break;
+    case 2: nearest_kernel<uint16_t><<<grid, 128, 0, st>>>(s, s_is, s_rp, sh, sw, d, d_is, d_rp, dh, dw, c, sx, sy); break;
+    case 4: nearest_kernel<uint32_t><<<grid, 128, 0, st>>>(s, s_is, s_rp, sh, sw, d, d_is, d_rp, dh, dw, c, sx, sy); break;
+    default: nearest_kernel<uint64_t><<<grid, 128, 0, st>>>(s, s_is, s_rp, sh, sw, d, d_is, d_rp, dh, dw, c, sx, sy); break;
+  }
+  return check_launch("fv_resize_nearest");
+}
+
+int fv_flip_horizontal(const void* src, int64_t s_is, int64_t s_rp, void* dst, int64_t d_is, int64_t d_rp,
+                       int32_t h, int32_t w, int32_t c, int32_t elem_size, int32_t n, void* stream) {
+  int rc = check_geom(src, dst, n, h, w, h, w, c, elem_size, "fv_flip_horizontal");
+  if (rc || n == 0) return rc;
+  dim3 grid((w + 127) / 128, h < 65535 ? h : 65535, n);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const char* s = static_cast<const char*>(src);
+  char* d = static_cast<char*>(dst);
+  switch (elem_size) {
+    case 1: flip_kernel<uint8_t><<<grid, 128, 0, st>>>(s, s_is, s_rp, d, d_is, d_rp, h, w, c); break;
+    case 2: flip_kernel<uint16_t><<<grid, 128, 0, st>>>(s, s_is, s_rp, d, d_is, d_rp, h, w, c); break;
+    case 4: flip_kernel<uint32_t><<<grid, 128, 0, st>>>(s, s_is, s_rp, d, d_is, d_rp, h, w, c); break;
+    default: flip_kernel<uint64_t><<<grid, 128, 0, st>>>(s, s_is, s_rp, d, d_is, d_rp, h, w, c); break;
+  }
+  return check_launch("fv_flip_horizontal");
+}
+
+int fv_sobel_f32(const float* src, int64_t s_is, int64_t s_rp, float* dst, int64_t d_is, int64_t d_rp, int32_t h,
+                 int32_t w, int32_t c, int32_t n, void* stream) {
+  int rc = check_geom(src, dst, n, h, w, h, w, c, 4, "fv_sobel_f32");
+  if (rc || n == 0) return rc;
+  if ((s_is | s_rp | d_is | d_rp) & 3) return set_error(FV_EINVAL, "fv_sobel_f32: strides not f32-aligned");
+  dim3 grid((w + 127) / 128, h < 65535 ? h : 65535, n);
+  sobel_kernel<<<grid, 128, 0, static_cast<cudaStream_t>(stream)>>>(reinterpret_cast<const char*>(src), s_is, s_rp,
+                                                                    reinterpret_cast<char*>(dst), d_is, d_rp, h, w, c);
+  return check_launch("fv_sobel_f32");
+}
+
+}  // extern "C"

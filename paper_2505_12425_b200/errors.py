@@ -32,6 +32,10 @@ class AliasedBuffers(FoveaError):
     """Source and destination share storage where they must be distinct (errors.py:58-59)."""
 
 
+class UnsupportedKernelSize(FoveaError):
+    """Filter kernel size outside the supported set (errors.py:62-63)."""
+
+
 class UnsupportedDevice(FoveaError):
     """Tensor is not resident on a CUDA device (there is no CPU path)."""
 

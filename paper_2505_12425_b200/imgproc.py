@@ -18,11 +18,11 @@ import torch
 
 from . import _native
 from ._tensors import F32, U8, as_image, as_planar, check_distinct, same_device, stream_ptr
-from .errors import ShapeMismatch, SingularTransform, SizeMismatch, UnsupportedDtype
+from .errors import ShapeMismatch, SingularTransform, SizeMismatch, UnsupportedDtype, UnsupportedKernelSize
 
 __all__ = [
     "gray_from_rgb", "resize_bilinear", "resize_bilinear_u8", "resize_normalize_chw",
-    "warp_affine", "warp_perspective", "normalize_lut",
+    "warp_affine", "warp_perspective", "normalize_lut", "flip_horizontal", "resize_nearest", "sobel",
 ]
 
 
@@ -208,3 +208,61 @@ def warp_perspective(src: torch.Tensor, dst: torch.Tensor, h, border=0, inverse:
     the forward 3x3 homography (or N of them), inverted once in f64 on the
     host. Pixels whose inverse-mapped W is 0 get the raw border value."""
     _warp(src, dst, h, border, inverse, perspective=True)
+
+
+# ---------------------------------------------------------------------------
+# SURVEY §8(f): flip, nearest, sobel
+# ---------------------------------------------------------------------------
+
+def flip_horizontal(src: torch.Tensor, dst: torch.Tensor) -> None:
+    """dst(y, x) = src(y, width-1-x), all channels (imgproc.py:67-73). Any
+    dtype of 1, 2, 4 or 8 bytes. Checks: layout (channels, dtype) ->
+    SizeMismatch, size -> SizeMismatch, distinct -> AliasedBuffers."""
+    s, d = as_image(src, "src"), as_image(dst, "dst")
+    if s.c != d.c or s.dtype != d.dtype:
+        raise SizeMismatch(f"source {s!r} and destination {d!r} differ in layout")
+    if s.size != d.size:
+        raise SizeMismatch(f"source {s!r} and destination {d!r} differ in size")
+    check_distinct(src, dst)
+    _check_batch(s, d)
+    same_device(src, dst)
+    with torch.cuda.device(src.device):
+        _native.call("fv_flip_horizontal", s.ptr, s.img_stride, s.row_pitch, d.ptr, d.img_stride, d.row_pitch,
+                     s.h, s.w, s.c, src.element_size(), s.n, stream_ptr(src))
+
+
+def resize_nearest(src: torch.Tensor, dst: torch.Tensor) -> None:
+    """Nearest-neighbour resize to dst's size (imgproc.py:89-97): index
+    clip(ceil((x + 0.5) * src_n / dst_n) - 1, 0, src_n - 1) per axis (round
+    half down of the pixel centre), any dtype of 1, 2, 4 or 8 bytes."""
+    s, d = as_image(src, "src"), as_image(dst, "dst")
+    if s.c != d.c or s.dtype != d.dtype:
+        raise SizeMismatch(f"source {s!r} and destination {d!r} differ in layout")
+    check_distinct(src, dst)
+    _check_batch(s, d)
+    same_device(src, dst)
+    with torch.cuda.device(src.device):
+        _native.call("fv_resize_nearest", s.ptr, s.img_stride, s.row_pitch, s.h, s.w, d.ptr, d.img_stride,
+                     d.row_pitch, d.h, d.w, s.c, src.element_size(), s.n, stream_ptr(src))
+
+
+def sobel(src: torch.Tensor, dst: torch.Tensor, kernel_size: int) -> None:
+    """Gradient magnitude sqrt(Gx^2 + Gy^2) per channel, replicate border
+    (imgproc.py:126-155), f32. Checks in the reference's order: kernel size
+    (UnsupportedKernelSize), dtype (UnsupportedDtype), channels and size
+    (SizeMismatch), distinct (AliasedBuffers)."""
+    if kernel_size != 3:
+        raise UnsupportedKernelSize(f"only kernel_size 3 is supported, got {kernel_size}")
+    s, d = as_image(src, "src"), as_image(dst, "dst")
+    if s.dtype != F32 or d.dtype != F32:
+        raise UnsupportedDtype(f"sobel requires f32 images, got {s.dtype} -> {d.dtype}")
+    if s.c != d.c:
+        raise SizeMismatch(f"source has {s.c} channels, destination {d.c}")
+    if s.size != d.size:
+        raise SizeMismatch(f"source {s!r} and destination {d!r} differ in size")
+    check_distinct(src, dst)
+    _check_batch(s, d)
+    same_device(src, dst)
+    with torch.cuda.device(src.device):
+        _native.call("fv_sobel_f32", s.ptr, s.img_stride, s.row_pitch, d.ptr, d.img_stride, d.row_pitch,
+                     s.h, s.w, s.c, s.n, stream_ptr(src))

@@ -6,7 +6,7 @@ Run once in the build container, where the read-only reference is mounted:
 
 It imports `fovea` from /root/reference/pkg/src and calls the reference's own
 functions — imgproc.gray_from_rgb (imgproc.py:43), imgproc.resize_bilinear
-(imgproc.py:100), image.to_float_scaled (image.py:150), Tensor.cast
+(imgproc.py:100), imgproc.flip_horizontal / resize_nearest / sobel (imgproc.py:67-155), image.to_float_scaled (image.py:150), Tensor.cast
 (tensor.py:265) and service.app._resize_u8 (app.py:64) — on small seeded
 inputs, and writes inputs + outputs to tests/golden/*.npz. The GPU box never
 reads /root/reference; tests there use only these committed fixtures.
@@ -76,6 +76,29 @@ def main() -> None:
         out[f"c{i}_src"] = a
         out[f"c{i}_dst"] = res.as_array().copy()
     np.savez_compressed(os.path.join(OUT, "resize_u8.npz"), **out)
+
+    # ---- flip (imgproc.py:67), nearest (:89), sobel (:126) ----
+    out = {}
+    for i, (h, w, c, dt) in enumerate([(7, 13, 3, np.uint8), (5, 9, 4, np.uint8), (6, 5, 2, np.float32),
+                                       (3, 4, 1, np.uint16)]):
+        a = (rng.integers(0, 60000, (h, w, c)).astype(dt) if dt != np.float32 else rng.random((h, w, c), dtype=dt))
+        dst = ImageType(dt, c).from_size_val(ImageSize(w, h), 0)
+        imgproc.flip_horizontal(Image.from_array(a), dst)
+        out[f"flip{i}_src"], out[f"flip{i}_dst"] = a, dst.as_array().copy()
+    for i, (sw, sh, dw, dh, c, dt) in enumerate([(7, 5, 13, 3, 3, np.uint8), (16, 16, 5, 9, 3, np.uint8),
+                                                  (3, 3, 3, 3, 3, np.uint8), (1, 1, 4, 4, 3, np.uint8),
+                                                  (12, 7, 25, 4, 2, np.float32), (9, 9, 6, 14, 1, np.uint16)]):
+        a = (rng.integers(0, 60000, (sh, sw, c)).astype(dt) if dt != np.float32 else rng.random((sh, sw, c), dtype=dt))
+        dst = ImageType(dt, c).from_size_val(ImageSize(dw, dh), 0)
+        imgproc.resize_nearest(Image.from_array(a), dst)
+        out[f"near{i}_src"], out[f"near{i}_dst"] = a, dst.as_array().copy()
+    ramp = np.tile(np.arange(6, dtype=np.float32)[None, :, None], (5, 1, 1))
+    for i, a in enumerate([rng.random((9, 12, 3), dtype=np.float32), np.full((5, 5, 1), 3.25, np.float32), ramp,
+                           rng.random((8, 8, 1), dtype=np.float32)]):
+        dst = ImageType(np.float32, a.shape[2]).from_size_val(ImageSize(a.shape[1], a.shape[0]), 0.0)
+        imgproc.sobel(Image.from_array(a), dst, 3)
+        out[f"sobel{i}_src"], out[f"sobel{i}_dst"] = a, dst.as_array().copy()
+    np.savez_compressed(os.path.join(OUT, "geom.npz"), **out)
 
     # ---- to_float_scaled for every u8 value; cast KATs ---------------------
     u = np.arange(256, dtype=np.uint8).reshape(1, 256, 1)

@@ -150,3 +150,31 @@ class TestBuilderContracts:
         from paper_2505_12425_b200.imgproc import normalize_lut
 
         assert np.array_equal(normalize_lut(synth.MEAN, synth.STD), O.normalize_lut(synth.MEAN, synth.STD))
+
+
+class TestGeomGolden:
+    """flip / nearest / sobel restatements vs the reference's outputs."""
+
+    def test_flip(self):
+        g = golden("geom.npz")
+        for i in range(4):
+            assert np.array_equal(O.flip_horizontal(g[f"flip{i}_src"]), g[f"flip{i}_dst"])
+
+    def test_nearest(self):
+        g = golden("geom.npz")
+        for i in range(6):
+            d = g[f"near{i}_dst"]
+            assert np.array_equal(O.resize_nearest(g[f"near{i}_src"], d.shape[1], d.shape[0]), d)
+
+    def test_sobel(self):
+        g = golden("geom.npz")
+        for i in range(4):
+            assert np.array_equal(O.sobel(g[f"sobel{i}_src"]), g[f"sobel{i}_dst"])
+
+    def test_reference_kats(self):
+        # pkg/tests/test_imgproc.py:61-105
+        assert O.resize_nearest(np.array([[[10], [200]]], np.uint8), 4, 1).ravel().tolist() == [10, 10, 200, 200]
+        assert O.resize_nearest(np.array([[[1], [2], [3], [4]]], np.uint8), 2, 1).ravel().tolist() == [1, 3]
+        assert O.flip_horizontal(np.array([[[10], [20]]], np.uint8)).ravel().tolist() == [20, 10]
+        ramp = np.tile(np.arange(6, dtype=np.float32)[None, :, None], (5, 1, 1))
+        assert np.allclose(O.sobel(ramp)[1:-1, 1:-1, 0], 8.0)
