@@ -52,6 +52,102 @@ __global__ void flip_kernel(const char* __restrict__ src, int64_t s_is, int64_t 
   }
 }
 
+// ---------------------------------------------------------------------------
+// vectorised paths: a thread owns 16 destination pixels of S bytes (16*S bytes,
+// S 16-byte stores) and walks a band of rows with its column indices fixed.
+// ---------------------------------------------------------------------------
+template <int S>
+struct Px16 {
+  uint32_t w[4 * S];  // 16 pixels x S bytes
+};
+
+// byte i of the 16-pixel block, compile-time i after unrolling
+template <int S>
+__device__ __forceinline__ uint32_t blk_byte(const Px16<S>& b, int i) {
+  return (b.w[i >> 2] >> ((i & 3) * 8)) & 0xFFu;
+}
+
+// flip: destination block g of a row is the reverse of source block
+// (w/16 - 1 - g); pixel order reversed in registers (w % 16 == 0, aligned rows)
+template <int S>
+__global__ void __launch_bounds__(128) flip16_kernel(const char* __restrict__ src, int64_t s_is, int64_t s_rp,
+                                                     char* __restrict__ dst, int64_t d_is, int64_t d_rp, int h,
+                                                     int w) {
+  const int n = blockIdx.z;
+  const int groups = w / 16;
+  const int g = blockIdx.x * blockDim.x + threadIdx.x;
+  if (g >= groups) return;
+  for (int y = blockIdx.y; y < h; y += gridDim.y) {
+    const uint4* s4 = reinterpret_cast<const uint4*>(src + n * s_is + (int64_t)y * s_rp + (int64_t)(groups - 1 - g) * 16 * S);
+    uint4* d4 = reinterpret_cast<uint4*>(dst + n * d_is + (int64_t)y * d_rp + (int64_t)g * 16 * S);
+    Px16<S> in;
+#pragma unroll
+    for (int i = 0; i < S; ++i) {
+      const uint4 v = __ldg(s4 + i);
+      in.w[4 * i] = v.x, in.w[4 * i + 1] = v.y, in.w[4 * i + 2] = v.z, in.w[4 * i + 3] = v.w;
+    }
+    uint32_t out[4 * S];
+#pragma unroll
+    for (int q = 0; q < 4 * S; ++q) {
+      uint32_t b[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int o = 4 * q + j, p = o / S, k = o % S;
+        b[j] = blk_byte(in, (15 - p) * S + k);
+      }
+      out[q] = b[0] | (b[1] << 8) | (b[2] << 16) | (b[3] << 24);
+    }
+#pragma unroll
+    for (int i = 0; i < S; ++i) __stcs(d4 + i, make_uint4(out[4 * i], out[4 * i + 1], out[4 * i + 2], out[4 * i + 3]));
+  }
+}
+
+// pixel of S bytes at byte offset `off` of a row (S = 3: three byte loads)
+template <int S>
+__device__ __forceinline__ void load_px(const char* p, uint8_t (&v)[S]) {
+#pragma unroll
+  for (int k = 0; k < S; ++k) v[k] = __ldg(reinterpret_cast<const uint8_t*>(p) + k);
+}
+
+// nearest: the thread's 16 source column indices are computed once (f64,
+// imgproc.py:81-86); each row gathers 16 pixels through L1 and writes S
+// 16-byte vectors (dw % 16 == 0, aligned destination rows)
+template <int S>
+__global__ void __launch_bounds__(128) nearest16_kernel(const char* __restrict__ src, int64_t s_is, int64_t s_rp,
+                                                        int sh, int sw, char* __restrict__ dst, int64_t d_is,
+                                                        int64_t d_rp, int dh, int dw, double scale_x,
+                                                        double scale_y, int rows_per_cta) {
+  const int n = blockIdx.z;
+  const int g = blockIdx.x * blockDim.x + threadIdx.x;
+  if (g >= dw / 16) return;
+  int sx[16];
+#pragma unroll
+  for (int p = 0; p < 16; ++p) sx[p] = nearest_index(g * 16 + p, scale_x, sw) * S;
+  const int y0 = blockIdx.y * rows_per_cta, y1 = min(y0 + rows_per_cta, dh);
+  for (int y = y0; y < y1; ++y) {
+    const char* srow = src + n * s_is + (int64_t)nearest_index(y, scale_y, sh) * s_rp;
+    uint8_t px[16][S];
+#pragma unroll
+    for (int p = 0; p < 16; ++p) load_px<S>(srow + sx[p], px[p]);
+    uint32_t out[4 * S];
+#pragma unroll
+    for (int q = 0; q < 4 * S; ++q) {
+      uint32_t b[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int o = 4 * q + j;
+        b[j] = px[o / S][o % S];
+      }
+      out[q] = b[0] | (b[1] << 8) | (b[2] << 16) | (b[3] << 24);
+    }
+    uint4* d4 = reinterpret_cast<uint4*>(dst + n * d_is + (int64_t)y * d_rp + (int64_t)g * 16 * S);
+#pragma unroll
+    for (int i = 0; i < S; ++i) __stcs(d4 + i, make_uint4(out[4 * i], out[4 * i + 1], out[4 * i + 2], out[4 * i + 3]));
+  }
+}
+
+static inline bool al16v(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
+
 // imgproc.py:139-155. p = edge-padded source; for each pixel and channel
 //   gx = ((ur - ul) + 2*(right - left)) + (dr - dl)
 //   gy = ((dl - ul) + 2*(down - up)) + (dr - ur)
@@ -100,10 +196,20 @@ int fv_resize_nearest(const void* src, int64_t s_is, int64_t s_rp, int32_t sh, i
   int rc = check_geom(src, dst, n, sh, sw, dh, dw, c, elem_size, "fv_resize_nearest");
   if (rc || n == 0) return rc;
   const double sx = (double)sw / (double)dw, sy = (double)sh / (double)dh;  // imgproc.py:83
-  dim3 grid((dw + 127) / 128, dh < 65535 ? dh : 65535, n);
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const char* s = static_cast<const char*>(src);
   char* d = static_cast<char*>(dst);
+  const int S = c * elem_size;
+  if ((S == 3 || S == 4) && dw % 16 == 0 && al16v(dst) && ((d_is | d_rp) & 15) == 0) {
+    const int rows = 16;
+    dim3 g16((dw / 16 + 127) / 128, (dh + rows - 1) / rows, n);
+    if (S == 3)
+      nearest16_kernel<3><<<g16, 128, 0, st>>>(s, s_is, s_rp, sh, sw, d, d_is, d_rp, dh, dw, sx, sy, rows);
+    else
+      nearest16_kernel<4><<<g16, 128, 0, st>>>(s, s_is, s_rp, sh, sw, d, d_is, d_rp, dh, dw, sx, sy, rows);
+    return check_launch("fv_resize_nearest");
+  }
+  dim3 grid((dw + 127) / 128, dh < 65535 ? dh : 65535, n);
   switch (elem_size) {
     case 1: nearest_kernel<uint8_t><<<grid, 128, 0, st>>>(s, s_is, s_rp, sh, sw, d, d_is, d_rp, dh, dw, c, sx, sy); break;
     case 2: nearest_kernel<uint16_t><<<grid, 128, 0, st>>>(s, s_is, s_rp, sh, sw, d, d_is, d_rp, dh, dw, c, sx, sy); break;
@@ -117,10 +223,22 @@ int fv_flip_horizontal(const void* src, int64_t s_is, int64_t s_rp, void* dst, i
                        int32_t h, int32_t w, int32_t c, int32_t elem_size, int32_t n, void* stream) {
   int rc = check_geom(src, dst, n, h, w, h, w, c, elem_size, "fv_flip_horizontal");
   if (rc || n == 0) return rc;
-  dim3 grid((w + 127) / 128, h < 65535 ? h : 65535, n);
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const char* s = static_cast<const char*>(src);
   char* d = static_cast<char*>(dst);
+  const int S = c * elem_size;
+  if ((S == 1 || S == 3 || S == 4 || S == 12) && w % 16 == 0 && al16v(src) && al16v(dst) &&
+      ((s_is | s_rp | d_is | d_rp) & 15) == 0) {
+    dim3 g16((w / 16 + 127) / 128, h < 65535 ? h : 65535, n);
+    switch (S) {
+      case 1: flip16_kernel<1><<<g16, 128, 0, st>>>(s, s_is, s_rp, d, d_is, d_rp, h, w); break;
+      case 3: flip16_kernel<3><<<g16, 128, 0, st>>>(s, s_is, s_rp, d, d_is, d_rp, h, w); break;
+      case 4: flip16_kernel<4><<<g16, 128, 0, st>>>(s, s_is, s_rp, d, d_is, d_rp, h, w); break;
+      default: flip16_kernel<12><<<g16, 128, 0, st>>>(s, s_is, s_rp, d, d_is, d_rp, h, w); break;
+    }
+    return check_launch("fv_flip_horizontal");
+  }
+  dim3 grid((w + 127) / 128, h < 65535 ? h : 65535, n);
   switch (elem_size) {
     case 1: flip_kernel<uint8_t><<<grid, 128, 0, st>>>(s, s_is, s_rp, d, d_is, d_rp, h, w, c); break;
     case 2: flip_kernel<uint16_t><<<grid, 128, 0, st>>>(s, s_is, s_rp, d, d_is, d_rp, h, w, c); break;

@@ -145,3 +145,22 @@ def test_empty_batch_is_a_no_op():
     fv.resize_bilinear_u8(src, dst)
     fv.flip_horizontal(src, torch.zeros_like(src))
     torch.cuda.synchronize()
+
+
+@pytest.mark.parametrize("dtype,c", [(np.uint8, 1), (np.uint8, 3), (np.uint8, 4), (np.float32, 3), (np.float32, 1),
+                                     (np.uint16, 3)])
+def test_flip_and_nearest_vector_paths(rng, dtype, c):
+    """16-pixel vectorised kernels (width % 16 == 0) and the generic ones
+    (ragged widths), batched, vs the oracle."""
+    for (h, w, dh, dw) in [(9, 64, 18, 128), (5, 48, 7, 32), (6, 37, 11, 21)]:
+        a = (rng.integers(0, 60000, (2, h, w, c)).astype(dtype) if dtype != np.float32
+             else rng.random((2, h, w, c), dtype=np.float32))
+        t = cu(a)
+        f = torch.zeros_like(t)
+        fv.flip_horizontal(t, f)
+        nn = torch.zeros((2, dh, dw, c), dtype=t.dtype, device=DEV)
+        fv.resize_nearest(t, nn)
+        fo, no = host(f), host(nn)
+        for i in range(2):
+            assert np.array_equal(fo[i], O.flip_horizontal(a[i]))
+            assert np.array_equal(no[i], O.resize_nearest(a[i], dw, dh))
