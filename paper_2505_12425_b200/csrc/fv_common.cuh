@@ -138,11 +138,15 @@ template <int N>
 __device__ __forceinline__ uint32_t magic_of(const uint32_t (&w)[N], int i) {
   return __byte_perm(w[i >> 2], 0x4B000000u, 0x7440 + (i & 3));
 }
+// The runtime {1.0f, 1.0f} pair, passed as a 64-bit kernel argument so that
+// it stays in a uniform register pair (ptxas cannot know its value).
+constexpr f2_t kOne2Bits = 0x3F8000003F800000ull;
+
 // y = RN(v * scale) then the u8 epilogue; returns the two float-bit words
-// whose low bytes are the results. `one` must be a runtime 1.0f.
-__device__ __forceinline__ f2_t scale_to_u8_bits2(f2_t v, float scale, float one) {
+// whose low bytes are the results. `one2` must be the runtime {1, 1} pair.
+__device__ __forceinline__ f2_t scale_to_u8_bits2(f2_t v, float scale, f2_t one2) {
   const f2_t y = fmul2(v, f2(scale, scale));
-  const f2_t t = ffma2(y, f2(one, one), f2(0.5f, 0.5f));
+  const f2_t t = ffma2(y, one2, f2(0.5f, 0.5f));
   return fadd2_rd(t, f2(8388608.0f, 8388608.0f));
 }
 // low bytes of two pairs -> one word

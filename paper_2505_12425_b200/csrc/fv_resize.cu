@@ -45,7 +45,7 @@ struct ResizeArgs {
   // strip kernel only
   int tile_px, band_rows, tiles_x, slot_bytes;
   int vec_store;
-  float one;  // runtime 1.0f (f32x2 contraction guard, fv_common.cuh)
+  f2_t one2;  // runtime {1.0f, 1.0f} (f32x2 contraction guard, fv_common.cuh)
 };
 
 struct LutArg {
@@ -226,7 +226,7 @@ __global__ void __launch_bounds__(StripCfg<InT, C, MODE>::NT, 3)
   const int all_copy = __syncthreads_and(hcopy);
   const int all_fma = __syncthreads_and(hfma);
   const int hmode = all_copy ? 2 : (all_fma ? 1 : 0);
-  const float one = a.one;
+  const f2_t one = a.one2;
 
   constexpr int NP = EPT / 2;  // element pairs (packed f32x2)
   f2_t ha[NP], hb[NP];
@@ -252,7 +252,7 @@ __global__ void __launch_bounds__(StripCfg<InT, C, MODE>::NT, 3)
       } else if (hmode == 1) {
         h[p] = ffma2(vb, f2(WB(e), WB(e + 1)), fmul2(va, f2(WA(e), WA(e + 1))));
       } else {
-        h[p] = ffma2(fmul2(vb, f2(WB(e), WB(e + 1))), f2(one, one), fmul2(va, f2(WA(e), WA(e + 1))));
+        h[p] = ffma2(fmul2(vb, f2(WB(e), WB(e + 1))), one, fmul2(va, f2(WA(e), WA(e + 1))));
       }
     }
     __syncwarp();
@@ -292,7 +292,7 @@ __global__ void __launch_bounds__(StripCfg<InT, C, MODE>::NT, 3)
       for (int p = 0; p < NP; ++p) o[p] = ffma2(ha[p], WY0, fmul2(hb[p], WY1));
     } else {
 #pragma unroll
-      for (int p = 0; p < NP; ++p) o[p] = ffma2(fmul2(hb[p], WY1), f2(one, one), fmul2(ha[p], WY0));
+      for (int p = 0; p < NP; ++p) o[p] = ffma2(fmul2(hb[p], WY1), one, fmul2(ha[p], WY0));
     }
 
     const int y = yb + i;
@@ -430,7 +430,7 @@ static ResizeArgs make_args(const void* src, int64_t s_is, int64_t s_rp, int sh,
   a.scale_y = (double)sh / (double)dh;
   const bool dst_al = (reinterpret_cast<uintptr_t>(dst) & 3) == 0 && (d_is & 3) == 0 && (d_rp & 3) == 0;
   a.vec_store = dst_al ? 1 : 0;
-  a.one = 1.0f;
+  a.one2 = kOne2Bits;
   (void)out_elem;
   return a;
 }

@@ -37,7 +37,7 @@ struct FastArgs {
   int groups;  // column groups per row
   int band;    // up2: source rows per band
   int bands;
-  float one;   // runtime 1.0f (see fv_common.cuh: f32x2 contraction guard)
+  f2_t one2;   // runtime {1.0f, 1.0f} (see fv_common.cuh: f32x2 contraction guard)
   int slot_bytes;
 };
 
@@ -88,7 +88,7 @@ __global__ void __launch_bounds__(128) resize_down2_kernel(const __grid_constant
                                unit2(magic_of(w0, o0 + C), magic_of(w0, o1 + C)));
         const f2_t bot = fadd2(unit2(magic_of(w1, o0), magic_of(w1, o1)),
                                unit2(magic_of(w1, o0 + C), magic_of(w1, o1 + C)));
-        r[j] = scale_to_u8_bits2(fadd2(top, bot), K, a.one);
+        r[j] = scale_to_u8_bits2(fadd2(top, bot), K, a.one2);
       }
       out[q] = pack4x2(r[0], r[1]);
     }
@@ -159,7 +159,7 @@ __device__ __forceinline__ void up2_h(const uint32_t (&w)[Up2<C>::NW], int t, in
 // one destination row from two h rows: o = fma(hb, 0.25, qa), epilogue in
 // f32x2, packed 4 bytes at a time and written as 8-byte stores (8*C bytes)
 template <int C>
-__device__ __forceinline__ void up2_emit(uint8_t* drow, const f2_t (&hb)[4 * C], const f2_t (&qa)[4 * C], float one) {
+__device__ __forceinline__ void up2_emit(uint8_t* drow, const f2_t (&hb)[4 * C], const f2_t (&qa)[4 * C], f2_t one) {
 #pragma unroll
   for (int i = 0; i < C; ++i) {
     uint32_t w[2];
@@ -175,7 +175,7 @@ __device__ __forceinline__ void up2_emit(uint8_t* drow, const f2_t (&hb)[4 * C],
 }
 // a row that is a plain copy of h (clamped rows 0 and 2H-1, fy = 0)
 template <int C>
-__device__ __forceinline__ void up2_emit_copy(uint8_t* drow, const f2_t (&h)[4 * C], float one) {
+__device__ __forceinline__ void up2_emit_copy(uint8_t* drow, const f2_t (&h)[4 * C], f2_t one) {
 #pragma unroll
   for (int i = 0; i < C; ++i) {
     uint32_t w[2];
@@ -211,13 +211,13 @@ __device__ __forceinline__ void up2_step_s(uint8_t* dimg, const FastArgs& a, int
                                            f2_t (&q)[4 * C], f2_t (&hn)[4 * C]) {
   up2_h<C>(w, t, a.groups - 1, hn);
   if (k == 0) {
-    up2_emit_copy<C>(dimg, hn, a.one);
+    up2_emit_copy<C>(dimg, hn, a.one2);
   } else {
-    up2_emit<C>(dimg + (int64_t)(2 * k - 1) * a.d_rp, hn, q, a.one);
+    up2_emit<C>(dimg + (int64_t)(2 * k - 1) * a.d_rp, hn, q, a.one2);
   }
 #pragma unroll
   for (int e = 0; e < 4 * C; ++e) q[e] = fmul2(hn[e], f2(0.75f, 0.75f));
-  if (k > 0) up2_emit<C>(dimg + (int64_t)(2 * k) * a.d_rp, hp, q, a.one);
+  if (k > 0) up2_emit<C>(dimg + (int64_t)(2 * k) * a.d_rp, hp, q, a.one2);
 }
 
 template <int C>
@@ -297,10 +297,10 @@ __global__ void __launch_bounds__((UP2_NCW + 1) * 32, 4) resize_up2_kernel(const
     take(k);
     if (active) {
       up2_step_s<C>(dimg, a, t, k, w, h0, q, h1);
-      if (k1 == a.sh) up2_emit_copy<C>(dimg + (int64_t)(2 * a.sh - 1) * a.d_rp, h1, a.one);
+      if (k1 == a.sh) up2_emit_copy<C>(dimg + (int64_t)(2 * a.sh - 1) * a.d_rp, h1, a.one2);
     }
   } else if (k1 == a.sh && active) {
-    up2_emit_copy<C>(dimg + (int64_t)(2 * a.sh - 1) * a.d_rp, h0, a.one);
+    up2_emit_copy<C>(dimg + (int64_t)(2 * a.sh - 1) * a.d_rp, h0, a.one2);
   }
 }
 
@@ -352,7 +352,7 @@ int resize_u8_fast(const uint8_t* src, int64_t s_is, int64_t s_rp, int sh, int s
     if (sw % 4 != 0 || sh < 2 || !aligned(src, 16) || !aligned(dst, 8) || (s_is | s_rp) & 15 || (d_is | d_rp) & 7)
       return FV_OK;
   }
-  FastArgs a{src, s_is, s_rp, sh, sw, dst, d_is, d_rp, dh, dw, n, 0, 0, 0, 1.0f, 0};
+  FastArgs a{src, s_is, s_rp, sh, sw, dst, d_is, d_rp, dh, dw, n, 0, 0, 0, kOne2Bits, 0};
   *taken = true;
   switch (c) {
     case 1: return launch_fast_c<1>(a, down, st);

@@ -28,7 +28,7 @@ struct WarpArgs {
   int c;
   float border_f;     // border as a blend operand (u8: RN(b/255))
   float border_raw;   // border as stored for non-finite coordinates
-  float one;          // runtime 1.0f (f32x2 contraction guard)
+  f2_t one2;          // runtime {1.0f, 1.0f} (f32x2 contraction guard)
 };
 
 struct WarpMats {
@@ -213,10 +213,10 @@ __global__ void __launch_bounds__(256) warp_kernel(const __grid_constant__ WarpA
 #pragma unroll
   for (int k = 0; k < 2; ++k) gather_raw<InT, C>(a, n, t[k], bord, v00[k], v01[k], v10[k], v11[k]);
 
-  const float one = a.one;
+  const f2_t one = a.one2;
   const f2_t WX0 = f2(t[0].wx0, t[1].wx0), WX1 = f2(t[0].wx1, t[1].wx1);
   const f2_t WY0 = f2(t[0].wy0, t[1].wy0), WY1 = f2(t[0].wy1, t[1].wy1);
-  const f2_t ONE = f2(one, one);
+  const f2_t ONE = one;
   InT* d = row_ptr_mut<InT>(a.dst, a.d_is, a.d_rp, n, y) + x * C;
 #pragma unroll
   for (int c = 0; c < C; ++c) {
@@ -297,7 +297,7 @@ static int launch_warp(const InT* src, int64_t s_is, int64_t s_rp, int sh, int s
   a.c = c;
   a.border_f = border_f;
   a.border_raw = border_raw;
-  a.one = 1.0f;
+  a.one2 = kOne2Bits;
   WarpMats mats;
   for (int b = 0; b < n; b += MAXW) {
     const int nb = (n - b) < MAXW ? (n - b) : MAXW;
