@@ -17,6 +17,7 @@
 namespace fv {
 
 constexpr int MAXW = 256;  // images per launch (matrices live in the param block)
+constexpr int WARP_ROWS = 4;  // rows per thread in warp_kernel
 
 struct WarpArgs {
   const void* src;
@@ -195,45 +196,49 @@ __global__ void __launch_bounds__(256) warp_kernel(const __grid_constant__ WarpA
                                                    const __grid_constant__ WarpMats mats) {
   const int n = blockIdx.z;
   const int x = blockIdx.x * 64 + threadIdx.x;
-  const int y = blockIdx.y * 8 + threadIdx.y;
-  if (x >= a.dw || y >= a.dh) return;
+  if (x >= a.dw) return;
   const bool two = x + 32 < a.dw;
   double m[9];
 #pragma unroll
   for (int i = 0; i < 9; ++i) m[i] = mats.m[n][i];
-  const double yd = (double)y;
-  const double rx = __dadd_rn(__dmul_rn(m[1], yd), m[2]);
-  const double ry = __dadd_rn(__dmul_rn(m[4], yd), m[5]);
-  const double rw = PERSP ? __dadd_rn(__dmul_rn(m[7], yd), m[8]) : 0.0;
-  WarpTap t[2];
-  t[0] = warp_tap<PERSP>(m, rx, ry, rw, x, a.sw, a.sh);
-  t[1] = warp_tap<PERSP>(m, rx, ry, rw, two ? x + 32 : x, a.sw, a.sh);
   const uint32_t bord = sizeof(InT) == 1 ? (0x4B000000u | (uint32_t)a.border_raw) : __float_as_uint(a.border_f);
-  uint32_t v00[2][C], v01[2][C], v10[2][C], v11[2][C];
+  const f2_t ONE = a.one2;
+  // WARP_ROWS rows per thread (stride 8): the per-warp setup (matrix, params,
+  // indices) is amortised over 64 x WARP_ROWS pixels
+  const int y_end = min(blockIdx.y * 8 * WARP_ROWS + 8 * WARP_ROWS, a.dh);
+#pragma unroll 1
+  for (int y = blockIdx.y * 8 * WARP_ROWS + threadIdx.y; y < y_end; y += 8) {
+    const double yd = (double)y;
+    const double rx = __dadd_rn(__dmul_rn(m[1], yd), m[2]);
+    const double ry = __dadd_rn(__dmul_rn(m[4], yd), m[5]);
+    const double rw = PERSP ? __dadd_rn(__dmul_rn(m[7], yd), m[8]) : 0.0;
+    WarpTap t[2];
+    t[0] = warp_tap<PERSP>(m, rx, ry, rw, x, a.sw, a.sh);
+    t[1] = warp_tap<PERSP>(m, rx, ry, rw, two ? x + 32 : x, a.sw, a.sh);
+    uint32_t v00[2][C], v01[2][C], v10[2][C], v11[2][C];
 #pragma unroll
-  for (int k = 0; k < 2; ++k) gather_raw<InT, C>(a, n, t[k], bord, v00[k], v01[k], v10[k], v11[k]);
+    for (int k = 0; k < 2; ++k) gather_raw<InT, C>(a, n, t[k], bord, v00[k], v01[k], v10[k], v11[k]);
 
-  const f2_t one = a.one2;
-  const f2_t WX0 = f2(t[0].wx0, t[1].wx0), WX1 = f2(t[0].wx1, t[1].wx1);
-  const f2_t WY0 = f2(t[0].wy0, t[1].wy0), WY1 = f2(t[0].wy1, t[1].wy1);
-  const f2_t ONE = one;
-  InT* d = row_ptr_mut<InT>(a.dst, a.d_is, a.d_rp, n, y) + x * C;
+    const f2_t WX0 = f2(t[0].wx0, t[1].wx0), WX1 = f2(t[0].wx1, t[1].wx1);
+    const f2_t WY0 = f2(t[0].wy0, t[1].wy0), WY1 = f2(t[0].wy1, t[1].wy1);
+    InT* d = row_ptr_mut<InT>(a.dst, a.d_is, a.d_rp, n, y) + x * C;
 #pragma unroll
-  for (int c = 0; c < C; ++c) {
-    // imgproc.py:118-123 order, each product and sum rounded (the sum is
-    // fma(q, runtime 1, p): see the f32x2 note in fv_common.cuh)
-    const f2_t top = ffma2(fmul2(tap2<InT>(v01[0][c], v01[1][c]), WX1), ONE, fmul2(tap2<InT>(v00[0][c], v00[1][c]), WX0));
-    const f2_t bot = ffma2(fmul2(tap2<InT>(v11[0][c], v11[1][c]), WX1), ONE, fmul2(tap2<InT>(v10[0][c], v10[1][c]), WX0));
-    const f2_t o = ffma2(fmul2(bot, WY1), ONE, fmul2(top, WY0));
-    uint32_t lo, hi;
-    if constexpr (sizeof(InT) == 1) {
-      f2split(scale_to_u8_bits2(o, 255.0f, one), lo, hi);
-      d[c] = t[0].finite ? (InT)(lo & 0xFF) : (InT)a.border_raw;
-      if (two) d[32 * C + c] = t[1].finite ? (InT)(hi & 0xFF) : (InT)a.border_raw;
-    } else {
-      f2split(o, lo, hi);
-      d[c] = t[0].finite ? __uint_as_float(lo) : a.border_raw;
-      if (two) d[32 * C + c] = t[1].finite ? __uint_as_float(hi) : a.border_raw;
+    for (int c = 0; c < C; ++c) {
+      // imgproc.py:118-123 order, each product and sum rounded (the sum is
+      // fma(q, runtime 1, p): see the f32x2 note in fv_common.cuh)
+      const f2_t top = ffma2(fmul2(tap2<InT>(v01[0][c], v01[1][c]), WX1), ONE, fmul2(tap2<InT>(v00[0][c], v00[1][c]), WX0));
+      const f2_t bot = ffma2(fmul2(tap2<InT>(v11[0][c], v11[1][c]), WX1), ONE, fmul2(tap2<InT>(v10[0][c], v10[1][c]), WX0));
+      const f2_t o = ffma2(fmul2(bot, WY1), ONE, fmul2(top, WY0));
+      uint32_t lo, hi;
+      if constexpr (sizeof(InT) == 1) {
+        f2split(scale_to_u8_bits2(o, 255.0f, ONE), lo, hi);
+        d[c] = t[0].finite ? (InT)(lo & 0xFF) : (InT)a.border_raw;
+        if (two) d[32 * C + c] = t[1].finite ? (InT)(hi & 0xFF) : (InT)a.border_raw;
+      } else {
+        f2split(o, lo, hi);
+        d[c] = t[0].finite ? __uint_as_float(lo) : a.border_raw;
+        if (two) d[32 * C + c] = t[1].finite ? __uint_as_float(hi) : a.border_raw;
+      }
     }
   }
 }
@@ -306,7 +311,7 @@ static int launch_warp(const InT* src, int64_t s_is, int64_t s_rp, int sh, int s
     a.src = reinterpret_cast<const char*>(src) + (int64_t)b * s_is;
     a.dst = reinterpret_cast<char*>(dst) + (int64_t)b * d_is;
     dim3 block(32, 8);
-    dim3 grid2((dw + 63) / 64, (dh + 7) / 8, nb);  // two pixels per thread
+    dim3 grid2((dw + 63) / 64, (dh + 8 * WARP_ROWS - 1) / (8 * WARP_ROWS), nb);  // 2 px x WARP_ROWS rows per thread
     dim3 grid1((dw + 31) / 32, (dh + 7) / 8, nb);
     switch (c) {
       case 1: warp_kernel<InT, PERSP, 1><<<grid2, block, 0, st>>>(a, mats); break;
