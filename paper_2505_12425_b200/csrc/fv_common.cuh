@@ -20,6 +20,23 @@ int set_error(int code, const char* fmt, ...);
 int check_launch(const char* what);
 void count_launch();
 
+// Raise a kernel's dynamic shared-memory limit once per (kernel, device):
+// the attribute is per device, and one process may drive several GPUs.
+// `mask` is a static owned by the (per-kernel) caller: bit d = device d done.
+template <typename K>
+inline int ensure_smem_attr(K kern, int bytes, unsigned long long (&mask)[2]) {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 128) return FV_ECUDA;
+  unsigned long long& word = mask[dev >> 6];
+  const unsigned long long bit = 1ull << (dev & 63);
+  if (!(__atomic_load_n(&word, __ATOMIC_ACQUIRE) & bit)) {
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes) != cudaSuccess)
+      return FV_ECUDA;
+    __atomic_fetch_or(&word, bit, __ATOMIC_RELEASE);
+  }
+  return FV_OK;
+}
+
 // ---------------------------------------------------------------------------
 // u8 <-> unit float
 // ---------------------------------------------------------------------------

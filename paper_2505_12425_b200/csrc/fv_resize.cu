@@ -371,11 +371,8 @@ static int launch_strip(ResizeArgs a, int n, const LutArg& lut, cudaStream_t st,
   a.slot_bytes = (int)slot;
   const int bands = (a.dh + a.band_rows - 1) / a.band_rows;
   auto kern = resize_strip_kernel<InT, C, MODE>;
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxStripSmem);
-    attr_set = true;
-  }
+  static unsigned long long attr_mask[2] = {0, 0};  // per instantiation
+  if (ensure_smem_attr(kern, kMaxStripSmem, attr_mask) != FV_OK) return check_launch("resize_strip_kernel (smem attribute)");
   dim3 grid(a.tiles_x, bands, n);
   kern<<<grid, Cfg::NT, (size_t)smem, st>>>(a, lut);
   *launched = true;

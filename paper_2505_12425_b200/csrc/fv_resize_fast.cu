@@ -325,11 +325,8 @@ static int launch_fast_c(const FastArgs& a0, bool down, cudaStream_t st) {
     a.slot_bytes = ((UP2_GROUPS * 4 + 2) * C + 16 + 15) / 16 * 16 + 32;
     const size_t smem = 16 * UP2_RING + 16 + (size_t)UP2_RING * a.slot_bytes;
     auto kern = resize_up2_kernel<C>;
-    static bool attr = false;
-    if (!attr) {
-      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      attr = true;
-    }
+    static unsigned long long attr_mask[2] = {0, 0};  // per instantiation
+  if (ensure_smem_attr(kern, (int)smem, attr_mask) != FV_OK) return check_launch("resize_up2_kernel (smem attribute)");
     dim3 grid((a.groups + UP2_GROUPS - 1) / UP2_GROUPS, a.bands, a.n);
     kern<<<grid, (UP2_NCW + 1) * 32, smem, st>>>(a);
   }

@@ -326,3 +326,60 @@ def test_native_kernels_launch():
     fv.gray_from_rgb(a, d)
     torch.cuda.synchronize()
     assert _native.launch_count() == before + 1
+
+
+# ---------------------------------------------------------------------------
+# property test: random geometry through every resize path
+# ---------------------------------------------------------------------------
+from hypothesis import given, settings  # noqa: E402
+from hypothesis import strategies as st  # noqa: E402
+
+
+@given(sw=st.integers(1, 70), sh=st.integers(1, 40), dw=st.integers(1, 90), dh=st.integers(1, 50),
+       c=st.sampled_from([1, 2, 3, 4, 5]), n=st.integers(1, 2), path=st.sampled_from([0, 1, 2]),
+       seed=st.integers(0, 2**31 - 1))
+@settings(max_examples=120, deadline=None)
+def test_resize_random_geometry_all_paths(sw, sh, dw, dh, c, n, path, seed):
+    rng = np.random.default_rng(seed)
+    a = rng.integers(0, 256, (n, sh, sw, c), dtype=np.uint8)
+    f = rng.random((n, sh, sw, c), dtype=np.float32)
+    _native.lib().fv_set_resize_path(path)
+    try:
+        du = torch.zeros((n, dh, dw, c), dtype=torch.uint8, device=DEV)
+        df = torch.zeros((n, dh, dw, c), dtype=torch.float32, device=DEV)
+        fv.resize_bilinear_u8(cu(a), du)
+        fv.resize_bilinear(cu(f), df)
+        ou, of = host(du), host(df)
+    finally:
+        _native.lib().fv_set_resize_path(0)
+    for i in range(n):
+        assert np.array_equal(ou[i], O.resize_u8(a[i], dw, dh))
+        assert np.array_equal(of[i], O.resize_bilinear(f[i], dw, dh))
+    if c <= 4:
+        mean, std = [0.3] * c, [0.2] * c
+        dc = torch.zeros((n, c, dh, dw), dtype=torch.float32, device=DEV)
+        fv.resize_normalize_chw(cu(a), dc, mean, std)
+        oc = host(dc)
+        for i in range(n):
+            assert np.array_equal(oc[i], O.resize_normalize_chw(a[i], dw, dh, mean, std))
+
+
+@given(h=st.integers(1, 30), w=st.integers(1, 40), oh=st.integers(1, 30), ow=st.integers(1, 40),
+       c=st.sampled_from([1, 2, 3, 4]), u8=st.booleans(), persp=st.booleans(), border=st.integers(0, 255),
+       seed=st.integers(0, 2**31 - 1))
+@settings(max_examples=80, deadline=None)
+def test_warp_random_geometry(h, w, oh, ow, c, u8, persp, border, seed):
+    rng = np.random.default_rng(seed)
+    a = rng.integers(0, 256, (h, w, c), dtype=np.uint8) if u8 else rng.random((h, w, c), dtype=np.float32)
+    if persp:
+        mat = np.eye(3) + rng.normal(0, 0.05, (3, 3))
+        mat[2, 2] = 1.0
+        inv = O.invert_homography(mat)
+    else:
+        mat = np.hstack([rng.normal(0, 1.0, (2, 2)) + np.eye(2), rng.normal(0, 5.0, (2, 1))])
+        inv = O.invert_affine(mat)
+    b = border if u8 else border / 255.0
+    dst = torch.zeros((oh, ow, c), dtype=torch.from_numpy(a).dtype, device=DEV)
+    (fv.warp_perspective if persp else fv.warp_affine)(cu(a), dst, inv, border=b, inverse=True)
+    ref = (O.warp_perspective if persp else O.warp_affine)(a, inv, oh, ow, border=b)
+    assert_exact(host(dst), ref)
