@@ -30,6 +30,7 @@ struct WarpArgs {
   float border_f;     // border as a blend operand (u8: RN(b/255))
   float border_raw;   // border as stored for non-finite coordinates
   f2_t one2;          // runtime {1.0f, 1.0f} (f32x2 contraction guard)
+  int zero_border;    // border is +0: fully-outside pixels are exactly 0
 };
 
 struct WarpMats {
@@ -87,6 +88,30 @@ __device__ __forceinline__ WarpTap warp_tap(const double (&m)[9], double rx, dou
   t.x0 = min(max(__double2int_rd(sx), -2), sw + 1);
   t.y0 = min(max(__double2int_rd(sy), -2), sh + 1);
   return t;
+}
+
+// Conservative, cheap test (no reciprocal): true only when every tap of the
+// pixel lies outside the source, or W == 0. With a +0 border such a pixel's
+// output is exactly +0 (a blend of four +0 operands, or the raw border), so
+// whole warps of them skip the exact coordinate pipeline and the gathers.
+// Affine: sx = X and sy = Y exactly, so the test is exact. Perspective:
+// sx = RN(X * RN(1/W)) is within a few ulp of X/W; the test compares X with
+// (bound -/+ 1e-6) * W, far outside that error for any |sx| < 1e9 (larger
+// coordinates are outside anyway).
+template <bool PERSP>
+__device__ __forceinline__ bool surely_outside(const double (&m)[9], double rx, double ry, double rw, int x, int sw,
+                                               int sh) {
+  const double xd = (double)x;
+  const double X = __dadd_rn(__dmul_rn(m[0], xd), rx);
+  const double Y = __dadd_rn(__dmul_rn(m[3], xd), ry);
+  if (!PERSP) return !(X >= -1.0 && X < (double)sw && Y >= -1.0 && Y < (double)sh);
+  const double W = __dadd_rn(__dmul_rn(m[6], xd), rw);
+  if (W == 0.0) return true;
+  const double lx = -1.000001 * W, hx = ((double)sw + 1e-6) * W;
+  const double ly = -1.000001 * W, hy = ((double)sh + 1e-6) * W;
+  const bool in_x = W > 0.0 ? (X >= lx && X <= hx) : (X <= lx && X >= hx);
+  const bool in_y = W > 0.0 ? (Y >= ly && Y <= hy) : (Y <= ly && Y >= hy);
+  return !(in_x && in_y);
 }
 
 // Raw taps of the two source pixels (x0, x0+1) of one row, all C channels:
@@ -212,6 +237,19 @@ __global__ void __launch_bounds__(256) warp_kernel(const __grid_constant__ WarpA
     const double rx = __dadd_rn(__dmul_rn(m[1], yd), m[2]);
     const double ry = __dadd_rn(__dmul_rn(m[4], yd), m[5]);
     const double rw = PERSP ? __dadd_rn(__dmul_rn(m[7], yd), m[8]) : 0.0;
+    InT* d = row_ptr_mut<InT>(a.dst, a.d_is, a.d_rp, n, y) + x * C;
+    if (PERSP && a.zero_border) {  // (affine: too few fully-outside warps to pay for the test)
+      const bool so = surely_outside<PERSP>(m, rx, ry, rw, x, a.sw, a.sh) &&
+                      (!two || surely_outside<PERSP>(m, rx, ry, rw, x + 32, a.sw, a.sh));
+      if (__all_sync(__activemask(), so)) {  // rows are warp-uniform, so is the vote
+#pragma unroll
+        for (int c = 0; c < C; ++c) {
+          d[c] = (InT)0;
+          if (two) d[32 * C + c] = (InT)0;
+        }
+        continue;
+      }
+    }
     WarpTap t[2];
     t[0] = warp_tap<PERSP>(m, rx, ry, rw, x, a.sw, a.sh);
     t[1] = warp_tap<PERSP>(m, rx, ry, rw, two ? x + 32 : x, a.sw, a.sh);
@@ -221,7 +259,6 @@ __global__ void __launch_bounds__(256) warp_kernel(const __grid_constant__ WarpA
 
     const f2_t WX0 = f2(t[0].wx0, t[1].wx0), WX1 = f2(t[0].wx1, t[1].wx1);
     const f2_t WY0 = f2(t[0].wy0, t[1].wy0), WY1 = f2(t[0].wy1, t[1].wy1);
-    InT* d = row_ptr_mut<InT>(a.dst, a.d_is, a.d_rp, n, y) + x * C;
 #pragma unroll
     for (int c = 0; c < C; ++c) {
       // imgproc.py:118-123 order, each product and sum rounded (the sum is
@@ -303,6 +340,7 @@ static int launch_warp(const InT* src, int64_t s_is, int64_t s_rp, int sh, int s
   a.border_f = border_f;
   a.border_raw = border_raw;
   a.one2 = kOne2Bits;
+  a.zero_border = (__builtin_bit_cast(uint32_t, border_f) == 0u && __builtin_bit_cast(uint32_t, border_raw) == 0u) ? 1 : 0;
   WarpMats mats;
   for (int b = 0; b < n; b += MAXW) {
     const int nb = (n - b) < MAXW ? (n - b) : MAXW;
