@@ -63,13 +63,6 @@ __device__ __forceinline__ uint32_t unit_to_u8(float v) {
   return __float_as_uint(r) - 0x4B000000u;
 }
 
-// unit_to_u8 without the final subtract: the float bits 0x4B0000qq, whose
-// low byte is the u8 result (for byte packing with __byte_perm).
-__device__ __forceinline__ uint32_t unit_to_u8_bits(float v) {
-  float y = __fmul_rn(v, 255.0f);
-  float t = __fadd_rn(y, 0.5f);
-  return __float_as_uint(__fadd_rd(t, 8388608.0f));
-}
 // y already equal to RN(v * 255)
 __device__ __forceinline__ uint32_t scaled_to_u8_bits(float y) {
   return __float_as_uint(__fadd_rd(__fadd_rn(y, 0.5f), 8388608.0f));
@@ -78,22 +71,6 @@ __device__ __forceinline__ uint32_t scaled_to_u8_bits(float y) {
 __device__ __forceinline__ uint32_t pack4(uint32_t b0, uint32_t b1, uint32_t b2, uint32_t b3) {
   return __byte_perm(__byte_perm(b0, b1, 0x0040), __byte_perm(b2, b3, 0x0040), 0x5410);
 }
-// byte i of a register array of 32-bit words (i compile-time after unrolling)
-template <int N>
-__device__ __forceinline__ uint32_t byte_of(const uint32_t (&w)[N], int i) {
-  return (w[i >> 2] >> ((i & 3) * 8)) & 0xFFu;
-}
-// u8_to_unit of byte i of a word array: the magic-number PRMT picks the byte
-// straight into 0x4B0000uu
-template <int N>
-__device__ __forceinline__ float unit_of(const uint32_t (&w)[N], int i) {
-  const float RHI = __uint_as_float(0x3B808081u);
-  const float RLO = __uint_as_float(0xAF7EFEFFu);
-  const uint32_t m = __byte_perm(w[i >> 2], 0x4B000000u, 0x7440 + (i & 3));
-  const float f = __fsub_rn(__uint_as_float(m), 8388608.0f);
-  return __fmaf_rn(f, RHI, __fmul_rn(f, RLO));
-}
-
 // ---------------------------------------------------------------------------
 // Packed f32x2 arithmetic (sm_100: FADD2 / FMUL2 / FFMA2, two IEEE f32 ops per
 // instruction, each lane rounded separately).
@@ -150,7 +127,8 @@ __device__ __forceinline__ f2_t unit2(uint32_t m_lo, uint32_t m_hi) {
   const f2_t f = fadd2(f2u(m_lo, m_hi), f2(-8388608.0f, -8388608.0f));
   return ffma2(f, f2(RHI, RHI), fmul2(f, f2(RLO, RLO)));
 }
-// magic word 0x4B0000uu of byte i of a word array (see unit_of)
+// magic word 0x4B0000uu of byte i of a word array: PRMT puts the byte under
+// the exponent of 2^23 (i compile-time after unrolling)
 template <int N>
 __device__ __forceinline__ uint32_t magic_of(const uint32_t (&w)[N], int i) {
   return __byte_perm(w[i >> 2], 0x4B000000u, 0x7440 + (i & 3));
@@ -174,27 +152,10 @@ __device__ __forceinline__ uint32_t pack4x2(f2_t a, f2_t b) {
   return pack4(a0, a1, b0, b1);
 }
 
-// Same as unit_to_u8 but with explicit saturation; used where the input is
-// not a convex blend of unit values.
-__device__ __forceinline__ uint32_t unit_to_u8_sat(float v) {
-  float y = __fmul_rn(v, 255.0f);
-  float t = __fadd_rn(y, 0.5f);
-  t = fminf(fmaxf(t, 0.0f), 255.0f);
-  float r = __fadd_rd(t, 8388608.0f);
-  return __float_as_uint(r) - 0x4B000000u;
-}
-
 // imgproc.py:118-123: top = a00*(1-fx) + a01*fx, etc. -- every product and
 // sum separately rounded. w0 = RN(1 - f), w1 = f.
 __device__ __forceinline__ float lerp_ref(float a, float b, float w0, float w1) {
   return __fadd_rn(__fmul_rn(a, w0), __fmul_rn(b, w1));
-}
-
-// The same value in two instructions when b*wb is exact (wb a power of two
-// or 0, b a non-negative blend of u8/255 values -- never subnormal):
-// RN(RN(a*wa) + RN(b*wb)) == RN(b*wb + RN(a*wa)) == fma(b, wb, RN(a*wa)).
-__device__ __forceinline__ float lerp_fma(float a, float b, float wa, float wb) {
-  return __fmaf_rn(b, wb, __fmul_rn(a, wa));
 }
 
 __device__ __forceinline__ bool pow2_or_zero(float w) { return (__float_as_uint(w) & 0x007FFFFFu) == 0; }
@@ -250,9 +211,6 @@ __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
 __device__ __forceinline__ void fence_mbar_init() {
   asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
 }
-__device__ __forceinline__ void fence_proxy_async() {
-  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-}
 __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
                : "memory");
@@ -270,26 +228,6 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       "}\n" ::"r"(smem_u32(bar)),
       "r"(parity)
       : "memory");
-}
-__device__ __forceinline__ bool mbar_try(uint64_t* bar, uint32_t parity) {
-  uint32_t ok;
-  asm volatile(
-      "{\n"
-      ".reg .pred p;\n"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
-      "selp.u32 %0, 1, 0, p;\n"
-      "}\n"
-      : "=r"(ok)
-      : "r"(smem_u32(bar)), "r"(parity)
-      : "memory");
-  return ok != 0;
-}
-// wait with back-off: for a producer that is ahead and must not steal issue
-// slots from the consumer warps while it waits for a free slot
-// (the ring is several rows deep, so a late wake-up costs nothing; polling
-// every ~1 us keeps the producer's issue share negligible)
-__device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity, unsigned ns = 1000) {
-  while (!mbar_try(bar, parity)) __nanosleep(ns);
 }
 // blocking wait: the thread is suspended (NANOSLEEP.SYNCS) until the phase
 // completes or the hint (ns) expires, instead of spinning on try_wait
