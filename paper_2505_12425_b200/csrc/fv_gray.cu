@@ -63,6 +63,49 @@ __global__ void __launch_bounds__(128) gray_u8_vec_kernel(const uint8_t* __restr
   }
 }
 
+// Same work as gray_u8_vec_kernel with a flat (image, row, group) index and
+// 512-thread CTAs: a 1080p frame is ~130K groups, i.e. ~250 CTAs -- one
+// wave, few CTA launches (CTA launch cost dominates such small frames).
+__global__ void __launch_bounds__(512) gray_u8_flat_kernel(const uint8_t* __restrict__ src, int64_t s_is,
+                                                           int64_t s_rp, uint8_t* __restrict__ dst, int64_t d_is,
+                                                           int64_t d_rp, int h, int w, int64_t total) {
+  // Programmatic dependent launch: wait for the previous grid in the stream
+  // (its writes visible) before reading, then let the next grid launch -- its
+  // CTA launch overlaps this grid's run instead of following its completion.
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;");
+  const int groups = (w + 15) >> 4;
+  const int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (gid >= total) return;
+  const int gx = (int)(gid % groups);
+  const int64_t r = gid / groups;
+  const int y = (int)(r % h);
+  const int n = (int)(r / h);
+  const uint8_t* s = row_ptr<uint8_t>(src, s_is, s_rp, n, y) + gx * 48;
+  uint8_t* d = row_ptr_mut<uint8_t>(dst, d_is, d_rp, n, y) + gx * 16;
+  const int x0 = gx * 16;
+  if (x0 + 16 <= w) {
+    uint4 v[3];
+    const uint4* s4 = reinterpret_cast<const uint4*>(s);
+    v[0] = __ldg(s4);
+    v[1] = __ldg(s4 + 1);
+    v[2] = __ldg(s4 + 2);
+    const uint32_t* wd = reinterpret_cast<const uint32_t*>(v);
+    uint32_t out[4] = {0, 0, 0, 0};
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      const int k = 3 * i;
+      uint32_t rr = (wd[k >> 2] >> ((k & 3) * 8)) & 0xFF;
+      uint32_t g = (wd[(k + 1) >> 2] >> (((k + 1) & 3) * 8)) & 0xFF;
+      uint32_t b = (wd[(k + 2) >> 2] >> (((k + 2) & 3) * 8)) & 0xFF;
+      out[i >> 2] |= gray_u8_px(rr, g, b) << ((i & 3) * 8);
+    }
+    __stcs(reinterpret_cast<uint4*>(d), make_uint4(out[0], out[1], out[2], out[3]));
+  } else {
+    for (int i = 0; x0 + i < w; ++i) d[i] = (uint8_t)gray_u8_px(s[3 * i], s[3 * i + 1], s[3 * i + 2]);
+  }
+}
+
 // any alignment / pitch: one pixel per thread
 __global__ void gray_u8_px_kernel(const uint8_t* __restrict__ src, int64_t s_is, int64_t s_rp,
                                   uint8_t* __restrict__ dst, int64_t d_is, int64_t d_rp, int h, int w) {
@@ -139,8 +182,22 @@ int fv_gray_from_rgb_u8(const uint8_t* src, int64_t s_is, int64_t s_rp, uint8_t*
   const int gy = h < 65535 ? h : 65535;
   if (al16(src) && al16(dst) && al16(s_is) && al16(s_rp) && al16(d_is) && al16(d_rp)) {
     const int groups = (w + 15) / 16;
-    dim3 grid((groups + 127) / 128, gy, n);
-    gray_u8_vec_kernel<<<grid, 128, 0, st>>>(src, s_is, s_rp, dst, d_is, d_rp, h, w);
+    const int64_t total = (int64_t)n * h * groups;
+    if (total <= (int64_t)148 * 2048 * 4) {  // small batches: one flat wave of large CTAs
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3((unsigned)((total + 511) / 512));
+      cfg.blockDim = dim3(512);
+      cfg.stream = st;
+      cudaLaunchAttribute attr[1];
+      attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+      attr[0].val.programmaticStreamSerializationAllowed = 1;
+      cfg.attrs = attr;
+      cfg.numAttrs = 1;
+      cudaLaunchKernelEx(&cfg, gray_u8_flat_kernel, src, s_is, s_rp, dst, d_is, d_rp, (int)h, (int)w, total);
+    } else {
+      dim3 grid((groups + 127) / 128, gy, n);
+      gray_u8_vec_kernel<<<grid, 128, 0, st>>>(src, s_is, s_rp, dst, d_is, d_rp, h, w);
+    }
   } else {
     dim3 grid((w + 127) / 128, gy, n);
     gray_u8_px_kernel<<<grid, 128, 0, st>>>(src, s_is, s_rp, dst, d_is, d_rp, h, w);
