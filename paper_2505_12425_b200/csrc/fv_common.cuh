@@ -229,6 +229,17 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       "r"(parity)
       : "memory");
 }
+// Consumer-side release of a TMA ring slot after reading it with ordinary
+// loads. Every lane fences its generic-proxy reads against the async proxy
+// (MEMBAR + FENCE.VIEW.ASYNC: the reads have completed before the slot can be
+// refilled by cp.async.bulk), the warp converges, one lane arrives. Without
+// the fence a refill could overtake a lane's in-flight LDS (observed as a
+// rare wrong row on the first launch in a process).
+__device__ __forceinline__ void slot_release(uint64_t* bar, int lane) {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  __syncwarp();
+  if (lane == 0) mbar_arrive(bar);
+}
 // blocking wait: the thread is suspended (NANOSLEEP.SYNCS) until the phase
 // completes or the hint (ns) expires, instead of spinning on try_wait
 __device__ __forceinline__ void mbar_wait_block(uint64_t* bar, uint32_t parity) {

@@ -255,8 +255,7 @@ __global__ void __launch_bounds__(StripCfg<InT, C, MODE>::NT, 3)
         h[p] = ffma2(fmul2(vb, f2(WB(e), WB(e + 1))), one, fmul2(va, f2(WA(e), WA(e + 1))));
       }
     }
-    __syncwarp();
-    if (lane == 0) mbar_arrive(&empty[slot]);
+    slot_release(&empty[slot], lane);
     ++k;
   };
 

@@ -274,8 +274,7 @@ __global__ void __launch_bounds__((UP2_NCW + 1) * 32, 4) resize_up2_kernel(const
     const int slot = i % UP2_RING;
     mbar_wait(&full[slot], (uint32_t)((i / UP2_RING) & 1));
     up2_lds<C>(slots + slot * a.slot_bytes - gstart, t, w);
-    __syncwarp();
-    if (lane == 0) mbar_arrive(&empty[slot]);
+    slot_release(&empty[slot], lane);
     ++i;
     (void)r;
   };
@@ -367,6 +366,7 @@ __global__ void __launch_bounds__((D2_NCW + 1) * 32) resize_down2_tma_kernel(con
         w1[4 * k] = v.x, w1[4 * k + 1] = v.y, w1[4 * k + 2] = v.z, w1[4 * k + 3] = v.w;
       }
     }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // see slot_release
     __syncwarp();
     if (lane == 0) {
       mbar_arrive(&empty[sa]);

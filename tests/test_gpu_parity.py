@@ -383,3 +383,36 @@ def test_warp_random_geometry(h, w, oh, ow, c, u8, persp, border, seed):
     (fv.warp_perspective if persp else fv.warp_affine)(cu(a), dst, inv, border=b, inverse=True)
     ref = (O.warp_perspective if persp else O.warp_affine)(a, inv, oh, ow, border=b)
     assert_exact(host(dst), ref)
+
+
+def test_cfg1_full_batch_properties():
+    """Size-independent properties at the full BASELINE configs[1] size (64
+    4K images, both kernels): a constant image resizes to the same constant
+    (exact at u8 level), and reruns are bit-identical."""
+    n = 64
+    vals = torch.tensor([(37 * i + 11) % 256 for i in range(n)], dtype=torch.uint8, device=DEV)
+    src = vals.view(n, 1, 1, 1).expand(n, 2160, 3840, 3).contiguous()
+    down = torch.zeros((n, 1080, 1920, 3), dtype=torch.uint8, device=DEV)
+    up = torch.zeros((n, 4320, 7680, 3), dtype=torch.uint8, device=DEV)
+    fv.resize_bilinear_u8(src, down)
+    fv.resize_bilinear_u8(src, up)
+    torch.cuda.synchronize()
+    for out in (down, up):
+        assert torch.equal(out.amin(dim=(1, 2, 3)), vals) and torch.equal(out.amax(dim=(1, 2, 3)), vals)
+    # random content: two runs bit-identical (checksum over the whole batch)
+    g = torch.Generator(device=DEV)
+    g.manual_seed(7)
+    src = torch.randint(0, 256, (n, 2160, 3840, 3), dtype=torch.uint8, device=DEV, generator=g)
+    fv.resize_bilinear_u8(src, up)
+    c1 = up.view(-1).to(torch.int64).sum().item()
+    up2 = torch.empty_like(up)
+    fv.resize_bilinear_u8(src, up2)
+    assert torch.equal(up, up2) and c1 == up2.view(-1).to(torch.int64).sum().item()
+
+
+def test_cfg1_upscale_full_image_exact():
+    """One full 3840x2160 -> 7680x4320 image against the oracle (every row)."""
+    a = synth.seeded_u8_image(3840, 2160, 3, seed=synth.SEED_RESIZE + 5)
+    dst = torch.zeros((4320, 7680, 3), dtype=torch.uint8, device=DEV)
+    fv.resize_bilinear_u8(cu(a), dst)
+    assert_exact(host(dst), O.resize_u8(a, 7680, 4320))
