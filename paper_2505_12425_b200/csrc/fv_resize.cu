@@ -24,6 +24,7 @@
 //  * resize_gather_kernel: any alignment, channel count or scale; one thread
 //    per destination pixel, taps gathered through L1.
 #include <algorithm>
+#include <type_traits>
 
 #include "fv_common.cuh"
 
@@ -229,31 +230,45 @@ __global__ void __launch_bounds__(StripCfg<InT, C, MODE>::NT, 3)
   const f2_t one = a.one2;
 
   constexpr int NP = EPT / 2;  // element pairs (packed f32x2)
+  const bool fast_store = a.vec_store && (p1 - p0) == Cfg::TW_PX;
   f2_t ha[NP], hb[NP];
   int ra = -1, rb = -1, k = 0;
 
-  auto consume = [&](f2_t (&h)[NP]) {
-    const int slot = k % RING;
-    mbar_wait(&full[slot], (uint32_t)((k / RING) & 1));
-    const InT* seg = reinterpret_cast<const InT*>(slots + slot * a.slot_bytes);
+  // horizontal pass of one staged source row into h; the blend form is a
+  // tile-uniform template switch (no per-element branches)
+  const int slot_bytes = a.slot_bytes;
+  auto hpass = [&](auto form, const InT* seg, f2_t (&h)[NP]) {
+    constexpr int HM = decltype(form)::value;
 #pragma unroll
     for (int p = 0; p < NP; ++p) {
       const int e = 2 * p;
       f2_t va, vb;
       if constexpr (sizeof(InT) == 1) {
         va = unit2(0x4B000000u | seg[OA(e)], 0x4B000000u | seg[OA(e + 1)]);
-        if (hmode != 2) vb = unit2(0x4B000000u | seg[OB(e)], 0x4B000000u | seg[OB(e + 1)]);
+        if constexpr (HM != 2) vb = unit2(0x4B000000u | seg[OB(e)], 0x4B000000u | seg[OB(e + 1)]);
       } else {
         va = f2(seg[OA(e)], seg[OA(e + 1)]);
-        if (hmode != 2) vb = f2(seg[OB(e)], seg[OB(e + 1)]);
+        if constexpr (HM != 2) vb = f2(seg[OB(e)], seg[OB(e + 1)]);
       }
-      if (hmode == 2) {
+      if constexpr (HM == 2) {
         h[p] = va;
-      } else if (hmode == 1) {
+      } else if constexpr (HM == 1) {
         h[p] = ffma2(vb, f2(WB(e), WB(e + 1)), fmul2(va, f2(WA(e), WA(e + 1))));
       } else {
         h[p] = ffma2(fmul2(vb, f2(WB(e), WB(e + 1))), one, fmul2(va, f2(WA(e), WA(e + 1))));
       }
+    }
+  };
+  auto consume = [&](f2_t (&h)[NP]) {
+    const int slot = k % RING;
+    mbar_wait(&full[slot], (uint32_t)((k / RING) & 1));
+    const InT* seg = reinterpret_cast<const InT*>(slots + slot * slot_bytes);
+    if (hmode == 2) {
+      hpass(std::integral_constant<int, 2>{}, seg, h);
+    } else if (hmode == 1) {
+      hpass(std::integral_constant<int, 1>{}, seg, h);
+    } else {
+      hpass(std::integral_constant<int, 0>{}, seg, h);
     }
     slot_release(&empty[slot], lane);
     ++k;
@@ -298,20 +313,29 @@ __global__ void __launch_bounds__(StripCfg<InT, C, MODE>::NT, 3)
     if constexpr (MODE == MODE_U8) {
       uint8_t* drow = row_ptr_mut<uint8_t>(a.dst, a.d_is, a.d_rp, n, y) + p0 * C;
       const int row_el = (p1 - p0) * C;
+      if (fast_store) {  // whole tile inside the row and 4-byte aligned: no per-group checks
 #pragma unroll
-      for (int j = 0; j < G; ++j) {
-        const int idx = warp * (32 * G * V) + j * (32 * V) + lane * V;
-        const f2_t r0 = scale_to_u8_bits2(o[2 * j], 255.0f, one);
-        const f2_t r1 = scale_to_u8_bits2(o[2 * j + 1], 255.0f, one);
-        if (a.vec_store && idx + V <= row_el) {
-          __stcs(reinterpret_cast<uint32_t*>(drow + idx), pack4x2(r0, r1));
-        } else {
-          uint32_t q[4];
-          f2split(r0, q[0], q[1]);
-          f2split(r1, q[2], q[3]);
+        for (int j = 0; j < G; ++j) {
+          const int idx = warp * (32 * G * V) + j * (32 * V) + lane * V;
+          __stcs(reinterpret_cast<uint32_t*>(drow + idx),
+                 pack4x2(scale_to_u8_bits2(o[2 * j], 255.0f, one), scale_to_u8_bits2(o[2 * j + 1], 255.0f, one)));
+        }
+      } else {
 #pragma unroll
-          for (int v = 0; v < V; ++v)
-            if (idx + v < row_el) drow[idx + v] = (uint8_t)(q[v] & 0xFF);
+        for (int j = 0; j < G; ++j) {
+          const int idx = warp * (32 * G * V) + j * (32 * V) + lane * V;
+          const f2_t r0 = scale_to_u8_bits2(o[2 * j], 255.0f, one);
+          const f2_t r1 = scale_to_u8_bits2(o[2 * j + 1], 255.0f, one);
+          if (a.vec_store && idx + V <= row_el) {
+            __stcs(reinterpret_cast<uint32_t*>(drow + idx), pack4x2(r0, r1));
+          } else {
+            uint32_t q[4];
+            f2split(r0, q[0], q[1]);
+            f2split(r1, q[2], q[3]);
+#pragma unroll
+            for (int v = 0; v < V; ++v)
+              if (idx + v < row_el) drow[idx + v] = (uint8_t)(q[v] & 0xFF);
+          }
         }
       }
     } else if constexpr (MODE == MODE_F32) {
