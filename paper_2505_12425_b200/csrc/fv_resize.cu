@@ -94,18 +94,17 @@ __global__ void __launch_bounds__(128) resize_gather_kernel(const __grid_constan
 
 template <typename InT, int C, int MODE>
 struct StripCfg {
-  // consumer warps; the tile must hold whole pixels (C = 3 -> multiple of 3)
-  static constexpr int NCW = MODE == MODE_CHW ? 5 : ((C == 3) ? 6 : 4);
-  // lane ownership: groups of V contiguous elements (u8: 4 bytes -> one
-  // 32-bit store) or V = 1 element / pixel, G groups per lane, groups of a
-  // warp interleaved so that a warp's taps and stores are contiguous
-  static constexpr int V = MODE == MODE_U8 ? 4 : 1;
-  static constexpr int G = MODE == MODE_U8 ? 2 : (MODE == MODE_F32 ? 8 : 4);
-  static constexpr int EPT = MODE == MODE_CHW ? G * C : G * V;  // elements per thread
-  static constexpr int TW_PX = MODE == MODE_CHW ? NCW * 32 * G : NCW * 32 * G * V / C;
+  // Lane ownership. MODE_U8: 4 consecutive pixels per lane (all channels:
+  // per-pixel taps, one 4C-byte run per row -> C 32-bit stores). MODE_CHW: 4
+  // pixels per lane at stride 32 (one coalesced 4-byte store per channel
+  // plane). MODE_F32: G single floats per lane, warp-interleaved.
+  static constexpr int NCW = MODE == MODE_CHW ? 5 : (MODE == MODE_U8 ? 4 : ((C == 3) ? 6 : 4));
+  static constexpr int V = 1;
+  static constexpr int G = MODE == MODE_F32 ? 8 : 4;
+  static constexpr int EPT = MODE == MODE_F32 ? G : G * C;  // elements per thread
+  static constexpr int TW_PX = MODE == MODE_F32 ? NCW * 32 * G / C : NCW * 32 * G;
   static constexpr int RING = 8;
   static constexpr int NT = (NCW + 1) * 32;  // + one producer warp
-  static_assert(MODE == MODE_CHW || (NCW * 32 * G * V) % C == 0, "tile must hold whole pixels");
 };
 
 // Weights whose products are exact for every operand of this mode: any
@@ -114,6 +113,40 @@ struct StripCfg {
 template <int MODE>
 __device__ __forceinline__ bool exact_weight(float w) {
   return MODE == MODE_F32 ? (w == 0.0f || w == 1.0f) : pow2_or_zero(w);
+}
+
+// Horizontal pass of one staged source row into the h pairs. HM: 2 = copy
+// (fx == 0), 1 = one exact product (fma form), 0 = the 3-op form -- chosen
+// tile-uniformly, so no per-element branches. Per-pixel taps (u8 / CHW
+// modes): element e reads tap offset o[e / C] + e % C (channel as immediate).
+template <typename InT, int C, int MODE, int HM, int NA, int NP>
+__device__ __forceinline__ void strip_hpass(const InT* seg, const int (&oa)[NA], const int (&ob)[NA],
+                                            const float (&wa)[NA], const float (&wb)[NA], f2_t one,
+                                            f2_t (&h)[NP]) {
+  constexpr bool PX = MODE != MODE_F32;
+#pragma unroll
+  for (int p = 0; p < NP; ++p) {
+    const int e0 = 2 * p, e1 = 2 * p + 1;
+    const int a0 = PX ? oa[e0 / C] + e0 % C : oa[e0], a1 = PX ? oa[e1 / C] + e1 % C : oa[e1];
+    const int b0 = PX ? ob[e0 / C] + e0 % C : ob[e0], b1 = PX ? ob[e1 / C] + e1 % C : ob[e1];
+    const float wa0 = PX ? wa[e0 / C] : wa[e0], wa1 = PX ? wa[e1 / C] : wa[e1];
+    const float wb0 = PX ? wb[e0 / C] : wb[e0], wb1 = PX ? wb[e1 / C] : wb[e1];
+    f2_t va, vb;
+    if constexpr (sizeof(InT) == 1) {
+      va = unit2(0x4B000000u | seg[a0], 0x4B000000u | seg[a1]);
+      if constexpr (HM != 2) vb = unit2(0x4B000000u | seg[b0], 0x4B000000u | seg[b1]);
+    } else {
+      va = f2(seg[a0], seg[a1]);
+      if constexpr (HM != 2) vb = f2(seg[b0], seg[b1]);
+    }
+    if constexpr (HM == 2) {
+      h[p] = va;
+    } else if constexpr (HM == 1) {
+      h[p] = ffma2(vb, f2(wb0, wb1), fmul2(va, f2(wa0, wa1)));
+    } else {
+      h[p] = ffma2(fmul2(vb, f2(wb0, wb1)), one, fmul2(va, f2(wa0, wa1)));
+    }
+  }
 }
 
 template <typename InT, int C, int MODE>
@@ -190,7 +223,7 @@ __global__ void __launch_bounds__(StripCfg<InT, C, MODE>::NT, 3)
   // horizontal taps, loop-invariant over the band: per element (HWC modes)
   // or per pixel (CHW: all channels of a pixel share them; element e of
   // pixel j = e / C reads offset oa[j] + e % C)
-  constexpr int NA = MODE == MODE_CHW ? G : EPT;
+  constexpr int NA = MODE != MODE_F32 ? G : EPT;  // per-pixel taps except f32 HWC
   const int shift_el = shift / (int)sizeof(InT);
   int oa[NA], ob[NA];
   float wa[NA], wb[NA];
@@ -200,6 +233,9 @@ __global__ void __launch_bounds__(StripCfg<InT, C, MODE>::NT, 3)
     int px, ch;
     if (MODE == MODE_CHW) {
       px = p0 + warp * 32 * G + e * 32 + lane;
+      ch = 0;
+    } else if (MODE == MODE_U8) {
+      px = p0 + (warp * 32 + lane) * G + e;
       ch = 0;
     } else {
       const int idx = warp * (32 * G * V) + (e / V) * (32 * V) + lane * V + (e % V);
@@ -218,10 +254,6 @@ __global__ void __launch_bounds__(StripCfg<InT, C, MODE>::NT, 3)
     hfma = hfma && exact_weight<MODE>(wb[e]);
     hcopy = hcopy && wb[e] == 0.0f && wa[e] == 1.0f;  // fx == 0: h is the tap itself
   }
-  auto OA = [&](int e) { return MODE == MODE_CHW ? oa[e / C] + e % C : oa[e]; };
-  auto OB = [&](int e) { return MODE == MODE_CHW ? ob[e / C] + e % C : ob[e]; };
-  auto WA = [&](int e) { return MODE == MODE_CHW ? wa[e / C] : wa[e]; };
-  auto WB = [&](int e) { return MODE == MODE_CHW ? wb[e / C] : wb[e]; };
   __syncthreads();  // row table, LUT and barriers ready
   // tile-uniform choice of the horizontal blend form (producer voted 1 above)
   const int all_copy = __syncthreads_and(hcopy);
@@ -230,45 +262,20 @@ __global__ void __launch_bounds__(StripCfg<InT, C, MODE>::NT, 3)
   const f2_t one = a.one2;
 
   constexpr int NP = EPT / 2;  // element pairs (packed f32x2)
-  const bool fast_store = a.vec_store && (p1 - p0) == Cfg::TW_PX;
   f2_t ha[NP], hb[NP];
   int ra = -1, rb = -1, k = 0;
 
-  // horizontal pass of one staged source row into h; the blend form is a
-  // tile-uniform template switch (no per-element branches)
   const int slot_bytes = a.slot_bytes;
-  auto hpass = [&](auto form, const InT* seg, f2_t (&h)[NP]) {
-    constexpr int HM = decltype(form)::value;
-#pragma unroll
-    for (int p = 0; p < NP; ++p) {
-      const int e = 2 * p;
-      f2_t va, vb;
-      if constexpr (sizeof(InT) == 1) {
-        va = unit2(0x4B000000u | seg[OA(e)], 0x4B000000u | seg[OA(e + 1)]);
-        if constexpr (HM != 2) vb = unit2(0x4B000000u | seg[OB(e)], 0x4B000000u | seg[OB(e + 1)]);
-      } else {
-        va = f2(seg[OA(e)], seg[OA(e + 1)]);
-        if constexpr (HM != 2) vb = f2(seg[OB(e)], seg[OB(e + 1)]);
-      }
-      if constexpr (HM == 2) {
-        h[p] = va;
-      } else if constexpr (HM == 1) {
-        h[p] = ffma2(vb, f2(WB(e), WB(e + 1)), fmul2(va, f2(WA(e), WA(e + 1))));
-      } else {
-        h[p] = ffma2(fmul2(vb, f2(WB(e), WB(e + 1))), one, fmul2(va, f2(WA(e), WA(e + 1))));
-      }
-    }
-  };
   auto consume = [&](f2_t (&h)[NP]) {
     const int slot = k % RING;
     mbar_wait(&full[slot], (uint32_t)((k / RING) & 1));
     const InT* seg = reinterpret_cast<const InT*>(slots + slot * slot_bytes);
     if (hmode == 2) {
-      hpass(std::integral_constant<int, 2>{}, seg, h);
+      strip_hpass<InT, C, MODE, 2, NA, NP>(seg, oa, ob, wa, wb, one, h);
     } else if (hmode == 1) {
-      hpass(std::integral_constant<int, 1>{}, seg, h);
+      strip_hpass<InT, C, MODE, 1, NA, NP>(seg, oa, ob, wa, wb, one, h);
     } else {
-      hpass(std::integral_constant<int, 0>{}, seg, h);
+      strip_hpass<InT, C, MODE, 0, NA, NP>(seg, oa, ob, wa, wb, one, h);
     }
     slot_release(&empty[slot], lane);
     ++k;
@@ -311,32 +318,20 @@ __global__ void __launch_bounds__(StripCfg<InT, C, MODE>::NT, 3)
 
     const int y = yb + i;
     if constexpr (MODE == MODE_U8) {
-      uint8_t* drow = row_ptr_mut<uint8_t>(a.dst, a.d_is, a.d_rp, n, y) + p0 * C;
-      const int row_el = (p1 - p0) * C;
-      if (fast_store) {  // whole tile inside the row and 4-byte aligned: no per-group checks
+      // the lane's 4 pixels = 4C consecutive bytes = C words (elements in order)
+      const int px = p0 + (warp * 32 + lane) * G;
+      uint8_t* dp = row_ptr_mut<uint8_t>(a.dst, a.d_is, a.d_rp, n, y) + (int64_t)px * C;
+      uint32_t wd[C];
 #pragma unroll
-        for (int j = 0; j < G; ++j) {
-          const int idx = warp * (32 * G * V) + j * (32 * V) + lane * V;
-          __stcs(reinterpret_cast<uint32_t*>(drow + idx),
-                 pack4x2(scale_to_u8_bits2(o[2 * j], 255.0f, one), scale_to_u8_bits2(o[2 * j + 1], 255.0f, one)));
-        }
+      for (int q = 0; q < C; ++q)
+        wd[q] = pack4x2(scale_to_u8_bits2(o[2 * q], 255.0f, one), scale_to_u8_bits2(o[2 * q + 1], 255.0f, one));
+      if (a.vec_store && px + G <= p1) {  // 4-byte aligned (px % 4 == 0, row 4-aligned)
+#pragma unroll
+        for (int q = 0; q < C; ++q) __stcs(reinterpret_cast<uint32_t*>(dp) + q, wd[q]);
       } else {
 #pragma unroll
-        for (int j = 0; j < G; ++j) {
-          const int idx = warp * (32 * G * V) + j * (32 * V) + lane * V;
-          const f2_t r0 = scale_to_u8_bits2(o[2 * j], 255.0f, one);
-          const f2_t r1 = scale_to_u8_bits2(o[2 * j + 1], 255.0f, one);
-          if (a.vec_store && idx + V <= row_el) {
-            __stcs(reinterpret_cast<uint32_t*>(drow + idx), pack4x2(r0, r1));
-          } else {
-            uint32_t q[4];
-            f2split(r0, q[0], q[1]);
-            f2split(r1, q[2], q[3]);
-#pragma unroll
-            for (int v = 0; v < V; ++v)
-              if (idx + v < row_el) drow[idx + v] = (uint8_t)(q[v] & 0xFF);
-          }
-        }
+        for (int e = 0; e < EPT; ++e)
+          if (px + e / C < p1) dp[e] = (uint8_t)((wd[e >> 2] >> ((e & 3) * 8)) & 0xFF);
       }
     } else if constexpr (MODE == MODE_F32) {
       float* drow = row_ptr_mut<float>(a.dst, a.d_is, a.d_rp, n, y) + p0 * C;
