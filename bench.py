@@ -451,6 +451,14 @@ def cpu_reference(cores, up_rows=270):
             "wall_s": wall}
 
 
+def headline_config(world):
+    """The `config` object of both arms' JSON line (BASELINE.json configs[1])."""
+    return {"workload": "cfg1: bilinear u8 resize (_resize_u8 semantics, app.py:64-78) of 64x 3840x2160x3 -> "
+                        "1920x1080x3 and -> 7680x4320x3 per step",
+            "global_batch": 64, "parallelism": f"image-sharded x{world}, no collective",
+            "l2": "inputs 1.59 GB >> 126 MB L2 (no flush needed)"}
+
+
 def host_cores():
     try:
         return len(os.sched_getaffinity(0))
@@ -487,11 +495,12 @@ def main():
             if i >= args.warmup:
                 vals.append(r)
         v = statistics.median(x["value"] for x in vals)
+        step_px = 64 * (1920 * 1080 + 7680 * 4320)
         line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
-                "steps": args.steps, "warmup": args.warmup, "higher_is_better": True, "scaling": "strong",
+                "steps": args.steps, "warmup": args.warmup, "ms_per_step": step_px / (v * 1e6) * 1e3,
+                "higher_is_better": True, "scaling": "strong",
                 "vs_baseline": None, "dtype": "u8", "data": "synthetic (seeded uniform u8)",
-                "config": {"workload": "cfg1: bilinear u8 resize 64x 3840x2160x3 -> 1920x1080x3 and -> 7680x4320x3",
-                           "parallelism": f"{cores} host processes"},
+                "config": dict(headline_config(1), parallelism=f"{cores} host processes (reference NumPy path)"),
                 "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "port",
                                  "sample": vals[0]["sample"]},
                 "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
@@ -575,10 +584,7 @@ def main():
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "u8", "data": "synthetic (seeded uniform u8/f32, generated on device)",
-            "config": {"workload": "cfg1: bilinear u8 resize (_resize_u8 semantics) of 64x 3840x2160x3 -> "
-                                   "1920x1080x3 and -> 7680x4320x3 per step",
-                       "global_batch": 64, "parallelism": f"image-sharded x{world}, no collective",
-                       "l2": "inputs 1.59 GB >> 126 MB L2 (no flush needed)"},
+            "config": headline_config(world),
             "roofline": {"bound": "hbm", "kernel": dom["kernel"], "achieved": dom["gbs"], "peak": peak,
                          "peak_source": peak_src, "unit": "GB/s", "frac": dom["gbs"] / peak,
                          "traffic": load_traffic().get(dom["kernel"], {}).get("dram_bytes"),
