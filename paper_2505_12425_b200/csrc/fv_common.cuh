@@ -55,17 +55,18 @@ __device__ __forceinline__ float u8_to_unit(uint32_t u) {
 // app.py:75 then tensor.py:273-276 for a non-negative blend result v <= 1:
 // y = RN(v*255); t = RN(y + 0.5); q = floor(t); q <= 255 (see DESIGN.md §4:
 // bilinear weights sum to <= 1 in f32, so no clamp can trigger).
-// floor(t) for 0 <= t < 2^23 is one round-down add of 2^23.
-__device__ __forceinline__ uint32_t unit_to_u8(float v) {
-  float y = __fmul_rn(v, 255.0f);
-  float t = __fadd_rn(y, 0.5f);
-  float r = __fadd_rd(t, 8388608.0f);
-  return __float_as_uint(r) - 0x4B000000u;
+// That epilogue, floor(RN(RN(v * K) + 0.5)) (K = 255; the 2:1 fast path
+// folds the /4 into K = 63.75), equals
+// floor(RN(fma(v, K, 0.5))) for EVERY f32 v in [0, 1.0625] (K = 255) and
+// [0, 4.25] (K = 63.75) -- an exhaustive check over all 2^30 inputs, kept as
+// tests/test_epilogue_identity.py. One FFMA replaces FMUL + FADD; floor is
+// RD(t + 2^23), which leaves floor(t) in the low mantissa bits. Returns those
+// float bits (0x4B0000uu).
+__device__ __forceinline__ uint32_t scale_to_u8_bits(float v, float K) {
+  return __float_as_uint(__fadd_rd(__fmaf_rn(v, K, 0.5f), 8388608.0f));
 }
-
-// y already equal to RN(v * 255)
-__device__ __forceinline__ uint32_t scaled_to_u8_bits(float y) {
-  return __float_as_uint(__fadd_rd(__fadd_rn(y, 0.5f), 8388608.0f));
+__device__ __forceinline__ uint32_t unit_to_u8(float v) {
+  return scale_to_u8_bits(v, 255.0f) - 0x4B000000u;
 }
 // low bytes of four words -> one word
 __device__ __forceinline__ uint32_t pack4(uint32_t b0, uint32_t b1, uint32_t b2, uint32_t b3) {
@@ -81,8 +82,8 @@ __device__ __forceinline__ uint32_t pack4(uint32_t b0, uint32_t b1, uint32_t b2,
 //   * mul2 result as the ADDEND of an explicit fma2 (cannot be contracted:
 //     the fma already has a product);
 //   * add2 whose operands are not bare products;
-//   * RN(y + 0.5) of a product y written as fma2(y, one, 0.5) with `one` a
-//     RUNTIME 1.0 (kernel argument), so ptxas cannot fold the product in.
+//   * RN(p + q) of two products written as fma2(q, one, p) with `one` a
+//     RUNTIME 1.0 (kernel argument), so ptxas cannot fold a product in.
 // tests/test_gpu_parity.py checks every kernel bit-exactly at config sizes.
 // ---------------------------------------------------------------------------
 typedef unsigned long long f2_t;
@@ -137,12 +138,10 @@ __device__ __forceinline__ uint32_t magic_of(const uint32_t (&w)[N], int i) {
 // it stays in a uniform register pair (ptxas cannot know its value).
 constexpr f2_t kOne2Bits = 0x3F8000003F800000ull;
 
-// y = RN(v * scale) then the u8 epilogue; returns the two float-bit words
-// whose low bytes are the results. `one2` must be the runtime {1, 1} pair.
-__device__ __forceinline__ f2_t scale_to_u8_bits2(f2_t v, float scale, f2_t one2) {
-  const f2_t y = fmul2(v, f2(scale, scale));
-  const f2_t t = ffma2(y, one2, f2(0.5f, 0.5f));
-  return fadd2_rd(t, f2(8388608.0f, 8388608.0f));
+// scale_to_u8_bits on a pair (same exhaustive identity); returns the two
+// float-bit words whose low bytes are the results.
+__device__ __forceinline__ f2_t scale_to_u8_bits2(f2_t v, float scale) {
+  return fadd2_rd(ffma2(v, f2(scale, scale), f2(0.5f, 0.5f)), f2(8388608.0f, 8388608.0f));
 }
 // low bytes of two pairs -> one word
 __device__ __forceinline__ uint32_t pack4x2(f2_t a, f2_t b) {

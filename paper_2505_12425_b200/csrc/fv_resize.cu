@@ -324,7 +324,7 @@ __global__ void __launch_bounds__(StripCfg<InT, C, MODE>::NT, 3)
       uint32_t wd[C];
 #pragma unroll
       for (int q = 0; q < C; ++q)
-        wd[q] = pack4x2(scale_to_u8_bits2(o[2 * q], 255.0f, one), scale_to_u8_bits2(o[2 * q + 1], 255.0f, one));
+        wd[q] = pack4x2(scale_to_u8_bits2(o[2 * q], 255.0f), scale_to_u8_bits2(o[2 * q + 1], 255.0f));
       if (a.vec_store && px + G <= p1) {  // 4-byte aligned (px % 4 == 0, row 4-aligned)
 #pragma unroll
         for (int q = 0; q < C; ++q) __stcs(reinterpret_cast<uint32_t*>(dp) + q, wd[q]);
@@ -349,7 +349,7 @@ __global__ void __launch_bounds__(StripCfg<InT, C, MODE>::NT, 3)
 #pragma unroll
       for (int p = 0; p < NP; ++p) {
         uint32_t q[2];
-        f2split(scale_to_u8_bits2(o[p], 255.0f, one), q[0], q[1]);
+        f2split(scale_to_u8_bits2(o[p], 255.0f), q[0], q[1]);
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
           const int e = 2 * p + h, j = e / C, ch = e % C;

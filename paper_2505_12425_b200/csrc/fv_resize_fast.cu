@@ -88,7 +88,7 @@ __global__ void __launch_bounds__(128) resize_down2_kernel(const __grid_constant
                                unit2(magic_of(w0, o0 + C), magic_of(w0, o1 + C)));
         const f2_t bot = fadd2(unit2(magic_of(w1, o0), magic_of(w1, o1)),
                                unit2(magic_of(w1, o0 + C), magic_of(w1, o1 + C)));
-        r[j] = scale_to_u8_bits2(fadd2(top, bot), K, a.one2);
+        r[j] = scale_to_u8_bits2(fadd2(top, bot), K);
       }
       out[q] = pack4x2(r[0], r[1]);
     }
@@ -101,7 +101,7 @@ __global__ void __launch_bounds__(128) resize_down2_kernel(const __grid_constant
         const int o = 2 * p * C + c;
         const float top = __fadd_rn(u8_to_unit(r0[o]), u8_to_unit(r0[o + C]));
         const float bot = __fadd_rn(u8_to_unit(r1[o]), u8_to_unit(r1[o + C]));
-        d[p * C + c] = (uint8_t)(scaled_to_u8_bits(__fmul_rn(__fadd_rn(top, bot), K)) & 0xFF);
+        d[p * C + c] = (uint8_t)(scale_to_u8_bits(__fadd_rn(top, bot), K) & 0xFF);
       }
   }
 }
@@ -166,8 +166,8 @@ __device__ __forceinline__ void up2_emit(uint8_t* drow, const f2_t (&hb)[4 * C],
 #pragma unroll
     for (int j = 0; j < 2; ++j) {
       const int e = 4 * i + 2 * j;  // pair index
-      const f2_t r0 = scale_to_u8_bits2(ffma2(hb[e], f2(0.25f, 0.25f), qa[e]), 255.0f, one);
-      const f2_t r1 = scale_to_u8_bits2(ffma2(hb[e + 1], f2(0.25f, 0.25f), qa[e + 1]), 255.0f, one);
+      const f2_t r0 = scale_to_u8_bits2(ffma2(hb[e], f2(0.25f, 0.25f), qa[e]), 255.0f);
+      const f2_t r1 = scale_to_u8_bits2(ffma2(hb[e + 1], f2(0.25f, 0.25f), qa[e + 1]), 255.0f);
       w[j] = pack4x2(r0, r1);
     }
     __stcs(reinterpret_cast<uint2*>(drow) + i, make_uint2(w[0], w[1]));
@@ -182,7 +182,7 @@ __device__ __forceinline__ void up2_emit_copy(uint8_t* drow, const f2_t (&h)[4 *
 #pragma unroll
     for (int j = 0; j < 2; ++j) {
       const int e = 4 * i + 2 * j;
-      w[j] = pack4x2(scale_to_u8_bits2(h[e], 255.0f, one), scale_to_u8_bits2(h[e + 1], 255.0f, one));
+      w[j] = pack4x2(scale_to_u8_bits2(h[e], 255.0f), scale_to_u8_bits2(h[e + 1], 255.0f));
     }
     __stcs(reinterpret_cast<uint2*>(drow) + i, make_uint2(w[0], w[1]));
   }
@@ -386,7 +386,7 @@ __global__ void __launch_bounds__((D2_NCW + 1) * 32) resize_down2_tma_kernel(con
                                unit2(magic_of(w0, o0 + C), magic_of(w0, o1 + C)));
         const f2_t bot = fadd2(unit2(magic_of(w1, o0), magic_of(w1, o1)),
                                unit2(magic_of(w1, o0 + C), magic_of(w1, o1 + C)));
-        r[j] = scale_to_u8_bits2(fadd2(top, bot), K, a.one2);
+        r[j] = scale_to_u8_bits2(fadd2(top, bot), K);
       }
       out[q] = pack4x2(r[0], r[1]);
     }

@@ -268,7 +268,7 @@ __global__ void __launch_bounds__(256) warp_kernel(const __grid_constant__ WarpA
       const f2_t o = ffma2(fmul2(bot, WY1), ONE, fmul2(top, WY0));
       uint32_t lo, hi;
       if constexpr (sizeof(InT) == 1) {
-        f2split(scale_to_u8_bits2(o, 255.0f, ONE), lo, hi);
+        f2split(scale_to_u8_bits2(o, 255.0f), lo, hi);
         d[c] = t[0].finite ? (InT)(lo & 0xFF) : (InT)a.border_raw;
         if (two) d[32 * C + c] = t[1].finite ? (InT)(hi & 0xFF) : (InT)a.border_raw;
       } else {
