@@ -12,7 +12,9 @@ import threading
 
 from .errors import NativeError
 
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "lib", "libfovea_b200.so")
+# FOVEA_B200_LIB overrides the in-tree library (A/B builds of the same ABI)
+LIB_PATH = os.environ.get("FOVEA_B200_LIB") or os.path.join(
+    os.path.dirname(os.path.abspath(__file__)), "lib", "libfovea_b200.so")
 
 _c = ctypes
 _I64, _I32, _P, _D = _c.c_int64, _c.c_int32, _c.c_void_p, _c.c_double

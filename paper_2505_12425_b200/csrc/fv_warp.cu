@@ -217,7 +217,7 @@ __device__ __forceinline__ f2_t tap2(uint32_t r0, uint32_t r1) {
 // f32x2 pairs. Interior pixels take unguarded loads, pixels whose four taps
 // are all outside skip the loads.
 template <typename InT, bool PERSP, int C>
-__global__ void __launch_bounds__(256) warp_kernel(const __grid_constant__ WarpArgs a,
+__global__ void __launch_bounds__(256, 4) warp_kernel(const __grid_constant__ WarpArgs a,
                                                    const __grid_constant__ WarpMats mats) {
   const int n = blockIdx.z;
   const int x = blockIdx.x * 64 + threadIdx.x;
