@@ -90,28 +90,10 @@ __device__ __forceinline__ WarpTap warp_tap(const double (&m)[9], double rx, dou
   return t;
 }
 
-// Conservative, cheap test (no reciprocal): true only when every tap of the
-// pixel lies outside the source, or W == 0. With a +0 border such a pixel's
-// output is exactly +0 (a blend of four +0 operands, or the raw border), so
-// whole warps of them skip the exact coordinate pipeline and the gathers.
-// Affine: sx = X and sy = Y exactly, so the test is exact. Perspective:
-// sx = RN(X * RN(1/W)) is within a few ulp of X/W; the test compares X with
-// (bound -/+ 1e-6) * W, far outside that error for any |sx| < 1e9 (larger
-// coordinates are outside anyway).
-template <bool PERSP>
-__device__ __forceinline__ bool surely_outside(const double (&m)[9], double rx, double ry, double rw, int x, int sw,
-                                               int sh) {
-  const double xd = (double)x;
-  const double X = __dadd_rn(__dmul_rn(m[0], xd), rx);
-  const double Y = __dadd_rn(__dmul_rn(m[3], xd), ry);
-  if (!PERSP) return !(X >= -1.0 && X < (double)sw && Y >= -1.0 && Y < (double)sh);
-  const double W = __dadd_rn(__dmul_rn(m[6], xd), rw);
-  if (W == 0.0) return true;
-  const double lx = -1.000001 * W, hx = ((double)sw + 1e-6) * W;
-  const double ly = -1.000001 * W, hy = ((double)sh + 1e-6) * W;
-  const bool in_x = W > 0.0 ? (X >= lx && X <= hx) : (X <= lx && X >= hx);
-  const bool in_y = W > 0.0 ? (Y >= ly && Y <= hy) : (Y <= ly && Y >= hy);
-  return !(in_x && in_y);
+// every tap of the pixel outside the source, or a non-finite map: the
+// gather's all-border case (gather_raw)
+__device__ __forceinline__ bool tap_outside(const WarpTap& t, int sw, int sh) {
+  return !t.finite || t.x0 < -1 || t.x0 >= sw || t.y0 < -1 || t.y0 >= sh;
 }
 
 // Raw taps of the two source pixels (x0, x0+1) of one row, all C channels:
@@ -174,7 +156,7 @@ __device__ __forceinline__ void gather_raw(const WarpArgs& a, int n, const WarpT
                                            uint32_t (&t00)[C], uint32_t (&t01)[C], uint32_t (&t10)[C],
                                            uint32_t (&t11)[C]) {
   const bool inx = t.x0 >= 0 && t.x0 + 1 < a.sw, iny = t.y0 >= 0 && t.y0 + 1 < a.sh;
-  const bool outside = t.x0 < -1 || t.x0 >= a.sw || t.y0 < -1 || t.y0 >= a.sh || !t.finite;
+  const bool outside = tap_outside(t, a.sw, a.sh);
   if (inx && iny) {
     const InT* r0 = row_ptr<InT>(a.src, a.s_is, a.s_rp, n, t.y0);
     const InT* r1 = row_ptr<InT>(a.src, a.s_is, a.s_rp, n, t.y0 + 1);
@@ -238,21 +220,22 @@ __global__ void __launch_bounds__(256, 4) warp_kernel(const __grid_constant__ Wa
     const double ry = __dadd_rn(__dmul_rn(m[4], yd), m[5]);
     const double rw = PERSP ? __dadd_rn(__dmul_rn(m[7], yd), m[8]) : 0.0;
     InT* d = row_ptr_mut<InT>(a.dst, a.d_is, a.d_rp, n, y) + x * C;
-    if (PERSP && a.zero_border) {  // (affine: too few fully-outside warps to pay for the test)
-      const bool so = surely_outside<PERSP>(m, rx, ry, rw, x, a.sw, a.sh) &&
-                      (!two || surely_outside<PERSP>(m, rx, ry, rw, x + 32, a.sw, a.sh));
-      if (__all_sync(__activemask(), so)) {  // rows are warp-uniform, so is the vote
-#pragma unroll
-        for (int c = 0; c < C; ++c) {
-          d[c] = (InT)0;
-          if (two) d[32 * C + c] = (InT)0;
-        }
-        continue;
-      }
-    }
     WarpTap t[2];
     t[0] = warp_tap<PERSP>(m, rx, ry, rw, x, a.sw, a.sh);
     t[1] = warp_tap<PERSP>(m, rx, ry, rw, two ? x + 32 : x, a.sw, a.sh);
+    // With a +0 border, a pixel whose four taps all lie outside the source
+    // (or whose map is non-finite) is exactly +0: a blend of four +0
+    // operands, or the raw border. Warps made only of such pixels skip the
+    // gathers and the blend (the vote is warp-uniform: rows are). Affine
+    // maps have too few such warps to pay for the vote (measured).
+    if (PERSP && a.zero_border && __all_sync(__activemask(), tap_outside(t[0], a.sw, a.sh) && tap_outside(t[1], a.sw, a.sh))) {
+#pragma unroll
+      for (int c = 0; c < C; ++c) {
+        d[c] = (InT)0;
+        if (two) d[32 * C + c] = (InT)0;
+      }
+      continue;
+    }
     uint32_t v00[2][C], v01[2][C], v10[2][C], v11[2][C];
 #pragma unroll
     for (int k = 0; k < 2; ++k) gather_raw<InT, C>(a, n, t[k], bord, v00[k], v01[k], v10[k], v11[k]);
