@@ -158,6 +158,12 @@ int fv_sobel_f32(const float* src, int64_t src_img_stride, int64_t src_row_pitch
  * paths. Exposed so the parity tests cover every GPU path. */
 void fv_set_resize_path(int32_t mode);
 
+/* Affine warp kernel selection: 0 = auto (default: the SMEM-staged tile
+ * kernel when rows are 16-byte aligned, with direct gathers for tiles whose
+ * source box exceeds the staging budget), 1 = always the direct-gather
+ * kernel. Perspective warps always gather directly. */
+void fv_set_warp_path(int32_t mode);
+
 #ifdef __cplusplus
 }
 #endif

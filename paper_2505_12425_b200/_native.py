@@ -26,6 +26,7 @@ SIGNATURES = {
     "fv_last_error": ([], _c.c_char_p),
     "fv_launch_count": ([], _c.c_uint64),
     "fv_set_resize_path": ([_I32], None),
+    "fv_set_warp_path": ([_I32], None),
     "fv_gray_from_rgb_u8": (_IMG2 + [_I32, _I32, _I32, _P], _c.c_int),
     "fv_gray_from_rgb_f32": (_IMG2 + [_I32, _I32, _I32, _P], _c.c_int),
     "fv_to_float_scaled": (_IMG2 + [_I32, _I32, _I32, _I32, _P], _c.c_int),

@@ -66,7 +66,8 @@ __global__ void __launch_bounds__(128) gray_u8_vec_kernel(const uint8_t* __restr
 // Same work as gray_u8_vec_kernel with a flat (image, row, group) index and
 // 512-thread CTAs: a 1080p frame is ~130K groups, i.e. ~250 CTAs -- one
 // wave, few CTA launches (CTA launch cost dominates such small frames).
-__global__ void __launch_bounds__(512) gray_u8_flat_kernel(const uint8_t* __restrict__ src, int64_t s_is,
+constexpr int kFlatThreads = 512;
+__global__ void __launch_bounds__(kFlatThreads) gray_u8_flat_kernel(const uint8_t* __restrict__ src, int64_t s_is,
                                                            int64_t s_rp, uint8_t* __restrict__ dst, int64_t d_is,
                                                            int64_t d_rp, int h, int w, int64_t total) {
   // Programmatic dependent launch: wait for the previous grid in the stream
@@ -195,8 +196,8 @@ int fv_gray_from_rgb_u8(const uint8_t* src, int64_t s_is, int64_t s_rp, uint8_t*
     const int64_t total = (int64_t)n * h * groups;
     if (total <= (int64_t)148 * 2048 * 4) {  // small batches: one flat wave of large CTAs
       cudaLaunchConfig_t cfg = {};
-      cfg.gridDim = dim3((unsigned)((total + 511) / 512));
-      cfg.blockDim = dim3(512);
+      cfg.gridDim = dim3((unsigned)((total + kFlatThreads - 1) / kFlatThreads));
+      cfg.blockDim = dim3(kFlatThreads);
       cfg.stream = st;
       cudaLaunchAttribute attr[1];
       attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;

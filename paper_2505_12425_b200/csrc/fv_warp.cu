@@ -191,6 +191,36 @@ __device__ __forceinline__ f2_t tap2(uint32_t r0, uint32_t r1) {
   else return f2u(r0, r1);
 }
 
+// Bilinear blend of the two pixels of a thread (t[0] -> d0, t[1] -> d1 when
+// ok1) from their raw taps, in imgproc.py:118-123 order with every product
+// and sum rounded (each sum is fma(q, runtime 1, p): see the f32x2 note in
+// fv_common.cuh); u8 results take the app.py:75-77 epilogue. Non-finite maps
+// store the raw border.
+template <typename InT, int C>
+__device__ __forceinline__ void blend_store(const WarpArgs& a, const WarpTap (&t)[2], const uint32_t (&v00)[2][C],
+                                            const uint32_t (&v01)[2][C], const uint32_t (&v10)[2][C],
+                                            const uint32_t (&v11)[2][C], InT* d0, InT* d1, bool ok1) {
+  const f2_t ONE = a.one2;
+  const f2_t WX0 = f2(t[0].wx0, t[1].wx0), WX1 = f2(t[0].wx1, t[1].wx1);
+  const f2_t WY0 = f2(t[0].wy0, t[1].wy0), WY1 = f2(t[0].wy1, t[1].wy1);
+#pragma unroll
+  for (int c = 0; c < C; ++c) {
+    const f2_t top = ffma2(fmul2(tap2<InT>(v01[0][c], v01[1][c]), WX1), ONE, fmul2(tap2<InT>(v00[0][c], v00[1][c]), WX0));
+    const f2_t bot = ffma2(fmul2(tap2<InT>(v11[0][c], v11[1][c]), WX1), ONE, fmul2(tap2<InT>(v10[0][c], v10[1][c]), WX0));
+    const f2_t o = ffma2(fmul2(bot, WY1), ONE, fmul2(top, WY0));
+    uint32_t lo, hi;
+    if constexpr (sizeof(InT) == 1) {
+      f2split(scale_to_u8_bits2(o, 255.0f), lo, hi);
+      d0[c] = t[0].finite ? (InT)(lo & 0xFF) : (InT)a.border_raw;
+      if (ok1) d1[c] = t[1].finite ? (InT)(hi & 0xFF) : (InT)a.border_raw;
+    } else {
+      f2split(o, lo, hi);
+      d0[c] = t[0].finite ? __uint_as_float(lo) : a.border_raw;
+      if (ok1) d1[c] = t[1].finite ? __uint_as_float(hi) : a.border_raw;
+    }
+  }
+}
+
 // Fixed-C kernel (C = 1, 3, 4): a 64 x 8 tile of destination pixels per CTA;
 // each thread samples pixels x and x + 32 (a warp covers 64 consecutive
 // pixels, lanes stay contiguous for the gathers). The matrix and the row
@@ -209,7 +239,6 @@ __global__ void __launch_bounds__(256, 4) warp_kernel(const __grid_constant__ Wa
 #pragma unroll
   for (int i = 0; i < 9; ++i) m[i] = mats.m[n][i];
   const uint32_t bord = sizeof(InT) == 1 ? (0x4B000000u | (uint32_t)a.border_raw) : __float_as_uint(a.border_f);
-  const f2_t ONE = a.one2;
   // WARP_ROWS rows per thread (stride 8): the per-warp setup (matrix, params,
   // indices) is amortised over 64 x WARP_ROWS pixels
   const int y_end = min(blockIdx.y * 8 * WARP_ROWS + 8 * WARP_ROWS, a.dh);
@@ -240,26 +269,181 @@ __global__ void __launch_bounds__(256, 4) warp_kernel(const __grid_constant__ Wa
 #pragma unroll
     for (int k = 0; k < 2; ++k) gather_raw<InT, C>(a, n, t[k], bord, v00[k], v01[k], v10[k], v11[k]);
 
-    const f2_t WX0 = f2(t[0].wx0, t[1].wx0), WX1 = f2(t[0].wx1, t[1].wx1);
-    const f2_t WY0 = f2(t[0].wy0, t[1].wy0), WY1 = f2(t[0].wy1, t[1].wy1);
+    blend_store<InT, C>(a, t, v00, v01, v10, v11, d, d + 32 * C, two);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Affine, staged: a 32 x 32 destination tile per CTA. An affine map sends the
+// tile to a parallelogram, so the source box spanned by the mapped corners
+// (+2 px: per-pixel rounding and the x0+1 / y0+1 taps) holds every in-image
+// tap of the tile. Warp 0 streams the box's row segments into shared memory
+// with 1-D bulk copies (each source sector crosses L2 -> SMEM once per tile);
+// the gathers then read SMEM. The direct kernel's limiter is L1 wavefronts
+// (a warp-wide LDG touches one line per source row its 32 slanted pixels
+// span, ~16 at 30 degrees, and each pixel needs 4 LDG.64 per tap row); an
+// LDS costs only its bank-conflict degree. Tiles whose box exceeds the
+// staging budget (strong zoom-out) take the direct gathers in the same
+// kernel. Same maps, taps and blend as warp_kernel: bit-identical output.
+// ---------------------------------------------------------------------------
+constexpr int AT = 32;  // tile width, destination pixels
+
+template <typename InT, int C>
+__device__ __forceinline__ uint32_t smem_raw(const uint8_t* p) {
+  if constexpr (sizeof(InT) == 1) return 0x4B000000u | *p;
+  else return *reinterpret_cast<const uint32_t*>(p);
+}
+
+// raw tap of channel c of the source pixel at SMEM byte offset o
+template <typename InT>
+__device__ __forceinline__ uint32_t lds_raw(uint32_t addr) {
+  uint32_t v;
+  if constexpr (sizeof(InT) == 1) {
+    asm volatile("ld.shared.u8 %0, [%1];" : "=r"(v) : "r"(addr));
+    return 0x4B000000u | v;
+  } else {
+    asm volatile("ld.shared.b32 %0, [%1];" : "=r"(v) : "r"(addr));
+    return v;
+  }
+}
+
+struct TileBox {
+  int bx0, bx1, by0, by1, off, rowbytes, pitch, staged;
+};
+
+// Plan one tile (thread 0): its source box from the mapped corners (floor
+// -2 / +3), and when the box fits the staging buffer, arm the barrier with
+// the bytes the row copies will deliver.
+template <int PB, int TH>
+__device__ __forceinline__ TileBox plan_tile(const WarpArgs& a, const double* m, int tx0, int ty0, int stage_bytes,
+                                             uint64_t* bar) {
+  double xlo = 0, xhi = 0, ylo = 0, yhi = 0;
+  bool fin = true;
 #pragma unroll
-    for (int c = 0; c < C; ++c) {
-      // imgproc.py:118-123 order, each product and sum rounded (the sum is
-      // fma(q, runtime 1, p): see the f32x2 note in fv_common.cuh)
-      const f2_t top = ffma2(fmul2(tap2<InT>(v01[0][c], v01[1][c]), WX1), ONE, fmul2(tap2<InT>(v00[0][c], v00[1][c]), WX0));
-      const f2_t bot = ffma2(fmul2(tap2<InT>(v11[0][c], v11[1][c]), WX1), ONE, fmul2(tap2<InT>(v10[0][c], v10[1][c]), WX0));
-      const f2_t o = ffma2(fmul2(bot, WY1), ONE, fmul2(top, WY0));
-      uint32_t lo, hi;
-      if constexpr (sizeof(InT) == 1) {
-        f2split(scale_to_u8_bits2(o, 255.0f), lo, hi);
-        d[c] = t[0].finite ? (InT)(lo & 0xFF) : (InT)a.border_raw;
-        if (two) d[32 * C + c] = t[1].finite ? (InT)(hi & 0xFF) : (InT)a.border_raw;
-      } else {
-        f2split(o, lo, hi);
-        d[c] = t[0].finite ? __uint_as_float(lo) : a.border_raw;
-        if (two) d[32 * C + c] = t[1].finite ? __uint_as_float(hi) : a.border_raw;
-      }
+  for (int k = 0; k < 4; ++k) {
+    const double cx = (double)((k & 1) ? min(tx0 + AT, a.dw) - 1 : tx0);
+    const double cy = (double)((k & 2) ? min(ty0 + TH, a.dh) - 1 : ty0);
+    const double sx = __dadd_rn(__dmul_rn(m[0], cx), __dadd_rn(__dmul_rn(m[1], cy), m[2]));
+    const double sy = __dadd_rn(__dmul_rn(m[3], cx), __dadd_rn(__dmul_rn(m[4], cy), m[5]));
+    fin = fin && isfinite(sx) && isfinite(sy);
+    xlo = k ? fmin(xlo, sx) : sx;
+    xhi = k ? fmax(xhi, sx) : sx;
+    ylo = k ? fmin(ylo, sy) : sy;
+    yhi = k ? fmax(yhi, sy) : sy;
+  }
+  TileBox b{0, -1, 0, -1, 0, 0, 0, 0};
+  if (fin) {
+    b.bx0 = (int)fmax(floor(xlo) - 2.0, 0.0);
+    b.bx1 = (int)fmin(floor(xhi) + 3.0, (double)(a.sw - 1));
+    b.by0 = (int)fmax(floor(ylo) - 2.0, 0.0);
+    b.by1 = (int)fmin(floor(yhi) + 3.0, (double)(a.sh - 1));
+  }
+  if (fin && b.bx0 <= b.bx1 && b.by0 <= b.by1) {
+    b.off = (PB * b.bx0) & 15;  // rows are 16-byte aligned (host-checked)
+    b.rowbytes = (b.off + (b.bx1 - b.bx0 + 1) * PB + 15) & ~15;
+    b.pitch = b.rowbytes + (((b.rowbytes >> 4) & 1) ? 0 : 16);  // odd multiple of 16 B: rows rotate banks
+    const int rows = b.by1 - b.by0 + 1;
+    b.staged = (int64_t)rows * b.pitch <= stage_bytes;
+    if (b.staged) {
+      mbar_init(bar, 1);
+      fence_mbar_init();
+      mbar_expect_tx(bar, (uint32_t)(rows * b.rowbytes));
     }
+  }
+  return b;
+}
+
+// One AT x TH destination tile per CTA (32 x TH/4 threads, 4 pixels each:
+// rows ly + {0, TH/4} and ly + {TH/2, 3TH/4} as two f32x2 pairs). Thread 0
+// plans the box, warp 0 issues the row copies, all wait on the barrier; the
+// other CTAs resident on the SM (8 for TH = 16) overlap the fill.
+template <typename InT, int C, int TH>
+__global__ void __launch_bounds__(8 * TH, 128 / TH) warp_affine_tile_kernel(const __grid_constant__ WarpArgs a,
+                                                                             const __grid_constant__ WarpMats mats) {
+  constexpr int PB = C * (int)sizeof(InT);  // bytes per pixel
+  constexpr int ES = (int)sizeof(InT);
+  constexpr int RS = TH / 4;                // row step between a thread's pixels
+  constexpr int STAGE = TH == 32 ? 48 * 1024 : 24 * 1024;
+  extern __shared__ __align__(128) uint8_t smem[];
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem);
+  TileBox* box = reinterpret_cast<TileBox*>(smem + 16);
+  uint8_t* stage = smem + 64;
+  const int n = blockIdx.z;
+  const int lx = threadIdx.x, ly = threadIdx.y;
+  const int tx0 = blockIdx.x * AT, ty0 = blockIdx.y * TH;
+  double m[9];
+#pragma unroll
+  for (int i = 0; i < 6; ++i) m[i] = mats.m[n][i];
+  m[6] = m[7] = m[8] = 0.0;
+
+  if (lx == 0 && ly == 0) *box = plan_tile<PB, TH>(a, m, tx0, ty0, STAGE, bar);
+  __syncthreads();
+  const TileBox b = *box;
+  if (b.staged && ly == 0) {  // warp 0 streams the box's row segments
+    const uint8_t* base = reinterpret_cast<const uint8_t*>(a.src) + n * a.s_is + (int64_t)b.by0 * a.s_rp +
+                          (int64_t)PB * b.bx0 - b.off;
+    for (int r = lx; r <= b.by1 - b.by0; r += 32)
+      tma_bulk_g2s(stage + r * b.pitch, base + (int64_t)r * a.s_rp, (uint32_t)b.rowbytes, bar);
+  }
+  const int x = tx0 + lx;
+  const uint32_t bord = sizeof(InT) == 1 ? (0x4B000000u | (uint32_t)a.border_raw) : __float_as_uint(a.border_f);
+  // SMEM address of source pixel (0, by0): (x, y) at sb + (y - by0) * pitch + x * PB
+  const uint32_t sb = smem_u32(stage) + (uint32_t)(b.off - b.bx0 * PB);
+  if (b.staged) mbar_wait_block(bar, 0);
+  if (x >= a.dw) return;  // (no CTA-wide barrier follows)
+#pragma unroll 1
+  for (int half = 0; half < 2; ++half) {
+    const int ya = ty0 + ly + 2 * RS * half, yb = ya + RS;
+    if (ya >= a.dh) break;
+    const bool okb = yb < a.dh;
+    WarpTap t[2];
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+      const double yd = (double)((k && okb) ? yb : ya);
+      const double rx = __dadd_rn(__dmul_rn(m[1], yd), m[2]);
+      const double ry = __dadd_rn(__dmul_rn(m[4], yd), m[5]);
+      t[k] = warp_tap<false>(m, rx, ry, 0.0, x, a.sw, a.sh);
+    }
+    uint32_t v00[2][C], v01[2][C], v10[2][C], v11[2][C];
+    if (b.staged) {
+#pragma unroll
+      for (int k = 0; k < 2; ++k) {
+        const WarpTap& q = t[k];
+        const bool inx = q.x0 >= 0 && q.x0 + 1 < a.sw, iny = q.y0 >= 0 && q.y0 + 1 < a.sh;
+        if (inx && iny) {  // interior: in-image taps lie inside the box
+          const uint32_t o = sb + (uint32_t)((q.y0 - b.by0) * b.pitch + q.x0 * PB);
+#pragma unroll
+          for (int c = 0; c < C; ++c) {
+            v00[k][c] = lds_raw<InT>(o + c * ES);
+            v01[k][c] = lds_raw<InT>(o + PB + c * ES);
+            v10[k][c] = lds_raw<InT>(o + b.pitch + c * ES);
+            v11[k][c] = lds_raw<InT>(o + b.pitch + PB + c * ES);
+          }
+        } else if (tap_outside(q, a.sw, a.sh)) {
+#pragma unroll
+          for (int c = 0; c < C; ++c) v00[k][c] = v01[k][c] = v10[k][c] = v11[k][c] = bord;
+        } else {  // straddles the image edge: per-tap test (clamps keep reads in the box)
+          const bool ix0 = q.x0 >= 0 && q.x0 < a.sw, ix1 = q.x0 + 1 >= 0 && q.x0 + 1 < a.sw;
+          const bool iy0 = q.y0 >= 0 && q.y0 < a.sh, iy1 = q.y0 + 1 >= 0 && q.y0 + 1 < a.sh;
+          const int cx0 = min(max(q.x0, b.bx0), b.bx1), cx1 = min(max(q.x0 + 1, b.bx0), b.bx1);
+          const int cy0 = min(max(q.y0, b.by0), b.by1) - b.by0, cy1 = min(max(q.y0 + 1, b.by0), b.by1) - b.by0;
+          const uint32_t r0 = sb + (uint32_t)(cy0 * b.pitch), r1 = sb + (uint32_t)(cy1 * b.pitch);
+#pragma unroll
+          for (int c = 0; c < C; ++c) {
+            v00[k][c] = (iy0 && ix0) ? lds_raw<InT>(r0 + cx0 * PB + c * ES) : bord;
+            v01[k][c] = (iy0 && ix1) ? lds_raw<InT>(r0 + cx1 * PB + c * ES) : bord;
+            v10[k][c] = (iy1 && ix0) ? lds_raw<InT>(r1 + cx0 * PB + c * ES) : bord;
+            v11[k][c] = (iy1 && ix1) ? lds_raw<InT>(r1 + cx1 * PB + c * ES) : bord;
+          }
+        }
+      }
+    } else {
+#pragma unroll
+      for (int k = 0; k < 2; ++k) gather_raw<InT, C>(a, n, t[k], bord, v00[k], v01[k], v10[k], v11[k]);
+    }
+    InT* da = row_ptr_mut<InT>(a.dst, a.d_is, a.d_rp, n, ya) + x * C;
+    InT* db = row_ptr_mut<InT>(a.dst, a.d_is, a.d_rp, n, okb ? yb : ya) + x * C;
+    blend_store<InT, C>(a, t, v00, v01, v10, v11, da, db, okb);
   }
 }
 
@@ -299,6 +483,21 @@ __global__ void __launch_bounds__(256) warp_kernel_any(const __grid_constant__ W
   }
 }
 
+static int g_warp_path = 0;  // 0 auto, 1 direct gathers only (fv_set_warp_path)
+
+constexpr int AT_H = 16;  // tile height of the staged affine kernel (16: 24 KB stage, 8 CTAs / SM)
+
+template <typename InT, int C>
+static int launch_tile(int dw, int dh, int nb, cudaStream_t st, const WarpArgs& a, const WarpMats& mats) {
+  auto kern = warp_affine_tile_kernel<InT, C, AT_H>;
+  const int smem = 64 + (AT_H == 32 ? 48 * 1024 : 24 * 1024);
+  static unsigned long long attr_mask[2] = {0, 0};  // per instantiation
+  if (ensure_smem_attr(kern, smem, attr_mask) != FV_OK) return check_launch("warp_affine_tile_kernel (smem attribute)");
+  dim3 grid((dw + AT - 1) / AT, (dh + AT_H - 1) / AT_H, nb);
+  kern<<<grid, dim3(32, AT_H / 4), smem, st>>>(a, mats);
+  return FV_OK;
+}
+
 template <typename InT, bool PERSP>
 static int launch_warp(const InT* src, int64_t s_is, int64_t s_rp, int sh, int sw, InT* dst, int64_t d_is,
                        int64_t d_rp, int dh, int dw, int c, int n, const double* mats_host, int mat_len,
@@ -334,6 +533,22 @@ static int launch_warp(const InT* src, int64_t s_is, int64_t s_rp, int sh, int s
     dim3 block(32, 8);
     dim3 grid2((dw + 63) / 64, (dh + 8 * WARP_ROWS - 1) / (8 * WARP_ROWS), nb);  // 2 px x WARP_ROWS rows per thread
     dim3 grid1((dw + 31) / 32, (dh + 7) / 8, nb);
+    // affine, 16-byte aligned rows: the SMEM-staged tile kernel
+    const int64_t pb = (int64_t)c * (int64_t)sizeof(InT);
+    const bool rows16 = (reinterpret_cast<uintptr_t>(a.src) & 15) == 0 && (s_rp & 15) == 0 &&
+                        (nb == 1 || (s_is & 15) == 0) && ((pb * sw) & 15) == 0;
+    if (!PERSP && g_warp_path == 0 && rows16 && (c == 1 || c == 3 || c == 4)) {
+      int rc = FV_OK;
+      switch (c) {
+        case 1: rc = launch_tile<InT, 1>(dw, dh, nb, st, a, mats); break;
+        case 3: rc = launch_tile<InT, 3>(dw, dh, nb, st, a, mats); break;
+        default: rc = launch_tile<InT, 4>(dw, dh, nb, st, a, mats); break;
+      }
+      if (rc) return rc;
+      rc = check_launch(fn);
+      if (rc) return rc;
+      continue;
+    }
     switch (c) {
       case 1: warp_kernel<InT, PERSP, 1><<<grid2, block, 0, st>>>(a, mats); break;
       case 3: warp_kernel<InT, PERSP, 3><<<grid2, block, 0, st>>>(a, mats); break;
@@ -351,6 +566,8 @@ static int launch_warp(const InT* src, int64_t s_is, int64_t s_rp, int sh, int s
 using namespace fv;
 
 extern "C" {
+
+void fv_set_warp_path(int32_t mode) { g_warp_path = mode; }
 
 int fv_warp_affine_f32(const float* src, int64_t s_is, int64_t s_rp, int32_t sh, int32_t sw, float* dst,
                        int64_t d_is, int64_t d_rp, int32_t dh, int32_t dw, int32_t c, int32_t n,

@@ -235,8 +235,15 @@ class TestFused:
 # a8 / a9 warps
 # ---------------------------------------------------------------------------
 
+@pytest.fixture(params=[0, 1], ids=["tile", "direct"])
+def warp_path(request):
+    _native.lib().fv_set_warp_path(request.param)
+    yield request.param
+    _native.lib().fv_set_warp_path(0)
+
+
 class TestWarp:
-    def test_cfg2_affine_full_images(self):
+    def test_cfg2_affine_full_images(self, warp_path):
         n = 2
         imgs = np.stack([synth.seeded_f32_image(1920, 1080, 3, seed=synth.SEED_AFFINE + i) for i in range(n)])
         ms = np.stack([synth.affine_forward(synth.SEED_AFFINE_PARAMS + i, 1920, 1080) for i in range(n)])
@@ -259,7 +266,7 @@ class TestWarp:
                 assert_exact(out[i, lo:hi], O.warp_perspective(imgs[i], hinv, 2160, 3840, border=0, rows=(lo, hi)))
 
     @pytest.mark.parametrize("dtype", [np.uint8, np.float32])
-    def test_small_shapes_with_border(self, rng, dtype):
+    def test_small_shapes_with_border(self, rng, dtype, warp_path):
         for (h, w, oh, ow, c) in [(14, 17, 12, 19, 3), (5, 5, 9, 9, 1), (33, 20, 20, 33, 4)]:
             a = rng.integers(0, 256, (h, w, c), dtype=np.uint8) if dtype == np.uint8 else rng.random((h, w, c), dtype=np.float32)
             m = O.affine_forward(7 + h, w, h)
@@ -271,6 +278,37 @@ class TestWarp:
                 inv = O.invert_homography(mat) if persp else O.invert_affine(mat)
                 ref = (O.warp_perspective if persp else O.warp_affine)(a, inv, oh, ow, border=7)
                 assert_exact(host(dst), ref)
+
+    @pytest.mark.parametrize("dtype", [np.uint8, np.float32])
+    @pytest.mark.parametrize("c", [1, 3, 4])
+    def test_affine_tile_kernel_cases(self, rng, dtype, c, warp_path):
+        """The SMEM-staged affine kernel against the oracle: 16-byte aligned
+        rows (staged), a zoom-out whose tile boxes exceed the staging budget
+        (direct gathers inside the same kernel), a map that sends whole tiles
+        outside the source (empty boxes), ragged tile edges, a batch, and a
+        crop view whose rows are not 16-byte aligned (direct kernel)."""
+        h, w = 70, 160  # 160 px: rows 16-byte aligned for every dtype / c
+        a = rng.integers(0, 256, (3, h, w + 16, c), dtype=np.uint8)
+        if dtype == np.float32:
+            a = (a / np.float32(255)).astype(np.float32)
+        base = [
+            O.affine_forward(5, w, h),                                   # rotation / scale / shift
+            np.array([[0.3, 0.05, 2.0], [-0.04, 0.35, 1.0]]),            # 3x zoom-out: boxes too big
+            np.array([[1.0, 0.0, 500.0], [0.0, 1.0, -300.0]]),           # everything outside
+            np.array([[0.9, 0.45, -20.0], [-0.45, 0.9, 30.0]]),          # 27 deg rotation
+        ]
+        for m in base:
+            for oh, ow in [(h, w), (45, 77)]:
+                for crop, border in [(False, 0), (True, 9)]:
+                    b = border if dtype == np.uint8 else border / 255.0
+                    view = a[:, :, 3:w + 3] if crop else np.ascontiguousarray(a[:, :, :w])
+                    src = cu(a)[:, :, 3:w + 3] if crop else cu(view)
+                    dst = torch.zeros((3, oh, ow, c), dtype=src.dtype, device=DEV)
+                    fv.warp_affine(src, dst, np.stack([m] * 3), border=b)
+                    got = host(dst)
+                    inv = O.invert_affine(m)
+                    for i in range(3):
+                        assert_exact(got[i], O.warp_affine(np.ascontiguousarray(view[i]), inv, oh, ow, border=b))
 
     def test_identity_and_zero_w(self, rng):
         a = rng.integers(0, 256, (10, 12, 3), dtype=np.uint8)
@@ -383,6 +421,24 @@ def test_warp_random_geometry(h, w, oh, ow, c, u8, persp, border, seed):
     (fv.warp_perspective if persp else fv.warp_affine)(cu(a), dst, inv, border=b, inverse=True)
     ref = (O.warp_perspective if persp else O.warp_affine)(a, inv, oh, ow, border=b)
     assert_exact(host(dst), ref)
+
+
+@given(h=st.integers(1, 80), w16=st.integers(1, 6), oh=st.integers(1, 80), ow=st.integers(1, 100),
+       c=st.sampled_from([1, 3, 4]), u8=st.booleans(), scale=st.floats(0.2, 3.0), angle=st.floats(-3.2, 3.2),
+       border=st.integers(0, 255), seed=st.integers(0, 2**31 - 1))
+@settings(max_examples=60, deadline=None)
+def test_affine_tile_random_geometry(h, w16, oh, ow, c, u8, scale, angle, border, seed):
+    """Random affine maps on 16-byte aligned rows (the staged tile kernel),
+    any rotation, zoom in and out, bit-exact against the oracle."""
+    rng = np.random.default_rng(seed)
+    w = 16 * w16
+    a = rng.integers(0, 256, (h, w, c), dtype=np.uint8) if u8 else rng.random((h, w, c), dtype=np.float32)
+    ca, sa = np.cos(angle) * scale, np.sin(angle) * scale
+    inv = np.array([[ca, -sa, rng.normal(0, 20)], [sa, ca, rng.normal(0, 20)]])
+    b = border if u8 else border / 255.0
+    dst = torch.zeros((oh, ow, c), dtype=torch.from_numpy(a).dtype, device=DEV)
+    fv.warp_affine(cu(a), dst, inv, border=b, inverse=True)
+    assert_exact(host(dst), O.warp_affine(a, inv, oh, ow, border=b))
 
 
 def test_cfg1_full_batch_properties():
