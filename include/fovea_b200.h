@@ -42,6 +42,9 @@ extern "C" {
 #define FV_OK 0
 #define FV_EINVAL (-1)
 #define FV_ECUDA (-2)
+#define FV_ECORRUPT (-3)     /* JPEG: malformed stream (errors.py CorruptStream) */
+#define FV_EUNSUPPORTED (-4) /* JPEG: valid but outside the subset (UnsupportedJpegFeature) */
+#define FV_ERANGE (-5)       /* JPEG: a coefficient does not fit the chosen width; retry wider */
 
 /* ABI version (major*100 + minor). */
 int fv_version(void);
@@ -150,6 +153,42 @@ int fv_flip_horizontal(const void* src, int64_t src_img_stride, int64_t src_row_
 int fv_sobel_f32(const float* src, int64_t src_img_stride, int64_t src_row_pitch,
                  float* dst, int64_t dst_img_stride, int64_t dst_row_pitch,
                  int32_t height, int32_t width, int32_t channels, int32_t n, void* stream);
+
+/* ---- decode -> preprocess: io.jpeg.decode_jpeg (io/jpeg.py:605-806) -----
+ * Baseline / extended-sequential Huffman JPEG, 1 or 3 components, sampling
+ * factors up to 2x2, restart markers, 8/16-bit quantisation tables --
+ * bit-identical to the reference decoder (integer "islow" IDCT, integer
+ * triangle chroma upsampling, 16-bit fixed-point YCbCr -> RGB).
+ * Three steps (the output size is only known after the header):
+ *   1. fv_jpeg_info       host: parse the headers and split the scan; sizes of
+ *                         the coefficient buffer and the plane scratch.
+ *   2. fv_jpeg_decode_coeffs  host, pure CPU, thread-safe: entropy-decode the
+ *                         scan into quantised coefficients (natural order,
+ *                         int16 or int64; FV_ERANGE asks for int64).
+ *   3. fv_jpeg_reconstruct    device, async on `stream`: dequantise + IDCT into
+ *                         the u8 component planes, then upsample + colour
+ *                         convert into dst (H x W x ncomp u8, row pitch in
+ *                         bytes).
+ * Errors carry the reference's classes: FV_ECORRUPT / FV_EUNSUPPORTED, with
+ * the message in fv_last_error(). Stream data is a HOST pointer. */
+typedef struct FvJpegInfo {
+  int32_t width, height, ncomp;        /* image size; 1 (gray) or 3 components */
+  int32_t hmax, vmax, mcus_x, mcus_y;  /* MCU grid */
+  int32_t restart_interval;            /* MCUs per restart segment, 0 = none */
+  int32_t h[3], v[3];                  /* sampling factors, scan order */
+  int32_t bw[3], bh[3];                /* blocks per component row / column */
+  int32_t cw[3], ch[3];                /* component plane size before upsampling */
+  int64_t coef_offset[3];              /* first coefficient of each component */
+  int64_t coef_count;                  /* coefficients in the buffer (64 per block) */
+  int64_t plane_offset[3];             /* byte offset of each u8 plane (pitch bw*8) */
+  int64_t plane_bytes;                 /* plane scratch bytes */
+  uint16_t qt[3][64];                  /* quantisation table per component, natural order */
+} FvJpegInfo;
+
+int fv_jpeg_info(const uint8_t* data, int64_t len, FvJpegInfo* info);
+int fv_jpeg_decode_coeffs(const uint8_t* data, int64_t len, void* coeffs, int64_t coef_count, int32_t coef_bytes);
+int fv_jpeg_reconstruct(const FvJpegInfo* info, const void* coeffs, int32_t coef_bytes, uint8_t* planes,
+                        uint8_t* dst, int64_t dst_row_pitch, void* stream);
 
 /* ---- tuning / introspection ---------------------------------------------
  * Resize kernel selection: 0 = auto (default: exact 2:1 / 1:2 fast paths,

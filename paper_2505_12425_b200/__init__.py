@@ -13,12 +13,14 @@ functions on torch CUDA tensors):
     resize_nearest(src, dst)                   imgproc.py:89-97
     flip_horizontal(src, dst)                  imgproc.py:67-73
     sobel(src, dst, 3)                         imgproc.py:126-155
+    io.decode_jpeg(data) -> tensor             io/jpeg.py:605-806 (decode -> preprocess)
 
 Every call is one sm_100a kernel launch through the C ABI in
 include/fovea_b200.h; there is no CPU fallback.
 """
 from .errors import (  # noqa: F401
     AliasedBuffers,
+    CorruptStream,
     FoveaError,
     NativeError,
     NonContiguous,
@@ -27,8 +29,10 @@ from .errors import (  # noqa: F401
     SizeMismatch,
     UnsupportedDevice,
     UnsupportedDtype,
+    UnsupportedJpegFeature,
     UnsupportedKernelSize,
 )
+from . import io  # noqa: F401,E402
 from .image import to_float_scaled  # noqa: F401
 from .imgproc import (  # noqa: F401
     flip_horizontal,

@@ -47,6 +47,30 @@ SIGNATURES = {
     "fv_sobel_f32": (_IMG2 + [_I32, _I32, _I32, _I32, _P], _c.c_int),
 }
 
+
+
+class FvJpegInfo(_c.Structure):
+    """Mirror of `FvJpegInfo` (include/fovea_b200.h)."""
+
+    _fields_ = [
+        ("width", _I32), ("height", _I32), ("ncomp", _I32),
+        ("hmax", _I32), ("vmax", _I32), ("mcus_x", _I32), ("mcus_y", _I32),
+        ("restart_interval", _I32),
+        ("h", _I32 * 3), ("v", _I32 * 3), ("bw", _I32 * 3), ("bh", _I32 * 3), ("cw", _I32 * 3), ("ch", _I32 * 3),
+        ("coef_offset", _I64 * 3), ("coef_count", _I64),
+        ("plane_offset", _I64 * 3), ("plane_bytes", _I64),
+        ("qt", (_c.c_uint16 * 64) * 3),
+    ]
+
+
+SIGNATURES.update({
+    "fv_jpeg_info": ([_P, _I64, _c.POINTER(FvJpegInfo)], _c.c_int),
+    "fv_jpeg_decode_coeffs": ([_P, _I64, _P, _I64, _I32], _c.c_int),
+    "fv_jpeg_reconstruct": ([_c.POINTER(FvJpegInfo), _P, _I32, _P, _P, _I64, _P], _c.c_int),
+})
+
+FV_ECORRUPT, FV_EUNSUPPORTED, FV_ERANGE = -3, -4, -5
+
 _lib = None
 _lock = threading.Lock()
 

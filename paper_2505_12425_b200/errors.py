@@ -36,6 +36,14 @@ class UnsupportedKernelSize(FoveaError):
     """Filter kernel size outside the supported set (errors.py:62-63)."""
 
 
+class CorruptStream(FoveaError):
+    """Byte stream is not a well-formed instance of the expected format (errors.py:68-69)."""
+
+
+class UnsupportedJpegFeature(FoveaError):
+    """Valid JPEG using a feature outside the supported subset, e.g. progressive (errors.py:76-77)."""
+
+
 class UnsupportedDevice(FoveaError):
     """Tensor is not resident on a CUDA device (there is no CPU path)."""
 

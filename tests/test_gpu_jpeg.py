@@ -1,0 +1,123 @@
+"""decode -> preprocess on the GPU: `io.decode_jpeg` (host entropy decoding
++ sm_100a IDCT / upsampling / colour kernels) against the reference
+decoder's own outputs (tests/golden/jpeg.npz, bit-exact), the reference's
+error classes, the batched path, and full-size frames against the oracle's
+reconstruction (numpy, vectorised) of the same coefficients."""
+import io as pyio
+import os
+import sys
+
+import numpy as np
+import pytest
+import torch
+
+sys.path.insert(0, os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "oracle"))
+import jpeg_oracle as O  # noqa: E402
+
+import paper_2505_12425_b200 as fv  # noqa: E402
+from paper_2505_12425_b200 import _native, synth  # noqa: E402
+from paper_2505_12425_b200 import io as fio  # noqa: E402
+
+pytestmark = pytest.mark.gpu
+
+_Z = np.load(os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "jpeg.npz"))
+NAMES = sorted({k.split("__")[0] for k in _Z.files})
+DECODED = [n for n in NAMES if n + "__out" in _Z.files]
+REJECTED = [n for n in NAMES if n + "__err" in _Z.files]
+
+
+def stream(name):
+    return _Z[name + "__jpg"].tobytes()
+
+
+@pytest.mark.parametrize("name", DECODED)
+def test_matches_reference_decoder_exactly(name):
+    out = fio.decode_jpeg(stream(name))
+    assert out.is_cuda and out.dtype == torch.uint8
+    assert np.array_equal(out.cpu().numpy(), _Z[name + "__out"])
+
+
+@pytest.mark.parametrize("name", REJECTED)
+def test_rejects_like_the_reference(name):
+    ref = str(_Z[name + "__err"])
+    cls = fv.UnsupportedJpegFeature if ref == "UnsupportedJpegFeature" else fv.CorruptStream
+    with pytest.raises(cls):
+        fio.decode_jpeg(stream(name))
+
+
+def test_batch_matches_single():
+    outs = fio.decode_jpeg_batch([stream(n) for n in DECODED], threads=8)
+    for n, o in zip(DECODED, outs):
+        assert np.array_equal(o.cpu().numpy(), _Z[n + "__out"]), n
+
+
+def test_batch_raises_first_error():
+    with pytest.raises(fv.CorruptStream):
+        fio.decode_jpeg_batch([stream(DECODED[0]), stream("err_png")])
+
+
+def _pil(arr, **kw):
+    from PIL import Image as PILImage
+    b = pyio.BytesIO()
+    PILImage.fromarray(arr).save(b, format="JPEG", **kw)
+    return b.getvalue()
+
+
+def _oracle_from_coefficients(data):
+    """The oracle's reconstruction (vectorised numpy) of the library's host
+    coefficients; the host entropy decoding is pinned against the oracle in
+    tests/test_jpeg_host.py."""
+    info, coef = fio.decode_coefficients(data)
+    o = O.parse(data)
+    comps = []
+    for e, c in enumerate(o["comps"]):
+        c["bw"], c["bh"] = info.bw[e], info.bh[e]
+        comps.append(coef[info.coef_offset[e]:info.coef_offset[e] + 64 * c["bw"] * c["bh"]].reshape(-1, 64))
+    planes = O.component_planes(o, comps)
+    return planes[0].astype(np.uint8)[:, :, None] if len(planes) == 1 else O.ycbcr_to_rgb(*planes)
+
+
+@pytest.mark.parametrize("sub", [0, 1, 2])
+def test_full_frame_1080p(sub):
+    pytest.importorskip("PIL")
+    arr = synth.seeded_u8_image(1920, 1080, 3, seed=60 + sub)
+    smooth = np.clip(arr.astype(np.int32) // 4 + 96, 0, 255).astype(np.uint8)  # milder spectrum
+    data = _pil(smooth, quality=90, subsampling=sub)
+    got = fio.decode_jpeg(data).cpu().numpy()
+    assert np.array_equal(got, _oracle_from_coefficients(data))
+
+
+def test_odd_sizes_restart_and_gray_full_path():
+    pytest.importorskip("PIL")
+    rng = np.random.default_rng(5)
+    for (w, h, sub, rst) in [(1001, 777, 2, 0), (641, 479, 1, 7), (333, 1, 2, 0), (1, 333, 2, 3)]:
+        arr = rng.integers(0, 256, (h, w, 3), dtype=np.uint8)
+        kw = {"restart_marker_blocks": rst} if rst else {}
+        data = _pil(arr, quality=85, subsampling=sub, **kw)
+        assert np.array_equal(fio.decode_jpeg(data).cpu().numpy(), _oracle_from_coefficients(data)), (w, h)
+    g = rng.integers(0, 256, (123, 457), dtype=np.uint8)
+    data = _pil(g, quality=75)
+    out = fio.decode_jpeg(data).cpu().numpy()
+    assert out.shape == (123, 457, 1)
+    assert np.array_equal(out, _oracle_from_coefficients(data))
+
+
+def test_deterministic_and_native():
+    n0 = _native.lib().fv_launch_count()
+    a = fio.decode_jpeg(stream("pil_photo_256"))
+    b = fio.decode_jpeg(stream("pil_photo_256"))
+    torch.cuda.synchronize()
+    assert torch.equal(a, b)
+    assert _native.lib().fv_launch_count() - n0 == 4  # IDCT + colour kernels per decode
+
+
+def test_decode_then_preprocess():
+    """The chain the row is named for: decoded frame -> fused resize ->
+    normalise -> CHW, against the oracle on the same decoded pixels."""
+    sys.path.insert(0, os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "oracle"))
+    import fovea_oracle as FO
+    img = fio.decode_jpeg(stream("pil_photo_256"))
+    dst = torch.empty((3, 96, 128), dtype=torch.float32, device=img.device)
+    fv.resize_normalize_chw(img, dst, synth.MEAN, synth.STD)
+    ref = FO.resize_normalize_chw(_Z["pil_photo_256__out"], 128, 96, synth.MEAN, synth.STD)
+    assert np.array_equal(dst.cpu().numpy(), ref)
