@@ -190,6 +190,23 @@ int fv_jpeg_decode_coeffs(const uint8_t* data, int64_t len, void* coeffs, int64_
 int fv_jpeg_reconstruct(const FvJpegInfo* info, const void* coeffs, int32_t coef_bytes, uint8_t* planes,
                         uint8_t* dst, int64_t dst_row_pitch, void* stream);
 
+/* Batched form (the runtime around the kernels, native): parse n streams on
+ * `threads` host threads (per-image status in `status`, FV_OK or the error
+ * code; messages via a single-image fv_jpeg_info call), then decode them:
+ * worker threads entropy-decode into the PINNED host buffer coef_host
+ * (int16, image i at coef_off[i]) while the calling thread, in input order,
+ * issues each ready image's H2D copy (coef_dev + coef_off[i]) and its
+ * reconstruction kernels (planes + plane_off[i] -> dst[i], pitch
+ * dst_pitch[i]) on `stream`. Returns the first failing image's code (its
+ * later images are not launched; FV_ERANGE: decode that image singly with
+ * int64 coefficients). */
+int fv_jpeg_info_batch(const uint8_t* const* data, const int64_t* lens, int32_t n, FvJpegInfo* infos,
+                       int32_t* status, int32_t threads);
+int fv_jpeg_decode_batch(const uint8_t* const* data, const int64_t* lens, int32_t n, const FvJpegInfo* infos,
+                         int16_t* coef_host, const int64_t* coef_off, int16_t* coef_dev, uint8_t* planes,
+                         const int64_t* plane_off, uint8_t* const* dst, const int64_t* dst_pitch, int32_t* status,
+                         int32_t threads, void* stream);
+
 /* ---- tuning / introspection ---------------------------------------------
  * Resize kernel selection: 0 = auto (default: exact 2:1 / 1:2 fast paths,
  * else the staged TMA strip kernel, else the direct-gather kernel),

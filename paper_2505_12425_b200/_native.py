@@ -67,6 +67,9 @@ SIGNATURES.update({
     "fv_jpeg_info": ([_P, _I64, _c.POINTER(FvJpegInfo)], _c.c_int),
     "fv_jpeg_decode_coeffs": ([_P, _I64, _P, _I64, _I32], _c.c_int),
     "fv_jpeg_reconstruct": ([_c.POINTER(FvJpegInfo), _P, _I32, _P, _P, _I64, _P], _c.c_int),
+    "fv_jpeg_info_batch": ([_P, _P, _I32, _c.POINTER(FvJpegInfo), _P, _I32], _c.c_int),
+    "fv_jpeg_decode_batch": ([_P, _P, _I32, _c.POINTER(FvJpegInfo), _P, _P, _P, _P, _P, _P, _P, _P, _I32, _P],
+                             _c.c_int),
 })
 
 FV_ECORRUPT, FV_EUNSUPPORTED, FV_ERANGE = -3, -4, -5

@@ -12,10 +12,12 @@
 // samples), then one kernel that upsamples the chroma planes with the
 // reference's integer triangle filters and converts YCbCr -> RGB (16-bit
 // fixed point), writing the HWC u8 image.
+#include <atomic>
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
 #include <memory>
+#include <thread>
 #include <vector>
 
 #include "fv_common.cuh"
@@ -54,10 +56,14 @@ struct Stream {
   bool qt_ok[16] = {};
   Huff dc[16], ac[16];
   int dri = 0;
-  std::vector<uint8_t> seg;       // unstuffed entropy-coded segments, back to back
-  std::vector<int64_t> seg_start;  // nseg + 1 offsets into seg
+  // entropy-coded segments as raw byte ranges of the stream (stuffing and
+  // fill bytes still in place) and their unstuffed lengths
+  std::vector<int64_t> seg_raw;  // nseg + 1 boundaries: segment k is [seg_raw[k], seg_end[k])
+  std::vector<int64_t> seg_end;
+  std::vector<int64_t> seg_len;  // unstuffed bytes
   // geometry (after SOS)
   int hmax = 1, vmax = 1, mcus_x = 0, mcus_y = 0;
+  const uint8_t* data = nullptr;  // the stream (segments point into it)
 };
 
 static int corrupt(const char* fmt, ...) {
@@ -107,30 +113,34 @@ static int build_huff(Huff& t, const uint8_t* bits, const uint8_t* vals, int cou
   return FV_OK;
 }
 
-// Unstuffed segments split at RSTn (jpeg.py:574-602).
+// Segments split at RSTn (jpeg.py:574-602), recorded as raw ranges plus
+// their unstuffed lengths (the bit reader unstuffs on the fly: no copy).
 static int split_scan(const uint8_t* d, int64_t n, int64_t i, Stream& s) {
-  s.seg.clear();
-  s.seg.reserve((size_t)(n - i));
-  s.seg_start.assign(1, 0);
+  s.seg_raw.assign(1, i);
+  s.seg_end.clear();
+  s.seg_len.clear();
+  int64_t len = 0;
   while (i < n) {
-    const uint8_t b = d[i];
-    if (b != 0xFF) {
-      s.seg.push_back(b);
-      ++i;
-      continue;
-    }
+    const uint8_t* f = static_cast<const uint8_t*>(memchr(d + i, 0xFF, (size_t)(n - i)));
+    if (!f) break;
+    len += (f - (d + i));
+    i = f - d;
     if (i + 1 >= n) return corrupt("scan ends mid-marker");
     const uint8_t nx = d[i + 1];
     if (nx == 0x00) {
-      s.seg.push_back(0xFF);
+      ++len;
       i += 2;
     } else if (nx >= 0xD0 && nx <= 0xD7) {
-      s.seg_start.push_back((int64_t)s.seg.size());
+      s.seg_end.push_back(i);
+      s.seg_len.push_back(len);
+      len = 0;
       i += 2;
+      s.seg_raw.push_back(i);
     } else if (nx == 0xFF) {
       i += 1;  // fill byte
     } else {
-      s.seg_start.push_back((int64_t)s.seg.size());
+      s.seg_end.push_back(i);
+      s.seg_len.push_back(len);
       return FV_OK;
     }
   }
@@ -141,6 +151,7 @@ static int split_scan(const uint8_t* d, int64_t n, int64_t i, Stream& s) {
 // then the post-header checks and the MCU geometry (jpeg.py:737-768).
 static int parse(const uint8_t* d, int64_t n, Stream& s) {
   if (!d || n < 4 || d[0] != 0xFF || d[1] != 0xD8) return corrupt("not a JPEG stream (bad SOI)");
+  s.data = d;
   int64_t i = 2;
   for (;;) {
     if (i + 2 > n) return corrupt("stream ends without EOI");
@@ -252,7 +263,7 @@ static int parse(const uint8_t* d, int64_t n, Stream& s) {
   s.mcus_y = (s.height + 8 * s.vmax - 1) / (8 * s.vmax);
   const int64_t total = (int64_t)s.mcus_x * s.mcus_y;
   const int64_t nexp = s.dri ? (total + s.dri - 1) / s.dri : 1;
-  const int64_t nseg = (int64_t)s.seg_start.size() - 1;
+  const int64_t nseg = (int64_t)s.seg_len.size();
   if (nseg < nexp) return corrupt("%lld entropy segments, expected %lld", (long long)nseg, (long long)nexp);
   // Every block consumes at least two bits (a DC and an AC symbol), and a
   // segment may not consume bits past its data: a header claiming more
@@ -260,7 +271,8 @@ static int parse(const uint8_t* d, int64_t n, Stream& s) {
   // (checked here, before any allocation, instead of after decoding).
   int64_t per_mcu = 0;
   for (int e = 0; e < s.nscan; ++e) per_mcu += s.sof[s.scan_comp[e]].h * s.sof[s.scan_comp[e]].v;
-  const int64_t bits = 8 * (s.seg_start[nexp] - s.seg_start[0]);
+  int64_t bits = 0;
+  for (int64_t k = 0; k < nexp; ++k) bits += 8 * s.seg_len[k];
   if (2 * per_mcu * total > bits) return corrupt("entropy segment too short for its MCUs");
   return FV_OK;
 }
@@ -318,16 +330,34 @@ static void fill_info(const Stream& s, FvJpegInfo& f) {
   f.plane_bytes = p;
 }
 
-// MSB-first bit reader over one unstuffed segment; zero bits past its end.
+// MSB-first bit reader over one segment: unstuffs the raw bytes on the fly
+// (FF 00 -> FF, a fill FF is skipped), zero bits past the segment's data.
 struct Bits {
   const uint8_t* p;
-  int64_t n, pos = 0;  // next byte to load
+  int64_t pos, end;      // raw cursor and the segment's terminating marker
+  int64_t fed = 0;       // bytes fed into acc (data or zero padding)
+  int64_t n;             // unstuffed data bytes
   uint64_t acc = 0;
-  int nb = 0;  // valid bits at the top of acc
+  int nb = 0;            // valid bits at the top of acc
   void fill() {
     while (nb <= 56) {
-      acc |= (uint64_t)(pos < n ? p[pos] : 0) << (56 - nb);
-      ++pos;
+      uint32_t b = 0;
+      while (pos < end) {
+        b = p[pos];
+        if (b != 0xFF) {
+          ++pos;
+          break;
+        }
+        if (p[pos + 1] == 0x00) {  // stuffed FF (pos + 1 < end: the segment ends at a marker)
+          pos += 2;
+          break;
+        }
+        ++pos;  // fill FF
+        b = 0;
+      }
+      if (fed >= n) b = 0;  // past the data: zero padding
+      acc |= (uint64_t)b << (56 - nb);
+      ++fed;
       nb += 8;
     }
   }
@@ -336,7 +366,7 @@ struct Bits {
     acc <<= k;
     nb -= k;
   }
-  bool over() const { return pos * 8 - nb > n * 8; }  // consumed bits past the data
+  bool over() const { return fed * 8 - nb > n * 8; }  // consumed bits past the data
 };
 
 static inline int symbol(Bits& b, const Huff& t) {
@@ -369,8 +399,10 @@ static int decode_scan(const Stream& s, const FvJpegInfo& f, T* coeffs) {
   for (int64_t sg = 0; sg < nexp; ++sg) {
     const int64_t cnt = s.dri ? std::min<int64_t>(s.dri, total - sg * s.dri) : total;
     Bits b;
-    b.p = s.seg.data() + s.seg_start[sg];
-    b.n = s.seg_start[sg + 1] - s.seg_start[sg];
+    b.p = s.data;
+    b.pos = s.seg_raw[sg];
+    b.end = s.seg_end[sg];
+    b.n = s.seg_len[sg];
     pred[0] = pred[1] = pred[2] = 0;
     for (int64_t m = 0; m < cnt; ++m, ++mcu) {
       const int64_t my = mcu / s.mcus_x, mx = mcu - my * s.mcus_x;
@@ -596,15 +628,16 @@ int fv_jpeg_decode_coeffs(const uint8_t* data, int64_t len, void* coeffs, int64_
                          : decode_scan<int64_t>(*s, f, static_cast<int64_t*>(coeffs));
 }
 
-int fv_jpeg_reconstruct(const FvJpegInfo* info, const void* coeffs, int32_t coef_bytes, uint8_t* planes,
-                        uint8_t* dst, int64_t dst_row_pitch, void* stream) {
-  if (!info || !coeffs || !planes || !dst) return set_error(FV_EINVAL, "fv_jpeg_reconstruct: null pointer");
-  if (coef_bytes != 2 && coef_bytes != 8) return set_error(FV_EINVAL, "fv_jpeg_reconstruct: coef_bytes must be 2 or 8");
-  const FvJpegInfo& f = *info;
+
+}  // extern "C"
+
+namespace fv {
+namespace jpg {
+static int reconstruct(const FvJpegInfo& f, const void* coeffs, int32_t coef_bytes, uint8_t* planes, uint8_t* dst,
+                       int64_t dst_row_pitch, cudaStream_t st) {
   if (f.ncomp != 1 && f.ncomp != 3) return set_error(FV_EINVAL, "fv_jpeg_reconstruct: ncomp %d", f.ncomp);
   if (dst_row_pitch < (int64_t)f.width * f.ncomp) return set_error(FV_EINVAL, "fv_jpeg_reconstruct: row pitch too small");
   if ((reinterpret_cast<uintptr_t>(planes) & 7) != 0) return set_error(FV_EINVAL, "fv_jpeg_reconstruct: planes not 8-byte aligned");
-  cudaStream_t st = static_cast<cudaStream_t>(stream);
   // distinct components (duplicated scan entries share coefficients and plane)
   IdctArgs ia{};
   ia.coeffs = coeffs;
@@ -647,6 +680,99 @@ int fv_jpeg_reconstruct(const FvJpegInfo* info, const void* coeffs, int32_t coef
   ca.d_rp = dst_row_pitch;
   jpeg_color_kernel<<<dim3((f.width + 255) / 256, f.height), 256, 0, st>>>(ca);
   return check_launch("jpeg_color_kernel");
+}
+
+static int decode_one(const uint8_t* data, int64_t len, void* coeffs, int64_t coef_count, int32_t coef_bytes,
+                      FvJpegInfo* info_out) {
+  std::unique_ptr<Stream> s(new Stream());
+  int rc = parse(data, len, *s);
+  if (rc) return rc;
+  FvJpegInfo f;
+  fill_info(*s, f);
+  if (info_out) *info_out = f;
+  if (coef_count < f.coef_count)
+    return set_error(FV_EINVAL, "fv_jpeg_decode_coeffs: buffer holds %lld coefficients, stream needs %lld",
+                     (long long)coef_count, (long long)f.coef_count);
+  return coef_bytes == 2 ? decode_scan<int16_t>(*s, f, static_cast<int16_t*>(coeffs))
+                         : decode_scan<int64_t>(*s, f, static_cast<int64_t*>(coeffs));
+}
+}  // namespace jpg
+}  // namespace fv
+
+extern "C" {
+
+int fv_jpeg_reconstruct(const FvJpegInfo* info, const void* coeffs, int32_t coef_bytes, uint8_t* planes,
+                        uint8_t* dst, int64_t dst_row_pitch, void* stream) {
+  if (!info || !coeffs || !planes || !dst) return set_error(FV_EINVAL, "fv_jpeg_reconstruct: null pointer");
+  if (coef_bytes != 2 && coef_bytes != 8) return set_error(FV_EINVAL, "fv_jpeg_reconstruct: coef_bytes must be 2 or 8");
+  return reconstruct(*info, coeffs, coef_bytes, planes, dst, dst_row_pitch, static_cast<cudaStream_t>(stream));
+}
+
+int fv_jpeg_info_batch(const uint8_t* const* data, const int64_t* lens, int32_t n, FvJpegInfo* infos,
+                       int32_t* status, int32_t threads) {
+  if (n < 0 || (n > 0 && (!data || !lens || !infos || !status)))
+    return set_error(FV_EINVAL, "fv_jpeg_info_batch: bad arguments");
+  std::atomic<int32_t> next{0};
+  auto work = [&]() {
+    for (int32_t i; (i = next.fetch_add(1)) < n;) {
+      std::unique_ptr<Stream> s(new Stream());
+      status[i] = parse(data[i], lens[i], *s);
+      if (status[i] == FV_OK) fill_info(*s, infos[i]);
+    }
+  };
+  const int nt = std::max(1, std::min<int>(threads, n));
+  std::vector<std::thread> pool;
+  for (int t = 1; t < nt; ++t) pool.emplace_back(work);
+  work();
+  for (auto& t : pool) t.join();
+  return FV_OK;
+}
+
+int fv_jpeg_decode_batch(const uint8_t* const* data, const int64_t* lens, int32_t n, const FvJpegInfo* infos,
+                         int16_t* coef_host, const int64_t* coef_off, int16_t* coef_dev, uint8_t* planes,
+                         const int64_t* plane_off, uint8_t* const* dst, const int64_t* dst_pitch, int32_t* status,
+                         int32_t threads, void* stream) {
+  if (n < 0 || (n > 0 && (!data || !lens || !infos || !coef_host || !coef_off || !coef_dev || !planes ||
+                          !plane_off || !dst || !dst_pitch || !status)))
+    return set_error(FV_EINVAL, "fv_jpeg_decode_batch: bad arguments");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  std::vector<std::atomic<int32_t>> done(n);
+  for (auto& d : done) d.store(1, std::memory_order_relaxed);  // 1 = pending
+  std::atomic<int32_t> next{0};
+  auto work = [&]() {
+    for (int32_t i; (i = next.fetch_add(1)) < n;) {
+      const int rc = decode_one(data[i], lens[i], coef_host + coef_off[i], infos[i].coef_count, 2, nullptr);
+      done[i].store(rc, std::memory_order_release);
+    }
+  };
+  const int nt = std::max(1, std::min<int>(threads, n));
+  std::vector<std::thread> pool;
+  for (int t = 0; t < nt; ++t) pool.emplace_back(work);
+  // in input order, as soon as an image's coefficients are ready: H2D + kernels
+  int first = FV_OK;
+  for (int32_t i = 0; i < n; ++i) {
+    int32_t rc;
+    while ((rc = done[i].load(std::memory_order_acquire)) == 1) std::this_thread::yield();
+    status[i] = rc;
+    if (rc != FV_OK || first != FV_OK) {
+      if (first == FV_OK) first = rc;
+      continue;
+    }
+    const int64_t bytes = infos[i].coef_count * 2;
+    if (cudaMemcpyAsync(coef_dev + coef_off[i], coef_host + coef_off[i], bytes, cudaMemcpyHostToDevice, st) !=
+        cudaSuccess) {
+      first = set_error(FV_ECUDA, "fv_jpeg_decode_batch: H2D: %s", cudaGetErrorString(cudaGetLastError()));
+      status[i] = first;
+      continue;
+    }
+    rc = reconstruct(infos[i], coef_dev + coef_off[i], 2, planes + plane_off[i], dst[i], dst_pitch[i], st);
+    if (rc) {
+      first = rc;
+      status[i] = rc;
+    }
+  }
+  for (auto& t : pool) t.join();
+  return first;
 }
 
 }  // extern "C"

@@ -17,7 +17,7 @@ from __future__ import annotations
 
 import ctypes
 import os
-from concurrent.futures import ThreadPoolExecutor
+import threading
 from typing import Sequence
 
 import torch
@@ -107,22 +107,76 @@ def decode_jpeg(data, device=None) -> torch.Tensor:
     return _reconstruct(info, coef, width, dev)
 
 
+class _Staging:
+    """Pinned host staging for the batched decode, reused across calls. The
+    library copies from it with its own cudaMemcpyAsync (invisible to torch's
+    host allocator), so reuse waits on the event recorded after the last
+    batch's copies."""
+
+    lock = threading.Lock()
+    buf = None
+    event = None
+
+    @classmethod
+    def get(cls, nbytes: int) -> torch.Tensor:
+        if cls.event is not None:
+            cls.event.synchronize()
+        if cls.buf is None or cls.buf.numel() < nbytes:
+            cls.buf = None
+            cls.buf = torch.empty(max(nbytes, 1 << 20), dtype=torch.uint8, pin_memory=True)
+        return cls.buf
+
+
 def decode_jpeg_batch(streams: Sequence, device=None, threads: int | None = None) -> list:
-    """Decode many streams: host entropy decoding on `threads` host threads
-    (default: the usable cores), reconstruction kernels on the current stream.
-    Raises the first stream's error, in input order."""
+    """Decode many streams with the native batch runtime
+    (`fv_jpeg_info_batch` / `fv_jpeg_decode_batch`): headers and entropy
+    decoding on `threads` host threads (default: the usable cores); each
+    image's H2D copy and kernels are issued on the current stream as soon as
+    its coefficients are ready, in input order. Raises the first failing
+    stream's error (input order), as a loop of `decode_jpeg` calls would."""
     dev = _device(device)
     bufs = [_bytes(d) for d in streams]
+    n = len(bufs)
+    if n == 0:
+        return []
     threads = threads or max(1, len(os.sched_getaffinity(0)))
-
-    def host(buf):
-        info = jpeg_info(buf)
-        coef, width = _decode_coeffs(buf, info, pinned=True)
-        return info, coef, width
-
-    with ThreadPoolExecutor(max_workers=min(threads, max(1, len(bufs)))) as ex:
-        parts = list(ex.map(host, bufs))
-    return [_reconstruct(info, coef, width, dev) for info, coef, width in parts]
+    lib = _native.lib()
+    data = (ctypes.c_char_p * n)(*bufs)
+    lens = (ctypes.c_int64 * n)(*[len(b) for b in bufs])
+    infos = (_native.FvJpegInfo * n)()
+    status = (ctypes.c_int32 * n)()
+    lib.fv_jpeg_info_batch(data, lens, n, infos, status, threads)
+    for i in range(n):
+        if status[i]:
+            jpeg_info(bufs[i])  # raises with the message
+    coef_off, plane_off = [], []
+    c = p = 0
+    for f in infos:
+        coef_off.append(c)
+        plane_off.append(p)
+        c += (int(f.coef_count) + 63) // 64 * 64
+        p += (int(f.plane_bytes) + 255) // 256 * 256
+    outs = [torch.empty((f.height, f.width, f.ncomp), dtype=torch.uint8, device=dev) for f in infos]
+    coef_dev = torch.empty(max(c, 1), dtype=torch.int16, device=dev)
+    planes = torch.empty(max(p, 256), dtype=torch.uint8, device=dev)
+    stream = torch.cuda.current_stream(dev)
+    with _Staging.lock:
+        host = _Staging.get(2 * c)
+        rc = lib.fv_jpeg_decode_batch(
+            data, lens, n, infos, host.data_ptr(), (ctypes.c_int64 * n)(*coef_off), coef_dev.data_ptr(),
+            planes.data_ptr(), (ctypes.c_int64 * n)(*plane_off), (ctypes.c_void_p * n)(*[o.data_ptr() for o in outs]),
+            (ctypes.c_int64 * n)(*[o.stride(0) for o in outs]), status, threads, stream.cuda_stream)
+        _Staging.event = torch.cuda.Event()
+        _Staging.event.record(stream)
+    if rc:
+        i = next(k for k in range(n) if status[k])
+        if status[i] != _native.FV_ERANGE:
+            decode_jpeg(bufs[i], dev)  # raises with the message
+            _raise(status[i], "fv_jpeg_decode_batch")
+        # a DC coefficient beyond int16: this image with int64 coefficients, then the rest
+        outs[i] = decode_jpeg(bufs[i], dev)
+        outs[i + 1:] = decode_jpeg_batch(bufs[i + 1:], dev, threads)
+    return outs
 
 
 def decoded_shape(data) -> tuple:

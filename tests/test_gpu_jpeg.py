@@ -54,6 +54,19 @@ def test_batch_matches_single():
 def test_batch_raises_first_error():
     with pytest.raises(fv.CorruptStream):
         fio.decode_jpeg_batch([stream(DECODED[0]), stream("err_png")])
+    with pytest.raises(fv.UnsupportedJpegFeature):  # header error vs entropy error: input order decides
+        fio.decode_jpeg_batch([stream("err_progressive"), stream("fuzz_mut_03")])
+
+
+def test_batch_int16_overflow_image_and_repeats():
+    """An image whose DC exceeds int16 inside a batch takes the int64 path;
+    the others still come from the batched runtime; reusing the pinned
+    staging across calls stays correct."""
+    names = ["pil_photo_256", "asm_gray_dc_int16_overflow", "pil_ss2_q85", "asm_440_q85"]
+    for _ in range(3):
+        outs = fio.decode_jpeg_batch([stream(n) for n in names], threads=3)
+        for n, o in zip(names, outs):
+            assert np.array_equal(o.cpu().numpy(), _Z[n + "__out"]), n
 
 
 def _pil(arr, **kw):
