@@ -9,7 +9,9 @@ a batch of 64 3840x2160x3 images down to 1920x1080x3 AND up to 7680x4320x3
 second over the whole job, inputs resident in HBM (1.59 GB of source >> the
 126 MB L2, so no flush is needed between steps). The other four configs are
 measured the same way and reported under "ops" (cfg0 rotates over 32 distinct
-images, 265 MB, so every step reads from HBM, not L2).
+images, 265 MB, so every step reads from HBM, not L2), plus the decode ->
+preprocess row (64 host-resident 1080p JPEGs decoded and
+resized/normalised to 3x640x640 per step, host entropy decoding included).
 
 Multi-GPU: one process per GPU (torchrun), each rank takes a contiguous shard
 of the images, no collective on the data path; a host barrier plus
@@ -227,7 +229,71 @@ def build_ops(n_scale, world, rank, dev, include):
                        lambda s=src, d=dst: fv.resize_normalize_chw(s, d, synth.MEAN, synth.STD),
                        n * (1920 * 1080 * 3 + 3 * 640 * 640 * 4))],
             dst_px=n * 640 * 640, src_px=n * 1920 * 1080, images=n_total, l2="inputs 3.2 GB >> L2")
+
+    if "jpeg" in include:
+        # SURVEY 8f rank 4, decode -> preprocess: host JPEG bytes -> decode
+        # (native batch runtime: threaded entropy decoding, GPU IDCT/colour)
+        # -> fused resize/normalise/CHW 640x640, per step
+        n_total = 64
+        lo, hi = shard(n_total, world, rank)
+        streams = jpeg_streams(lo, hi)
+        dst = torch.empty((hi - lo, 3, 640, 640), dtype=torch.float32, device=dev)
+        from paper_2505_12425_b200 import io as fio
+
+        def step(st=streams, d=dst):
+            for k, img in enumerate(fio.decode_jpeg_batch(st, dev)):
+                fv.resize_normalize_chw(img, d[k], synth.MEAN, synth.STD)
+
+        nbytes = sum(len(b) for b in streams) + dst.numel() * 4
+        ops["f4_jpeg_decode_preprocess_64x1080p"] = dict(
+            launches=[("jpeg_decode+preprocess (host entropy + GPU)", step, nbytes)],
+            dst_px=(hi - lo) * 1920 * 1080, src_px=(hi - lo) * 1920 * 1080, images=n_total,
+            l2="host JPEG bytes (q90 4:2:0, ~200 KB each); bound by host entropy decoding",
+            extra={"mean_stream_kb": round(sum(len(b) for b in streams) / len(streams) / 1e3, 1),
+                   "host_threads": host_cores(), "px_basis": "decoded 1920x1080 pixels",
+                   "cpu_oracle_mps_1core": jpeg_cpu_oracle_mps()})
     return ops
+
+
+def jpeg_streams(lo, hi):
+    """Seeded smooth 1080p frames (synth.seeded_smooth_u8_image, the
+    reference's codec fixture) as Pillow q90 4:2:0 JPEGs: 4 base frames,
+    each image a distinct cyclic shift of one of them."""
+    import io as pyio
+
+    import numpy as np
+    from PIL import Image
+
+    from paper_2505_12425_b200 import synth
+
+    bases = [synth.seeded_smooth_u8_image(1920, 1080, 3, seed=70000 + b) for b in range(4)]
+    out = []
+    for i in range(lo, hi):
+        img = np.roll(bases[i % 4], shift=(37 * i, 101 * i), axis=(0, 1))
+        buf = pyio.BytesIO()
+        Image.fromarray(img).save(buf, format="JPEG", quality=90, subsampling=2)
+        out.append(buf.getvalue())
+    return out
+
+
+def jpeg_cpu_oracle_mps():
+    """The oracle port of the reference decoder (oracle/jpeg_oracle.py, pure
+    Python like the reference) on one 480x270 frame, one core: decoded MP/s."""
+    import io as pyio
+
+    from PIL import Image
+
+    from paper_2505_12425_b200 import synth
+
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import jpeg_oracle
+
+    buf = pyio.BytesIO()
+    Image.fromarray(synth.seeded_smooth_u8_image(480, 270, 3, seed=1)).save(buf, format="JPEG", quality=90,
+                                                                           subsampling=2)
+    t = time.perf_counter()
+    jpeg_oracle.decode_jpeg(buf.getvalue())
+    return round(480 * 270 / (time.perf_counter() - t) / 1e6, 3)
 
 
 def footprint_bytes(mats, perspective, h, w, bpp, dev):
@@ -476,7 +542,7 @@ def main():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="fovea", choices=["fovea", "reference"])
-    ap.add_argument("--ops", default="gray,resize,affine,persp,fused")
+    ap.add_argument("--ops", default="gray,resize,affine,persp,fused,jpeg")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-cores", type=int, default=0)
@@ -550,7 +616,7 @@ def main():
 
     summary = {}
     for name, r in results.items():
-        summary[name] = {"dst_mps": job_mps(name), "ms_per_step": r["ms_per_step"],
+        summary[name] = {"dst_mps": job_mps(name), "ms_per_step": r["ms_per_step"], **r["op"].get("extra", {}),
                          "kernels": [{k: (round(v, 4) if isinstance(v, float) else v) for k, v in kk.items()}
                                      for kk in r["kernels"]],
                          "l2": r["op"]["l2"]}
@@ -609,6 +675,7 @@ def per_batch_dst_px(name):
         "cfg2_warp_affine_f32_32x1080p": 32 * 1920 * 1080,
         "cfg3_warp_perspective_u8_16x4k": 16 * 3840 * 2160,
         "cfg4_resize_normalize_chw_512x1080p": 512 * 640 * 640,
+        "f4_jpeg_decode_preprocess_64x1080p": 64 * 1920 * 1080,
     }[name]
 
 
