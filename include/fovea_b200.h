@@ -182,6 +182,7 @@ typedef struct FvJpegInfo {
   int64_t coef_count;                  /* coefficients in the buffer (64 per block) */
   int64_t plane_offset[3];             /* byte offset of each u8 plane (pitch bw*8) */
   int64_t plane_bytes;                 /* plane scratch bytes */
+  int64_t sparse_words;                /* batch runtime: bound of the sparse coefficient words */
   uint16_t qt[3][64];                  /* quantisation table per component, natural order */
 } FvJpegInfo;
 
@@ -193,17 +194,19 @@ int fv_jpeg_reconstruct(const FvJpegInfo* info, const void* coeffs, int32_t coef
 /* Batched form (the runtime around the kernels, native): parse n streams on
  * `threads` host threads (per-image status in `status`, FV_OK or the error
  * code; messages via a single-image fv_jpeg_info call), then decode them:
- * worker threads entropy-decode into the PINNED host buffer coef_host
- * (int16, image i at coef_off[i]) while the calling thread, in input order,
- * issues each ready image's H2D copy (coef_dev + coef_off[i]) and its
- * reconstruction kernels (planes + plane_off[i] -> dst[i], pitch
- * dst_pitch[i]) on `stream`. Returns the first failing image's code (its
- * later images are not launched; FV_ERANGE: decode that image singly with
- * int64 coefficients). */
+ * worker threads entropy-decode each image into a SPARSE coefficient stream
+ * in the PINNED host buffer `words_host` (image i at word_off[i], capacity
+ * coef_count/64 + sparse_words words: one header index per block, then per
+ * block a count word and one (int16 value << 16 | natural position) word per
+ * stored coefficient) while the calling thread, in input order, copies each
+ * ready image's used words to words_dev + word_off[i] and launches its
+ * reconstruction (planes + plane_off[i] -> dst[i], row pitch dst_pitch[i])
+ * on `stream`. Returns the first failing image's code (later images are not
+ * launched; FV_ERANGE: decode that image singly with int64 coefficients). */
 int fv_jpeg_info_batch(const uint8_t* const* data, const int64_t* lens, int32_t n, FvJpegInfo* infos,
                        int32_t* status, int32_t threads);
 int fv_jpeg_decode_batch(const uint8_t* const* data, const int64_t* lens, int32_t n, const FvJpegInfo* infos,
-                         int16_t* coef_host, const int64_t* coef_off, int16_t* coef_dev, uint8_t* planes,
+                         uint32_t* words_host, const int64_t* word_off, uint32_t* words_dev, uint8_t* planes,
                          const int64_t* plane_off, uint8_t* const* dst, const int64_t* dst_pitch, int32_t* status,
                          int32_t threads, void* stream);
 

@@ -58,7 +58,7 @@ class FvJpegInfo(_c.Structure):
         ("restart_interval", _I32),
         ("h", _I32 * 3), ("v", _I32 * 3), ("bw", _I32 * 3), ("bh", _I32 * 3), ("cw", _I32 * 3), ("ch", _I32 * 3),
         ("coef_offset", _I64 * 3), ("coef_count", _I64),
-        ("plane_offset", _I64 * 3), ("plane_bytes", _I64),
+        ("plane_offset", _I64 * 3), ("plane_bytes", _I64), ("sparse_words", _I64),
         ("qt", (_c.c_uint16 * 64) * 3),
     ]
 

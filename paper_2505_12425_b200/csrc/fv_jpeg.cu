@@ -33,8 +33,14 @@ static const int kZigzag[64] = {0,  1,  8,  16, 9,  2,  3,  10, 17, 24, 32, 25, 
 
 // Canonical Huffman table (jpeg.py:269-296): 8-bit lookup for short codes,
 // per-length ranges for the rest.
+// Fast table entries, indexed by the next 10 bits: kFull = code and its
+// magnitude bits both fit: total length (bits 0-4), zero run (8-11), signed
+// value (16-31); kSym = the code fits: its length (0-4) and symbol (16-23).
+constexpr int32_t kFull = 1 << 12, kSym = 1 << 13;
+
 struct Huff {
   bool present = false;
+  int32_t fast[1 << 10];
   uint8_t lut_len[256];  // 0 = no code of <= 8 bits has this prefix
   uint8_t lut_val[256];
   int32_t mincode[17], maxcode[17], valptr[17];
@@ -83,7 +89,9 @@ static int unsupported(const char* fmt, ...) {
   return set_error(FV_EUNSUPPORTED, "%s", msg);
 }
 
-static int build_huff(Huff& t, const uint8_t* bits, const uint8_t* vals, int count) {
+static inline int64_t extend(uint32_t v, int size);
+
+static int build_huff(Huff& t, const uint8_t* bits, const uint8_t* vals, int count, bool dc) {
   memset(t.lut_len, 0, sizeof(t.lut_len));
   memcpy(t.values, vals, count);
   int code = 0, idx = 0;
@@ -108,6 +116,23 @@ static int build_huff(Huff& t, const uint8_t* bits, const uint8_t* vals, int cou
       t.maxcode[len] = code - 1;
     }
     code <<= 1;
+  }
+  for (int x = 0; x < (1 << 10); ++x) {
+    t.fast[x] = 0;
+    for (int len = 1; len <= 10; ++len) {
+      const int code = x >> (10 - len);
+      if (t.maxcode[len] < 0 || code > t.maxcode[len]) continue;
+      const int sym = t.values[t.valptr[len] + code - t.mincode[len]];
+      const int size = dc ? sym : (sym & 15);
+      const bool valid = dc ? size <= 11 : size > 0;  // DC: the size check stays on the slow path
+      if (valid && len + size <= 10) {
+        const int64_t v = size ? extend((uint32_t)(x >> (10 - len - size)) & ((1u << size) - 1), size) : 0;
+        t.fast[x] = kFull | (len + size) | ((dc ? 0 : sym >> 4) << 8) | (int32_t)((uint32_t)(v & 0xFFFF) << 16);
+      } else {
+        t.fast[x] = kSym | len | (sym << 16);
+      }
+      break;
+    }
   }
   t.present = true;
   return FV_OK;
@@ -218,7 +243,7 @@ static int parse(const uint8_t* d, int64_t n, Stream& s) {
         int cnt = 0;
         for (int k = 1; k <= 16; ++k) cnt += pl[p + k];
         if (p + 17 + cnt > pn) return corrupt("truncated DHT values");
-        const int rc = build_huff(tc == 0 ? s.dc[th] : s.ac[th], pl + p + 1, pl + p + 17, cnt);
+        const int rc = build_huff(tc == 0 ? s.dc[th] : s.ac[th], pl + p + 1, pl + p + 17, cnt, tc == 0);
         if (rc) return rc;
         p += 17 + cnt;
       }
@@ -291,6 +316,8 @@ static int distinct(const Stream& s, int (&slot)[3]) {
   return nd;
 }
 
+static int64_t sparse_cap(const Stream& s);
+
 static void fill_info(const Stream& s, FvJpegInfo& f) {
   memset(&f, 0, sizeof(f));
   f.width = s.width;
@@ -328,6 +355,7 @@ static void fill_info(const Stream& s, FvJpegInfo& f) {
   }
   f.coef_count = c;
   f.plane_bytes = p;
+  f.sparse_words = sparse_cap(s);
 }
 
 // MSB-first bit reader over one segment: unstuffs the raw bytes on the fly
@@ -340,6 +368,24 @@ struct Bits {
   uint64_t acc = 0;
   int nb = 0;            // valid bits at the top of acc
   void fill() {
+    if (nb > 56) return;
+    // fast path: the next 8 raw bytes are data and hold no 0xFF (SWAR test
+    // for a zero byte in ~w): append the k = (64 - nb) / 8 bytes at once
+    if (pos + 8 <= end && fed + 8 <= n) {
+      uint64_t w;
+      memcpy(&w, p + pos, 8);
+      const uint64_t x = ~w;
+      if (((x - 0x0101010101010101ull) & ~x & 0x8080808080808080ull) == 0) {
+        const int k = (64 - nb) >> 3;
+        uint64_t be = __builtin_bswap64(w);
+        if (k < 8) be &= ~((1ull << (64 - 8 * k)) - 1);
+        acc |= be >> nb;
+        pos += k;
+        fed += k;
+        nb += 8 * k;
+        return;
+      }
+    }
     while (nb <= 56) {
       uint32_t b = 0;
       while (pos < end) {
@@ -390,8 +436,61 @@ static inline int64_t extend(uint32_t v, int size) {
 }
 
 // Entropy decoding (jpeg.py:326-409, 770-780) into `coeffs`.
+// Where decoded blocks go. Dense<T>: 64 coefficients per block in natural
+// order (the standalone ABI and the int64 path). Sparse: per block a header
+// word (count) plus one word per stored coefficient, (int16 value << 16) |
+// natural position, and the block's header index in `ptr` -- what the batch
+// runtime ships to the GPU (no host zero-fill, ~3x fewer H2D bytes).
 template <typename T>
-static int decode_scan(const Stream& s, const FvJpegInfo& f, T* coeffs) {
+struct Dense {
+  T* coeffs;
+  T* blk = nullptr;
+  bool begin(const FvJpegInfo& f, int e, int64_t rb) {
+    blk = coeffs + f.coef_offset[e] + 64 * rb;
+    for (int z = 0; z < 64; ++z) blk[z] = 0;
+    return true;
+  }
+  void put(int pos, int64_t v) { blk[pos] = (T)v; }
+  void end() {}
+  static constexpr bool kInt16 = sizeof(T) == 2;
+};
+
+struct Sparse {
+  uint32_t* ptr;  // header index of each block (component blocks concatenated)
+  uint32_t* ent;
+  int64_t cap, cur = 0, hdr = 0;
+  uint32_t cnt = 0;
+  bool begin(const FvJpegInfo& f, int e, int64_t rb) {
+    if (cur + 65 > cap) return false;
+    ptr[f.coef_offset[e] / 64 + rb] = (uint32_t)cur;
+    hdr = cur++;
+    cnt = 0;
+    return true;
+  }
+  void put(int pos, int64_t v) {
+    ent[cur++] = ((uint32_t)(uint16_t)(int16_t)v << 16) | (uint32_t)pos;
+    ++cnt;
+  }
+  void end() { ent[hdr] = cnt; }
+  static constexpr bool kInt16 = true;
+};
+
+// Upper bound of the sparse entry words of a well-formed scan: a header and
+// a DC word per decoded block, and each further word costs >= 2 bits (an AC
+// symbol and its magnitude). Exceeding it means padding bits were consumed,
+// i.e. the stream is corrupt (the reference's end-of-segment check).
+static int64_t sparse_cap(const Stream& s) {
+  int64_t per_mcu = 0, bits = 0;
+  for (int e = 0; e < s.nscan; ++e) per_mcu += s.sof[s.scan_comp[e]].h * s.sof[s.scan_comp[e]].v;
+  const int64_t total = (int64_t)s.mcus_x * s.mcus_y;
+  const int64_t nexp = s.dri ? (total + s.dri - 1) / s.dri : 1;
+  for (int64_t k = 0; k < nexp; ++k) bits += 8 * s.seg_len[k];
+  return 2 * per_mcu * total + bits / 2 + 65;
+}
+
+// Entropy decoding (jpeg.py:326-409, 770-780).
+template <class Sink>
+static int decode_scan(const Stream& s, const FvJpegInfo& f, Sink& sink) {
   int64_t pred[3] = {0, 0, 0};  // per SOF component (duplicated scan entries share it)
   const int64_t total = (int64_t)s.mcus_x * s.mcus_y;
   const int64_t nexp = s.dri ? (total + s.dri - 1) / s.dri : 1;
@@ -413,23 +512,50 @@ static int decode_scan(const Stream& s, const FvJpegInfo& f, T* coeffs) {
         const Huff& act = s.ac[cp.ta];
         for (int by = 0; by < cp.v; ++by)
           for (int bx = 0; bx < cp.h; ++bx) {
-            T* blk = coeffs + f.coef_offset[e] + 64 * ((my * cp.v + by) * (int64_t)f.bw[e] + mx * cp.h + bx);
-            for (int z = 0; z < 64; ++z) blk[z] = 0;
+            if (!sink.begin(f, e, (my * cp.v + by) * (int64_t)f.bw[e] + mx * cp.h + bx))
+              return corrupt("entropy segment too short for its MCUs");
             b.fill();
-            const int size = symbol(b, dct);
-            if (size < 0) return corrupt("invalid Huffman code");
-            if (size) {
-              if (size > 11) return corrupt("bad DC size %d", size);
-              const uint32_t v = b.peek(size);
-              b.skip(size);
-              pred[k] += extend(v, size);
+            const int32_t fd = dct.fast[b.peek(10)];
+            if (fd & kFull) {
+              b.skip(fd & 31);
+              pred[k] += fd >> 16;
+            } else {
+              int size;
+              if (fd & kSym) {
+                b.skip(fd & 31);
+                size = (fd >> 16) & 0xFF;
+              } else {
+                size = symbol(b, dct);
+              }
+              if (size < 0) return corrupt("invalid Huffman code");
+              if (size) {
+                if (size > 11) return corrupt("bad DC size %d", size);
+                const uint32_t v = b.peek(size);
+                b.skip(size);
+                pred[k] += extend(v, size);
+              }
             }
-            if (sizeof(T) == 2 && (pred[k] < -32768 || pred[k] > 32767))
+            if (Sink::kInt16 && (pred[k] < -32768 || pred[k] > 32767))
               return set_error(FV_ERANGE, "DC coefficient %lld does not fit int16", (long long)pred[k]);
-            blk[0] = (T)pred[k];
+            sink.put(0, pred[k]);
             for (int z = 1; z < 64;) {
               b.fill();
-              const int rs = symbol(b, act);
+              const int32_t fa = act.fast[b.peek(10)];
+              if (fa & kFull) {  // code + magnitude in one lookup
+                b.skip(fa & 31);
+                z += (fa >> 8) & 15;
+                if (z > 63) return corrupt("AC run past end of block");
+                sink.put(kZigzag[z], fa >> 16);
+                ++z;
+                continue;
+              }
+              int rs;
+              if (fa & kSym) {
+                b.skip(fa & 31);
+                rs = (fa >> 16) & 0xFF;
+              } else {
+                rs = symbol(b, act);
+              }
               if (rs < 0) return corrupt("invalid Huffman code");
               const int sz = rs & 15;
               if (sz == 0) {
@@ -443,9 +569,10 @@ static int decode_scan(const Stream& s, const FvJpegInfo& f, T* coeffs) {
               if (z > 63) return corrupt("AC run past end of block");
               const uint32_t v = b.peek(sz);
               b.skip(sz);
-              blk[kZigzag[z]] = (T)extend(v, sz);  // |v| < 2^15: fits int16
+              sink.put(kZigzag[z], extend(v, sz));  // |v| < 2^15: fits int16
               ++z;
             }
+            sink.end();
           }
       }
     }
@@ -491,6 +618,28 @@ __device__ __forceinline__ void idct8(const int64_t (&s)[8], int64_t (&o)[8]) {
   o[7] = a10 - o3;
 }
 
+// Second half of a block's IDCT, shared by the dense and sparse kernels:
+// s = the dequantised column j (vertical frequencies 0..7) of block g.
+__device__ __forceinline__ void idct_rows_store(int64_t (&s)[8], int64_t (&ws)[16][8][9], int g, int j, uint32_t mask,
+                                                uint8_t* dst) {
+  int64_t o[8];
+  idct8(s, o);
+#pragma unroll
+  for (int k = 0; k < 8; ++k) ws[g][k][j] = (o[k] + (1 << 10)) >> 11;
+  __syncwarp(mask);
+#pragma unroll
+  for (int k = 0; k < 8; ++k) s[k] = ws[g][j][k];
+  idct8(s, o);
+  uint32_t w[2] = {0, 0};
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    int64_t v = ((o[k] + (1 << 17)) >> 18) + 128;
+    v = v < 0 ? 0 : (v > 255 ? 255 : v);
+    w[k >> 2] |= (uint32_t)v << (8 * (k & 3));
+  }
+  *reinterpret_cast<uint2*>(dst) = make_uint2(w[0], w[1]);
+}
+
 // 16 JPEG blocks per CTA, 8 threads per block: thread j runs the vertical
 // pass on column j, then the horizontal pass on row j, and stores row j
 // (8 samples, one 8-byte store) into the component plane.
@@ -504,27 +653,43 @@ __global__ void __launch_bounds__(128) jpeg_idct_kernel(const __grid_constant__ 
   while (c + 1 < a.ncomp && blk >= a.first_block[c + 1]) ++c;
   const int64_t lb = blk - a.first_block[c];
   const T* co = reinterpret_cast<const T*>(a.coeffs) + a.coef_offset[c] + 64 * lb;
-  int64_t s[8], o[8];
+  int64_t s[8];
 #pragma unroll
   for (int k = 0; k < 8; ++k) s[k] = (int64_t)co[8 * k + j] * (int64_t)a.qt[c][8 * k + j];
-  idct8(s, o);
-#pragma unroll
-  for (int k = 0; k < 8; ++k) ws[g][k][j] = (o[k] + (1 << 10)) >> 11;
-  __syncwarp(0xFFu << (threadIdx.x & 24));  // this block's 8 lanes
-#pragma unroll
-  for (int k = 0; k < 8; ++k) s[k] = ws[g][j][k];
-  idct8(s, o);
-  uint32_t w[2] = {0, 0};
-#pragma unroll
-  for (int k = 0; k < 8; ++k) {
-    int64_t v = ((o[k] + (1 << 17)) >> 18) + 128;
-    v = v < 0 ? 0 : (v > 255 ? 255 : v);
-    w[k >> 2] |= (uint32_t)v << (8 * (k & 3));
-  }
   const int64_t by = lb / a.bw[c], bx = lb - by * a.bw[c];
-  const int64_t pitch = (int64_t)a.bw[c] * 8;
-  uint8_t* dst = a.planes + a.plane_offset[c] + (by * 8 + j) * pitch + bx * 8;
-  *reinterpret_cast<uint2*>(dst) = make_uint2(w[0], w[1]);
+  uint8_t* dst = a.planes + a.plane_offset[c] + (by * 8 + j) * (int64_t)a.bw[c] * 8 + bx * 8;
+  idct_rows_store(s, ws, g, j, 0xFFu << (threadIdx.x & 24), dst);
+}
+
+// Same, from the batch runtime's sparse stream: the block's 8 threads zero
+// a SMEM block, scatter its stored coefficients, then run the IDCT.
+__global__ void __launch_bounds__(128) jpeg_idct_sparse_kernel(const __grid_constant__ IdctArgs a, const uint32_t* words,
+                                                               int64_t nblk) {
+  __shared__ int64_t ws[16][8][9];
+  __shared__ int32_t cb[16][64];
+  const int g = threadIdx.x >> 3, j = threadIdx.x & 7;
+  const uint32_t mask = 0xFFu << (threadIdx.x & 24);
+  const int64_t blk = (int64_t)blockIdx.x * 16 + g;
+  if (blk >= a.first_block[a.ncomp]) return;
+  int c = 0;
+  while (c + 1 < a.ncomp && blk >= a.first_block[c + 1]) ++c;
+  const int64_t lb = blk - a.first_block[c];
+  const uint32_t* ent = words + nblk + words[blk];
+  const uint32_t n = ent[0];
+#pragma unroll
+  for (int z = j; z < 64; z += 8) cb[g][z] = 0;
+  __syncwarp(mask);
+  for (uint32_t i = j; i < n; i += 8) {
+    const uint32_t w = ent[1 + i];
+    cb[g][w & 63] = (int32_t)(int16_t)(w >> 16);
+  }
+  __syncwarp(mask);
+  int64_t s[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) s[k] = (int64_t)cb[g][8 * k + j] * (int64_t)a.qt[c][8 * k + j];
+  const int64_t by = lb / a.bw[c], bx = lb - by * a.bw[c];
+  uint8_t* dst = a.planes + a.plane_offset[c] + (by * 8 + j) * (int64_t)a.bw[c] * 8 + bx * 8;
+  idct_rows_store(s, ws, g, j, mask, dst);
 }
 
 struct ColorArgs {
@@ -624,8 +789,12 @@ int fv_jpeg_decode_coeffs(const uint8_t* data, int64_t len, void* coeffs, int64_
   if (coef_count < f.coef_count)
     return set_error(FV_EINVAL, "fv_jpeg_decode_coeffs: buffer holds %lld coefficients, stream needs %lld",
                      (long long)coef_count, (long long)f.coef_count);
-  return coef_bytes == 2 ? decode_scan<int16_t>(*s, f, static_cast<int16_t*>(coeffs))
-                         : decode_scan<int64_t>(*s, f, static_cast<int64_t*>(coeffs));
+  if (coef_bytes == 2) {
+    Dense<int16_t> sink{static_cast<int16_t*>(coeffs)};
+    return decode_scan(*s, f, sink);
+  }
+  Dense<int64_t> sink{static_cast<int64_t*>(coeffs)};
+  return decode_scan(*s, f, sink);
 }
 
 
@@ -633,6 +802,8 @@ int fv_jpeg_decode_coeffs(const uint8_t* data, int64_t len, void* coeffs, int64_
 
 namespace fv {
 namespace jpg {
+// coef_bytes 2 / 8: dense int16 / int64 coefficients; 4: the sparse word
+// stream of the batch runtime
 static int reconstruct(const FvJpegInfo& f, const void* coeffs, int32_t coef_bytes, uint8_t* planes, uint8_t* dst,
                        int64_t dst_row_pitch, cudaStream_t st) {
   if (f.ncomp != 1 && f.ncomp != 3) return set_error(FV_EINVAL, "fv_jpeg_reconstruct: ncomp %d", f.ncomp);
@@ -661,7 +832,8 @@ static int reconstruct(const FvJpegInfo& f, const void* coeffs, int32_t coef_byt
   const int64_t grid = (nb + 15) / 16;
   if (grid > 0x7FFFFFFF) return set_error(FV_EINVAL, "fv_jpeg_reconstruct: too many blocks");
   if (coef_bytes == 2) jpeg_idct_kernel<int16_t><<<(unsigned)grid, 128, 0, st>>>(ia);
-  else jpeg_idct_kernel<int64_t><<<(unsigned)grid, 128, 0, st>>>(ia);
+  else if (coef_bytes == 8) jpeg_idct_kernel<int64_t><<<(unsigned)grid, 128, 0, st>>>(ia);
+  else jpeg_idct_sparse_kernel<<<(unsigned)grid, 128, 0, st>>>(ia, static_cast<const uint32_t*>(coeffs), f.coef_count / 64);
   int rc = check_launch("jpeg_idct_kernel");
   if (rc) return rc;
   ColorArgs ca{};
@@ -693,8 +865,28 @@ static int decode_one(const uint8_t* data, int64_t len, void* coeffs, int64_t co
   if (coef_count < f.coef_count)
     return set_error(FV_EINVAL, "fv_jpeg_decode_coeffs: buffer holds %lld coefficients, stream needs %lld",
                      (long long)coef_count, (long long)f.coef_count);
-  return coef_bytes == 2 ? decode_scan<int16_t>(*s, f, static_cast<int16_t*>(coeffs))
-                         : decode_scan<int64_t>(*s, f, static_cast<int64_t*>(coeffs));
+  if (coef_bytes == 2) {
+    Dense<int16_t> sink{static_cast<int16_t*>(coeffs)};
+    return decode_scan(*s, f, sink);
+  }
+  Dense<int64_t> sink{static_cast<int64_t*>(coeffs)};
+  return decode_scan(*s, f, sink);
+}
+
+// Batch worker: parse + sparse entropy decoding into `words` (block header
+// indices first, then the entries); *used = words written.
+static int decode_one_sparse(const uint8_t* data, int64_t len, uint32_t* words, int64_t nwords, int64_t* used) {
+  std::unique_ptr<Stream> s(new Stream());
+  int rc = parse(data, len, *s);
+  if (rc) return rc;
+  FvJpegInfo f;
+  fill_info(*s, f);
+  const int64_t nblk = f.coef_count / 64;
+  if (nwords < nblk + f.sparse_words) return set_error(FV_EINVAL, "fv_jpeg_decode_batch: sparse buffer too small");
+  Sparse sink{words, words + nblk, f.sparse_words};
+  rc = decode_scan(*s, f, sink);
+  *used = nblk + sink.cur;
+  return rc;
 }
 }  // namespace jpg
 }  // namespace fv
@@ -729,26 +921,29 @@ int fv_jpeg_info_batch(const uint8_t* const* data, const int64_t* lens, int32_t 
 }
 
 int fv_jpeg_decode_batch(const uint8_t* const* data, const int64_t* lens, int32_t n, const FvJpegInfo* infos,
-                         int16_t* coef_host, const int64_t* coef_off, int16_t* coef_dev, uint8_t* planes,
+                         uint32_t* words_host, const int64_t* word_off, uint32_t* words_dev, uint8_t* planes,
                          const int64_t* plane_off, uint8_t* const* dst, const int64_t* dst_pitch, int32_t* status,
                          int32_t threads, void* stream) {
-  if (n < 0 || (n > 0 && (!data || !lens || !infos || !coef_host || !coef_off || !coef_dev || !planes ||
+  if (n < 0 || (n > 0 && (!data || !lens || !infos || !words_host || !word_off || !words_dev || !planes ||
                           !plane_off || !dst || !dst_pitch || !status)))
     return set_error(FV_EINVAL, "fv_jpeg_decode_batch: bad arguments");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   std::vector<std::atomic<int32_t>> done(n);
+  std::vector<int64_t> used(n, 0);
   for (auto& d : done) d.store(1, std::memory_order_relaxed);  // 1 = pending
   std::atomic<int32_t> next{0};
   auto work = [&]() {
     for (int32_t i; (i = next.fetch_add(1)) < n;) {
-      const int rc = decode_one(data[i], lens[i], coef_host + coef_off[i], infos[i].coef_count, 2, nullptr);
+      const int64_t cap = infos[i].coef_count / 64 + infos[i].sparse_words;
+      const int rc = decode_one_sparse(data[i], lens[i], words_host + word_off[i], cap, &used[i]);
       done[i].store(rc, std::memory_order_release);
     }
   };
   const int nt = std::max(1, std::min<int>(threads, n));
   std::vector<std::thread> pool;
   for (int t = 0; t < nt; ++t) pool.emplace_back(work);
-  // in input order, as soon as an image's coefficients are ready: H2D + kernels
+  // in input order, as soon as an image's coefficients are ready: H2D of the
+  // words it used, then its kernels
   int first = FV_OK;
   for (int32_t i = 0; i < n; ++i) {
     int32_t rc;
@@ -758,14 +953,13 @@ int fv_jpeg_decode_batch(const uint8_t* const* data, const int64_t* lens, int32_
       if (first == FV_OK) first = rc;
       continue;
     }
-    const int64_t bytes = infos[i].coef_count * 2;
-    if (cudaMemcpyAsync(coef_dev + coef_off[i], coef_host + coef_off[i], bytes, cudaMemcpyHostToDevice, st) !=
+    if (cudaMemcpyAsync(words_dev + word_off[i], words_host + word_off[i], used[i] * 4, cudaMemcpyHostToDevice, st) !=
         cudaSuccess) {
       first = set_error(FV_ECUDA, "fv_jpeg_decode_batch: H2D: %s", cudaGetErrorString(cudaGetLastError()));
       status[i] = first;
       continue;
     }
-    rc = reconstruct(infos[i], coef_dev + coef_off[i], 2, planes + plane_off[i], dst[i], dst_pitch[i], st);
+    rc = reconstruct(infos[i], words_dev + word_off[i], 4, planes + plane_off[i], dst[i], dst_pitch[i], st);
     if (rc) {
       first = rc;
       status[i] = rc;

@@ -149,21 +149,21 @@ def decode_jpeg_batch(streams: Sequence, device=None, threads: int | None = None
     for i in range(n):
         if status[i]:
             jpeg_info(bufs[i])  # raises with the message
-    coef_off, plane_off = [], []
+    word_off, plane_off = [], []
     c = p = 0
     for f in infos:
-        coef_off.append(c)
+        word_off.append(c)
         plane_off.append(p)
-        c += (int(f.coef_count) + 63) // 64 * 64
+        c += (int(f.coef_count) // 64 + int(f.sparse_words) + 31) // 32 * 32
         p += (int(f.plane_bytes) + 255) // 256 * 256
     outs = [torch.empty((f.height, f.width, f.ncomp), dtype=torch.uint8, device=dev) for f in infos]
-    coef_dev = torch.empty(max(c, 1), dtype=torch.int16, device=dev)
+    words_dev = torch.empty(max(c, 1), dtype=torch.int32, device=dev)
     planes = torch.empty(max(p, 256), dtype=torch.uint8, device=dev)
     stream = torch.cuda.current_stream(dev)
     with _Staging.lock:
-        host = _Staging.get(2 * c)
+        host = _Staging.get(4 * c)
         rc = lib.fv_jpeg_decode_batch(
-            data, lens, n, infos, host.data_ptr(), (ctypes.c_int64 * n)(*coef_off), coef_dev.data_ptr(),
+            data, lens, n, infos, host.data_ptr(), (ctypes.c_int64 * n)(*word_off), words_dev.data_ptr(),
             planes.data_ptr(), (ctypes.c_int64 * n)(*plane_off), (ctypes.c_void_p * n)(*[o.data_ptr() for o in outs]),
             (ctypes.c_int64 * n)(*[o.stride(0) for o in outs]), status, threads, stream.cuda_stream)
         _Staging.event = torch.cuda.Event()
