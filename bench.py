@@ -238,18 +238,23 @@ def build_ops(n_scale, world, rank, dev, include):
         lo, hi = shard(n_total, world, rank)
         streams = jpeg_streams(lo, hi)
         dst = torch.empty((hi - lo, 3, 640, 640), dtype=torch.float32, device=dev)
+        frames = torch.empty((hi - lo, 1080, 1920, 3), dtype=torch.uint8, device=dev)
         from paper_2505_12425_b200 import io as fio
 
-        def step(st=streams, d=dst):
-            for k, img in enumerate(fio.decode_jpeg_batch(st, dev)):
-                fv.resize_normalize_chw(img, d[k], synth.MEAN, synth.STD)
+        def step(st=streams, d=dst, fr=frames):
+            fio.decode_jpeg_batch(st, dev, out=fr)  # the frames as one batch ...
+            fv.resize_normalize_chw(fr, d, synth.MEAN, synth.STD)  # ... preprocessed in one launch
 
         nbytes = sum(len(b) for b in streams) + dst.numel() * 4
+        gpu0 = fio.stats["gpu_entropy"]
+        step()
+        on_gpu = fio.stats["gpu_entropy"] - gpu0
         ops["f4_jpeg_decode_preprocess_64x1080p"] = dict(
             launches=[("jpeg_decode+preprocess (host entropy + GPU)", step, nbytes)],
             dst_px=(hi - lo) * 1920 * 1080, src_px=(hi - lo) * 1920 * 1080, images=n_total,
-            l2="host JPEG bytes (q90 4:2:0, ~200 KB each); bound by host entropy decoding",
+            l2="host JPEG bytes (q90 4:2:0, ~200 KB each)",
             extra={"mean_stream_kb": round(sum(len(b) for b in streams) / len(streams) / 1e3, 1),
+                   "entropy_decoding": f"GPU ({on_gpu}/{hi - lo} images; self-synchronising subsequences)",
                    "host_threads": host_cores(), "px_basis": "decoded 1920x1080 pixels",
                    "cpu_oracle_mps_1core": jpeg_cpu_oracle_mps()})
     return ops

@@ -45,6 +45,7 @@ extern "C" {
 #define FV_ECORRUPT (-3)     /* JPEG: malformed stream (errors.py CorruptStream) */
 #define FV_EUNSUPPORTED (-4) /* JPEG: valid but outside the subset (UnsupportedJpegFeature) */
 #define FV_ERANGE (-5)       /* JPEG: a coefficient does not fit the chosen width; retry wider */
+#define FV_EFALLBACK (-6)    /* JPEG, GPU entropy path: this image needs the host decoder (not an error) */
 
 /* ABI version (major*100 + minor). */
 int fv_version(void);
@@ -209,6 +210,19 @@ int fv_jpeg_decode_batch(const uint8_t* const* data, const int64_t* lens, int32_
                          uint32_t* words_host, const int64_t* word_off, uint32_t* words_dev, uint8_t* planes,
                          const int64_t* plane_off, uint8_t* const* dst, const int64_t* dst_pitch, int32_t* status,
                          int32_t threads, void* stream);
+
+/* GPU entropy decoding (batch): headers are parsed and the entropy-coded
+ * segments unstuffed on `threads` host threads; the Huffman decoding itself
+ * runs on the GPU (speculative, self-synchronising subsequence decoding: see
+ * csrc/fv_jpeg_gpu.cu), followed by the same reconstruction kernels. One
+ * stream synchronisation per call. status[i] = FV_OK when image i was decoded
+ * into dst[i]; FV_EFALLBACK when it needs the host decoder (stream outside
+ * the GPU path's coverage, or an anomaly on its decode path -- a corrupt
+ * stream); the caller decodes those with fv_jpeg_decode_batch, which also
+ * yields the exact error. Device scratch is stream-ordered (cudaMallocAsync). */
+int fv_jpeg_decode_batch_gpu(const uint8_t* const* data, const int64_t* lens, int32_t n, const FvJpegInfo* infos,
+                             uint8_t* planes, const int64_t* plane_off, uint8_t* const* dst, const int64_t* dst_pitch,
+                             int32_t* status, int32_t threads, void* stream);
 
 /* ---- tuning / introspection ---------------------------------------------
  * Resize kernel selection: 0 = auto (default: exact 2:1 / 1:2 fast paths,

@@ -70,9 +70,10 @@ SIGNATURES.update({
     "fv_jpeg_info_batch": ([_P, _P, _I32, _c.POINTER(FvJpegInfo), _P, _I32], _c.c_int),
     "fv_jpeg_decode_batch": ([_P, _P, _I32, _c.POINTER(FvJpegInfo), _P, _P, _P, _P, _P, _P, _P, _P, _I32, _P],
                              _c.c_int),
+    "fv_jpeg_decode_batch_gpu": ([_P, _P, _I32, _c.POINTER(FvJpegInfo), _P, _P, _P, _P, _P, _I32, _P], _c.c_int),
 })
 
-FV_ECORRUPT, FV_EUNSUPPORTED, FV_ERANGE = -3, -4, -5
+FV_ECORRUPT, FV_EUNSUPPORTED, FV_ERANGE, FV_EFALLBACK = -3, -4, -5, -6
 
 _lib = None
 _lock = threading.Lock()

@@ -1,0 +1,817 @@
+// fv_jpeg_gpu.cu -- GPU entropy decoding for the batched JPEG path
+// (decode -> preprocess).
+//
+// Huffman decoding is serial along a segment, but the code is
+// self-synchronising: a decoder started at an arbitrary bit soon falls into
+// step with the true decode. Each restart segment's (unstuffed) bits are cut
+// into kSubBits subsequences, one thread each:
+//   1. speculative pass: thread t decodes from the start of its subsequence
+//      with a guessed context (block slot 0, coefficient 0) and records the
+//      state at which it leaves the subsequence (bit position, slot, z);
+//   2. sync rounds: E_t = decode(E_{t-1}, subsequence t) until no state
+//      changes -- a fixed point is the true decode by induction (subsequence
+//      0 of a segment starts exact); unconverged images fall back;
+//   3. count pass: blocks started per subsequence -> exclusive scan -> the
+//      first block index of every subsequence;
+//   4. write pass: coefficients (DC as differences) into a zeroed dense int32
+//      buffer; DC prediction is a per-(segment, component) prefix sum.
+// Any anomaly on the true path (invalid code, DC size > 11, AC run past the
+// block, bits consumed past the segment) or a stream the GPU path does not
+// cover sends that image to the host decoder, which reproduces the
+// reference's exact error -- results are bit-identical either way.
+#include <atomic>
+#include <chrono>
+#include <cstdlib>
+#include <mutex>
+#include <thread>
+
+#include "fv_jpeg_host.cuh"
+
+namespace fv {
+namespace jpg {
+
+constexpr int kSubBits = 1024;
+constexpr int kMaxSlots = 12;
+constexpr int kSyncRounds = 6;    // rounds per chunk (one 4-byte readback per chunk)
+constexpr int kSyncChunks = 32;   // cap: images still changing after this fall back
+constexpr int kChain = 8;         // subsequences one thread may carry a changed state through per round
+
+__constant__ int kZigzagDev[64] = {0,  1,  8,  16, 9,  2,  3,  10, 17, 24, 32, 25, 18, 11, 4,  5,
+                                   12, 19, 26, 33, 40, 48, 41, 34, 27, 20, 13, 6,  7,  14, 21, 28,
+                                   35, 42, 49, 56, 57, 50, 43, 36, 29, 22, 15, 23, 30, 37, 44, 51,
+                                   58, 59, 52, 45, 38, 31, 39, 46, 53, 60, 61, 54, 47, 55, 62, 63};
+
+struct DevHuff {
+  int32_t fast[1 << 10];
+  int32_t maxcode[18];
+  int32_t mincode[17];
+  int32_t valptr[17];
+  uint8_t values[256];
+};
+
+struct DevImg {
+  DevHuff dc[3], ac[3];  // per scan entry
+  int8_t slot_e[kMaxSlots], slot_bx[kMaxSlots], slot_by[kMaxSlots];
+  int32_t nslots, mcus_x;
+  int32_t h[3], v[3], bw[3];
+  int64_t coef_offset[3];  // within the image's dense int32 region
+  int64_t coef_base;       // the region's start in the batch buffer
+};
+
+struct DevSeg {
+  int32_t img;
+  int32_t first_sub, nsub;
+  int64_t byte_off;     // unstuffed bytes in the batch stream buffer
+  int64_t bits;         // 8 * unstuffed length
+  int64_t first_block;  // decode-order index of the segment's first block in its image
+  int64_t nblocks;
+  int64_t first_mcu, nmcu;
+};
+
+__device__ __forceinline__ uint64_t pack_state(int64_t pos, int slot, int z) {
+  return ((uint64_t)pos << 16) | ((uint64_t)slot << 8) | (uint64_t)z;
+}
+__device__ __forceinline__ void unpack_state(uint64_t s, int64_t& pos, int& slot, int& z) {
+  pos = (int64_t)(s >> 16);
+  slot = (int)((s >> 8) & 0xFF);
+  z = (int)(s & 0xFF);
+}
+
+// MSB-first reader over one unstuffed segment (16-byte aligned, zero padded
+// to a multiple of 16 bytes in the batch buffer): refills 32 bits at a time
+// from aligned words; words past the segment read as zero.
+struct DBits {
+  const uint32_t* w;  // the segment's words
+  int64_t nw;         // words holding data (the rest of the segment's padding reads as zero too)
+  int64_t cur;        // next word to load
+  uint64_t acc;
+  int nb;
+  __device__ __forceinline__ void init(const uint8_t* seg, int64_t nbytes) {
+    w = reinterpret_cast<const uint32_t*>(seg);
+    nw = (nbytes + 3) >> 2;
+  }
+  __device__ __forceinline__ void fill() {
+    while (nb <= 32) {
+      const uint32_t x = cur < nw ? __byte_perm(__ldg(w + cur), 0, 0x0123) : 0u;
+      acc |= (uint64_t)x << (32 - nb);
+      nb += 32;
+      ++cur;
+    }
+  }
+  __device__ __forceinline__ void start(int64_t bit) {
+    cur = bit >> 5;
+    acc = 0;
+    nb = 0;
+    fill();
+    acc <<= (bit & 31);
+    nb -= (int)(bit & 31);
+    fill();
+  }
+  __device__ __forceinline__ uint32_t peek(int k) const { return (uint32_t)(acc >> (64 - k)); }
+  __device__ __forceinline__ void skip(int k) {
+    acc <<= k;
+    nb -= k;
+  }
+  __device__ __forceinline__ int64_t pos() const { return cur * 32 - nb; }
+};
+
+// one Huffman symbol; -1 = no code matches
+__device__ __forceinline__ int dsym(DBits& b, const DevHuff& t, int32_t f) {
+  if (f & (kFull | kSym)) {
+    b.skip(f & 31);
+    return (f >> 16) & 0xFF;
+  }
+  for (int len = 11; len <= 16; ++len) {
+    const int32_t code = (int32_t)b.peek(len);
+    if (t.maxcode[len] >= 0 && code <= t.maxcode[len]) {
+      b.skip(len);
+      return t.values[t.valptr[len] + code - t.mincode[len]];
+    }
+  }
+  return -1;
+}
+
+__device__ __forceinline__ int32_t dextend(uint32_t v, int size) {
+  return v < (1u << (size - 1)) ? (int32_t)v - (1 << size) + 1 : (int32_t)v;
+}
+
+enum { kModeSync = 0, kModeCount = 1, kModeWrite = 2 };
+
+// Decode symbols starting before `end_bit` (write mode on the segment's last
+// subsequence: until the segment's last block is complete). Anomalies on the
+// true path (write mode, blocks of the segment) set *bad; elsewhere the
+// decoder steps on deterministically (skip a bit / end the block).
+template <int MODE>
+__device__ uint64_t decode_run(const DevImg& im, DBits& b, int slot, int z, int64_t end_bit, bool last_sub,
+                               int64_t blk, const DevSeg& sg, int32_t* coef, int* nstart, int* bad) {
+  const int64_t limit = sg.first_block + sg.nblocks;
+  for (;;) {
+    const int64_t pos = b.pos();
+    if (MODE == kModeWrite && last_sub) {
+      if (blk >= limit && z == 0) break;              // the segment's blocks are done
+      if (pos > sg.bits + 64 * 16) { *bad = 1; break; }  // decoding deep into padding: corrupt
+    } else if (pos >= end_bit) {
+      break;
+    }
+    b.fill();
+    const int e = im.slot_e[slot];
+    int32_t* dst = nullptr;
+    if (MODE == kModeWrite) {
+      const int64_t cb = z == 0 ? blk : blk - 1;  // block this symbol belongs to
+      if (cb >= sg.first_block && cb < limit) {
+        const int64_t mcu = cb / im.nslots;
+        const int s = (int)(cb - mcu * im.nslots);
+        const int ee = im.slot_e[s];
+        const int64_t my = mcu / im.mcus_x, mx = mcu - my * im.mcus_x;
+        const int64_t r = (my * im.v[ee] + im.slot_by[s]) * im.bw[ee] + mx * im.h[ee] + im.slot_bx[s];
+        dst = coef + im.coef_base + im.coef_offset[ee] + 64 * r;
+      }
+    }
+    if (z == 0) {  // DC of a new block
+      if (MODE == kModeCount) ++*nstart;
+      if (MODE == kModeWrite) ++blk;
+      const DevHuff& t = im.dc[e];
+      const int32_t f = t.fast[b.peek(10)];
+      int32_t diff;
+      if (f & kFull) {
+        b.skip(f & 31);
+        diff = f >> 16;
+      } else {
+        const int size = dsym(b, t, f);
+        if (size < 0 || size > 11) {
+          if (MODE == kModeWrite && dst) *bad = 1;
+          if (size < 0) b.skip(1);
+          diff = 0;
+        } else if (size) {
+          diff = dextend(b.peek(size), size);
+          b.skip(size);
+        } else {
+          diff = 0;
+        }
+      }
+      if (MODE == kModeWrite && dst) dst[0] = diff;
+      z = 1;
+    } else {
+      const DevHuff& t = im.ac[e];
+      const int32_t f = t.fast[b.peek(10)];
+      if (f & kFull) {
+        b.skip(f & 31);
+        z += (f >> 8) & 15;
+        if (z > 63) {
+          if (MODE == kModeWrite && dst) *bad = 1;
+          z = 64;
+        } else {
+          if (MODE == kModeWrite && dst) dst[kZigzagDev[z]] = f >> 16;
+          ++z;
+        }
+      } else {
+        const int rs = dsym(b, t, f);
+        if (rs < 0) {
+          if (MODE == kModeWrite && dst) *bad = 1;
+          b.skip(1);
+          z = 64;
+        } else {
+          const int sz = rs & 15;
+          if (sz == 0) {
+            z = rs == 0xF0 ? z + 16 : 64;
+          } else {
+            z += rs >> 4;
+            if (z > 63) {
+              if (MODE == kModeWrite && dst) *bad = 1;
+              z = 64;
+            } else {
+              const int32_t v = dextend(b.peek(sz), sz);
+              b.skip(sz);
+              if (MODE == kModeWrite && dst) dst[kZigzagDev[z]] = v;
+              ++z;
+            }
+          }
+        }
+      }
+    }
+    if (z >= 64) {  // block complete
+      z = 0;
+      slot = slot + 1 == im.nslots ? 0 : slot + 1;
+      if (MODE == kModeWrite && blk == limit && b.pos() > sg.bits) *bad = 1;  // consumed padding
+    }
+  }
+  return pack_state(b.pos(), slot, z);
+}
+
+
+// ---------------------------------------------------------------------------
+// passes (one thread per subsequence)
+// ---------------------------------------------------------------------------
+
+struct Pass {
+  const DevImg* imgs;
+  const DevSeg* segs;
+  const int32_t* sub_seg;
+  const uint8_t* stream;
+  int64_t nsub;
+};
+
+__device__ __forceinline__ void sub_range(const Pass& P, int64_t t, const DevSeg*& sg, int64_t& local, int64_t& start,
+                                          int64_t& end) {
+  sg = &P.segs[P.sub_seg[t]];
+  local = t - sg->first_sub;
+  start = local * kSubBits;
+  end = min(start + (int64_t)kSubBits, sg->bits);
+}
+
+__global__ void __launch_bounds__(128) k_spec(const __grid_constant__ Pass P, uint64_t* E) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= P.nsub) return;
+  const DevSeg* sg;
+  int64_t local, start, end;
+  sub_range(P, t, sg, local, start, end);
+  DBits b;
+  b.init(P.stream + sg->byte_off, sg->bits >> 3);
+  b.start(start);
+  E[t] = decode_run<kModeSync>(P.imgs[sg->img], b, 0, 0, end, false, 0, *sg, nullptr, nullptr, nullptr);
+}
+
+// One propagation round over a work queue: for each queued subsequence t,
+// E[t] = decode(E[t-1]). E is updated in place (64-bit stores are atomic, and
+// reading a predecessor's old or new state is a valid iteration step). The
+// invariant that makes the final state the fixed point: EVERY change of E[t]
+// queues t+1 for the next round (deduplicated by a per-subsequence round
+// mark), so t+1 is re-derived from E[t]'s final value; rounds run until one
+// changes nothing. As an accelerator, a thread that changed E[t] also carries
+// the new state on through up to kChain following subsequences itself (a
+// desynchronised stretch would otherwise advance one subsequence per round).
+// all_subs: the first round takes every subsequence (implicit queue).
+__device__ __forceinline__ void enqueue(int32_t* qout, int* nout, int* mark, int64_t t, int round) {
+  if (atomicExch(&mark[t], round) != round) qout[atomicAdd(nout, 1)] = (int32_t)t;
+}
+
+__global__ void __launch_bounds__(128) k_round(const __grid_constant__ Pass P, uint64_t* E, const int32_t* qin,
+                                               const int* nin, int32_t* qout, int* nout, int* mark, int round,
+                                               int all_subs) {
+  const int64_t n = all_subs ? P.nsub : *nin;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    int64_t t = all_subs ? i : qin[i];
+    const DevSeg* sg;
+    int64_t local, start, end;
+    sub_range(P, t, sg, local, start, end);
+    if (local == 0) continue;
+    uint64_t in = E[t - 1];
+    for (int step = 0;; ++step) {
+      int64_t pos;
+      int slot, z;
+      unpack_state(in, pos, slot, z);
+      DBits b;
+      b.init(P.stream + sg->byte_off, sg->bits >> 3);
+      b.start(pos);
+      const uint64_t e =
+          decode_run<kModeSync>(P.imgs[sg->img], b, slot, z, end, false, 0, *sg, nullptr, nullptr, nullptr);
+      if (e == E[t]) break;
+      E[t] = e;
+      if (local + 1 >= sg->nsub) break;
+      enqueue(qout, nout, mark, t + 1, round);  // re-derive t+1 next round, whatever happens below
+      if (step + 1 == kChain) break;
+      in = e;
+      ++t;
+      ++local;
+      start = local * kSubBits;
+      end = min(start + (int64_t)kSubBits, sg->bits);
+    }
+  }
+}
+
+// After the rounds: any subsequence whose state still disagrees with its
+// predecessor's decode marks its image (not converged -> host decoder).
+__global__ void __launch_bounds__(128) k_verify(const __grid_constant__ Pass P, const uint64_t* E, const int32_t* q,
+                                                const int* nq, int* img_bad) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < *nq; i += (int64_t)gridDim.x * blockDim.x)
+    img_bad[P.segs[P.sub_seg[q[i]]].img] = 1;
+}
+
+__device__ __forceinline__ void entry_state(const Pass& P, const uint64_t* E, int64_t t, int64_t local, int64_t start,
+                                            int64_t& pos, int& slot, int& z) {
+  if (local == 0) {
+    pos = start;
+    slot = 0;
+    z = 0;
+  } else {
+    unpack_state(E[t - 1], pos, slot, z);
+  }
+}
+
+__global__ void __launch_bounds__(128) k_count(const __grid_constant__ Pass P, const uint64_t* E, int32_t* cnt) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= P.nsub) return;
+  const DevSeg* sg;
+  int64_t local, start, end, pos;
+  int slot, z, n = 0;
+  sub_range(P, t, sg, local, start, end);
+  entry_state(P, E, t, local, start, pos, slot, z);
+  DBits b;
+  b.init(P.stream + sg->byte_off, sg->bits >> 3);
+  b.start(pos);
+  decode_run<kModeCount>(P.imgs[sg->img], b, slot, z, end, false, 0, *sg, nullptr, &n, nullptr);
+  cnt[t] = n;
+}
+
+// exclusive scan of the block-start counts of each segment's subsequences
+__global__ void __launch_bounds__(256) k_scan(const DevSeg* segs, int32_t nseg, const int32_t* cnt, int64_t* base) {
+  __shared__ int64_t warp_sum[8];
+  const int sgi = blockIdx.x;
+  if (sgi >= nseg) return;
+  const DevSeg& sg = segs[sgi];
+  int64_t carry = sg.first_block;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  for (int64_t c0 = 0; c0 < sg.nsub; c0 += 256) {
+    const int64_t i = c0 + threadIdx.x;
+    const int64_t v = i < sg.nsub ? cnt[sg.first_sub + i] : 0;
+    int64_t x = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int64_t y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x += y;
+    }
+    if (lane == 31) warp_sum[w] = x;
+    __syncthreads();
+    int64_t pre = 0, tot = 0;
+    for (int k = 0; k < 8; ++k) {
+      if (k < w) pre += warp_sum[k];
+      tot += warp_sum[k];
+    }
+    if (i < sg.nsub) base[sg.first_sub + i] = carry + pre + x - v;
+    carry += tot;
+    __syncthreads();
+  }
+}
+
+__global__ void __launch_bounds__(128) k_write(const __grid_constant__ Pass P, const uint64_t* E, const int64_t* base,
+                                               int32_t* coef, int* img_bad) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= P.nsub) return;
+  const DevSeg* sg;
+  int64_t local, start, end, pos;
+  int slot, z, bad = 0;
+  sub_range(P, t, sg, local, start, end);
+  entry_state(P, E, t, local, start, pos, slot, z);
+  DBits b;
+  b.init(P.stream + sg->byte_off, sg->bits >> 3);
+  b.start(pos);
+  decode_run<kModeWrite>(P.imgs[sg->img], b, slot, z, end, local == sg->nsub - 1, base[t], *sg, coef, nullptr, &bad);
+  if (bad) img_bad[sg->img] = 1;
+}
+
+// DC prediction: per (segment, scan entry), a prefix sum of the DC
+// differences over the component's blocks in decode order (MCU, then by, bx)
+__global__ void __launch_bounds__(256) k_dcpred(const DevImg* imgs, const DevSeg* segs, int32_t* coef) {
+  __shared__ int32_t warp_sum[8];
+  const DevSeg& sg = segs[blockIdx.x];
+  const DevImg& im = imgs[sg.img];
+  const int e = blockIdx.y;
+  if (e >= 3 || im.h[e] == 0) return;
+  const int hv = im.h[e] * im.v[e];
+  const int64_t nblk = sg.nmcu * hv;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  int32_t carry = 0;
+  for (int64_t c0 = 0; c0 < nblk; c0 += 256) {
+    const int64_t j = c0 + threadIdx.x;
+    int32_t* dc = nullptr;
+    int32_t v = 0;
+    if (j < nblk) {
+      const int64_t mcu = sg.first_mcu + j / hv;
+      const int k = (int)(j % hv), by = k / im.h[e], bx = k - by * im.h[e];
+      const int64_t my = mcu / im.mcus_x, mx = mcu - my * im.mcus_x;
+      dc = coef + im.coef_base + im.coef_offset[e] + 64 * ((my * im.v[e] + by) * im.bw[e] + mx * im.h[e] + bx);
+      v = *dc;
+    }
+    int32_t x = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int32_t y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x += y;
+    }
+    if (lane == 31) warp_sum[w] = x;
+    __syncthreads();
+    int32_t pre = 0, tot = 0;
+    for (int k = 0; k < 8; ++k) {
+      if (k < w) pre += warp_sum[k];
+      tot += warp_sum[k];
+    }
+    if (dc) *dc = carry + pre + x;
+    carry += tot;
+    __syncthreads();
+  }
+}
+
+// ---------------------------------------------------------------------------
+// host planning
+// ---------------------------------------------------------------------------
+
+inline void to_dev_huff(const Huff& h, DevHuff& d) {
+  memcpy(d.fast, h.fast, sizeof(d.fast));
+  for (int l = 0; l < 17; ++l) {
+    d.maxcode[l] = h.maxcode[l];
+    d.mincode[l] = h.mincode[l];
+    d.valptr[l] = h.valptr[l];
+  }
+  d.maxcode[17] = -1;
+  memcpy(d.values, h.values, 256);
+}
+
+struct Plan {
+  std::unique_ptr<Stream> s;
+  int rc = FV_OK;
+  bool gpu = false;
+  int64_t nseg = 0, nsub = 0, bytes = 0, coefs = 0;
+};
+
+// Can the GPU path decode this stream exactly? (else: the host decoder)
+inline bool gpu_eligible(const Stream& s, const FvJpegInfo& f) {
+  int seen = 0;
+  for (int e = 0; e < s.nscan; ++e) {
+    const int k = s.scan_comp[e];
+    if (seen & (1 << k)) return false;  // a component named twice by the scan
+    seen |= 1 << k;
+    const Comp& c = s.sof[k];
+    int nv = 0;
+    for (int l = 1; l <= 16; ++l) nv += s.dc[c.td].maxcode[l] >= 0 ? s.dc[c.td].maxcode[l] - s.dc[c.td].mincode[l] + 1 : 0;
+    if (nv > 256) return false;
+    nv = 0;
+    for (int l = 1; l <= 16; ++l) nv += s.ac[c.ta].maxcode[l] >= 0 ? s.ac[c.ta].maxcode[l] - s.ac[c.ta].mincode[l] + 1 : 0;
+    if (nv > 256) return false;
+    // DC values of a segment stay within int32 (|diff| <= 2047 per block)
+    const int64_t per_seg = (int64_t)(s.dri ? s.dri : (int64_t)s.mcus_x * s.mcus_y) * c.h * c.v;
+    if (per_seg * 2047 >= (1ll << 31)) return false;
+  }
+  int64_t per_mcu = 0;
+  for (int e = 0; e < s.nscan; ++e) per_mcu += s.sof[s.scan_comp[e]].h * s.sof[s.scan_comp[e]].v;
+  if (per_mcu > kMaxSlots) return false;
+  return f.coef_count > 0;
+}
+
+// Pinned host staging for the uploads, kept across calls (one caller at a
+// time: the call synchronises its stream before returning, so the buffer is
+// free again when the next call takes the lock).
+struct PinnedStage {
+  std::mutex lock;
+  uint8_t* p = nullptr;
+  size_t cap = 0;
+  uint8_t* get(size_t bytes) {
+    if (bytes > cap) {
+      if (p) cudaFreeHost(p);
+      cap = std::max(bytes, cap * 2);
+      if (cudaHostAlloc(reinterpret_cast<void**>(&p), cap, cudaHostAllocDefault) != cudaSuccess) {
+        p = nullptr;
+        cap = 0;
+      }
+    }
+    return p;
+  }
+};
+inline PinnedStage& pinned_stage() {
+  static PinnedStage s;
+  return s;
+}
+
+// The scratch comes from the device's default stream-ordered pool; by
+// default the pool returns freed memory to the OS at every synchronisation,
+// which would re-map ~1 GB per batch. Keep it (once per device).
+inline void keep_pool_memory() {
+  static std::mutex m;
+  static unsigned long long done[2] = {0, 0};
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 128) return;
+  std::lock_guard<std::mutex> g(m);
+  if (done[dev >> 6] & (1ull << (dev & 63))) return;
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+    uint64_t keep = UINT64_MAX;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+  }
+  done[dev >> 6] |= 1ull << (dev & 63);
+}
+
+template <typename T>
+struct DevBuf {
+  T* p = nullptr;
+  size_t n = 0;
+  int alloc(size_t count, cudaStream_t st) {
+    n = count;
+    return cudaMallocAsync(reinterpret_cast<void**>(&p), std::max<size_t>(count, 1) * sizeof(T), st) == cudaSuccess
+               ? FV_OK
+               : set_error(FV_ECUDA, "fv_jpeg_decode_batch_gpu: device allocation of %zu bytes", count * sizeof(T));
+  }
+  void release(cudaStream_t st) {
+    if (p) cudaFreeAsync(p, st);
+    p = nullptr;
+  }
+};
+
+}  // namespace jpg
+}  // namespace fv
+
+using namespace fv;
+using namespace fv::jpg;
+
+namespace {
+struct PhaseTimer {  // FV_JPEG_TIMING=1: host phase times to stderr
+  bool on = getenv("FV_JPEG_TIMING") != nullptr;
+  std::chrono::steady_clock::time_point t0 = std::chrono::steady_clock::now();
+  void mark(const char* what) {
+    if (!on) return;
+    const auto t = std::chrono::steady_clock::now();
+    fprintf(stderr, "[fv_jpeg_gpu] %-28s %8.3f ms\n", what, std::chrono::duration<double, std::milli>(t - t0).count());
+    t0 = t;
+  }
+};
+}  // namespace
+
+extern "C" {
+
+int fv_jpeg_decode_batch_gpu(const uint8_t* const* data, const int64_t* lens, int32_t n, const FvJpegInfo* infos,
+                             uint8_t* planes, const int64_t* plane_off, uint8_t* const* dst, const int64_t* dst_pitch,
+                             int32_t* status, int32_t threads, void* stream) {
+  if (n < 0 || (n > 0 && (!data || !lens || !infos || !planes || !plane_off || !dst || !dst_pitch || !status)))
+    return set_error(FV_EINVAL, "fv_jpeg_decode_batch_gpu: bad arguments");
+  if (n == 0) return FV_OK;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  keep_pool_memory();
+  PhaseTimer timer;
+  const int nt = std::max(1, std::min<int>(threads, n));
+  auto parallel = [&](auto&& fn) {
+    std::atomic<int32_t> next{0};
+    auto work = [&]() {
+      for (int32_t i; (i = next.fetch_add(1)) < n;) fn(i);
+    };
+    std::vector<std::thread> pool;
+    for (int t = 1; t < nt; ++t) pool.emplace_back(work);
+    work();
+    for (auto& t : pool) t.join();
+  };
+  // 1. parse, eligibility, sizes
+  std::vector<Plan> plan(n);
+  parallel([&](int32_t i) {
+    Plan& p = plan[i];
+    p.s.reset(new Stream());
+    p.rc = parse(data[i], lens[i], *p.s);
+    if (p.rc) return;
+    FvJpegInfo f;
+    fill_info(*p.s, f);
+    p.gpu = gpu_eligible(*p.s, f);
+    if (!p.gpu) return;
+    const Stream& s = *p.s;
+    const int64_t total = (int64_t)s.mcus_x * s.mcus_y;
+    p.nseg = s.dri ? (total + s.dri - 1) / s.dri : 1;
+    for (int64_t k = 0; k < p.nseg; ++k) {
+      p.bytes += (s.seg_len[k] + 15) / 16 * 16;
+      p.nsub += std::max<int64_t>(1, (8 * s.seg_len[k] + kSubBits - 1) / kSubBits);
+    }
+    p.coefs = f.coef_count;
+  });
+  timer.mark("parse + plan");
+  // 2. offsets
+  std::vector<int64_t> seg_off(n), sub_off(n), byte_off(n), coef_off(n), img_idx(n, -1);
+  int64_t nseg = 0, nsub = 0, nbytes = 0, ncoef = 0;
+  int32_t nimg = 0;
+  for (int32_t i = 0; i < n; ++i) {
+    status[i] = FV_EFALLBACK;
+    if (!plan[i].gpu) continue;
+    img_idx[i] = nimg++;
+    seg_off[i] = nseg;
+    sub_off[i] = nsub;
+    byte_off[i] = nbytes;
+    coef_off[i] = ncoef;
+    nseg += plan[i].nseg;
+    nsub += plan[i].nsub;
+    nbytes += (plan[i].bytes + 15) / 16 * 16;
+    ncoef += plan[i].coefs;
+  }
+  if (nimg == 0) return FV_OK;
+  // 3. host staging: images, segments, subsequence -> segment, unstuffed bytes
+  PinnedStage& stage = pinned_stage();
+  std::lock_guard<std::mutex> stage_guard(stage.lock);
+  const size_t o_img = 0, o_seg = o_img + ((nimg * sizeof(DevImg) + 255) & ~size_t(255));
+  const size_t o_sub = o_seg + ((nseg * sizeof(DevSeg) + 255) & ~size_t(255));
+  const size_t o_bytes = o_sub + ((nsub * sizeof(int32_t) + 255) & ~size_t(255));
+  const size_t stage_bytes = o_bytes + nbytes + 16;
+  uint8_t* sbase = stage.get(stage_bytes);
+  if (!sbase) return set_error(FV_ECUDA, "fv_jpeg_decode_batch_gpu: pinned staging of %zu bytes", stage_bytes);
+  DevImg* himg = reinterpret_cast<DevImg*>(sbase + o_img);
+  DevSeg* hseg = reinterpret_cast<DevSeg*>(sbase + o_seg);
+  int32_t* hsub = reinterpret_cast<int32_t*>(sbase + o_sub);
+  uint8_t* hbytes = sbase + o_bytes;
+  parallel([&](int32_t i) {
+    if (!plan[i].gpu) return;
+    const Stream& s = *plan[i].s;
+    FvJpegInfo f;
+    fill_info(s, f);
+    DevImg& d = himg[img_idx[i]];
+    memset(&d, 0, sizeof(d));
+    int slot = 0;
+    for (int e = 0; e < s.nscan; ++e) {
+      const Comp& c = s.sof[s.scan_comp[e]];
+      to_dev_huff(s.dc[c.td], d.dc[e]);
+      to_dev_huff(s.ac[c.ta], d.ac[e]);
+      d.h[e] = c.h;
+      d.v[e] = c.v;
+      d.bw[e] = f.bw[e];
+      d.coef_offset[e] = f.coef_offset[e];
+      for (int by = 0; by < c.v; ++by)
+        for (int bx = 0; bx < c.h; ++bx, ++slot) {
+          d.slot_e[slot] = (int8_t)e;
+          d.slot_bx[slot] = (int8_t)bx;
+          d.slot_by[slot] = (int8_t)by;
+        }
+    }
+    d.nslots = slot;
+    d.mcus_x = s.mcus_x;
+    d.coef_base = coef_off[i];
+    const int64_t total = (int64_t)s.mcus_x * s.mcus_y;
+    int64_t bo = byte_off[i], so = sub_off[i];
+    for (int64_t k = 0; k < plan[i].nseg; ++k) {
+      DevSeg& g = hseg[seg_off[i] + k];
+      g.img = (int32_t)img_idx[i];
+      g.byte_off = bo;
+      g.bits = 8 * s.seg_len[k];
+      g.first_mcu = s.dri ? k * s.dri : 0;
+      g.nmcu = s.dri ? std::min<int64_t>(s.dri, total - k * s.dri) : total;
+      g.first_block = g.first_mcu * slot;
+      g.nblocks = g.nmcu * slot;
+      g.first_sub = (int32_t)so;
+      g.nsub = (int32_t)std::max<int64_t>(1, (g.bits + kSubBits - 1) / kSubBits);
+      for (int32_t q = 0; q < g.nsub; ++q) hsub[so + q] = (int32_t)(seg_off[i] + k);
+      so += g.nsub;
+      // unstuff the segment: copy runs between 0xFF bytes, FF 00 -> FF, drop fill FFs
+      uint8_t* out = hbytes + bo;
+      for (int64_t r = s.seg_raw[k]; r < s.seg_end[k];) {
+        const uint8_t* f = static_cast<const uint8_t*>(memchr(s.data + r, 0xFF, (size_t)(s.seg_end[k] - r)));
+        const int64_t run = f ? (f - (s.data + r)) : (s.seg_end[k] - r);
+        memcpy(out, s.data + r, (size_t)run);
+        out += run;
+        r += run;
+        if (r >= s.seg_end[k]) break;
+        if (s.data[r + 1] == 0x00) {
+          *out++ = 0xFF;
+          r += 2;
+        } else {
+          ++r;  // fill byte
+        }
+      }
+      memset(out, 0, (size_t)((s.seg_len[k] + 15) / 16 * 16 - s.seg_len[k]));  // zero padding
+      bo += (s.seg_len[k] + 15) / 16 * 16;  // 16-byte aligned, zero padded (DBits reads whole words)
+    }
+  });
+  timer.mark("unstuff + tables");
+  // 4. device buffers and passes
+  DevBuf<DevImg> dimg;
+  DevBuf<DevSeg> dseg;
+  DevBuf<int32_t> dsub, dcnt, dcoef, dflags;
+  DevBuf<uint8_t> dbytes;
+  DevBuf<uint64_t> dE0;
+  DevBuf<int32_t> dq0, dq1, dmark;
+  DevBuf<int64_t> dbase;
+  int rc = FV_OK;
+  rc = rc ? rc : dimg.alloc(nimg, st);
+  rc = rc ? rc : dseg.alloc(nseg, st);
+  rc = rc ? rc : dsub.alloc(nsub, st);
+  rc = rc ? rc : dcnt.alloc(nsub, st);
+  rc = rc ? rc : dbytes.alloc(nbytes + 16, st);
+  rc = rc ? rc : dE0.alloc(nsub, st);
+  rc = rc ? rc : dq0.alloc(nsub, st);
+  rc = rc ? rc : dq1.alloc(nsub, st);
+  rc = rc ? rc : dmark.alloc(nsub, st);
+  rc = rc ? rc : dbase.alloc(nsub, st);
+  rc = rc ? rc : dcoef.alloc(ncoef, st);
+  const int nrounds = kSyncRounds * kSyncChunks;
+  rc = rc ? rc : dflags.alloc(nimg + nrounds + 2, st);
+  std::vector<int32_t> hflags(nimg + nrounds + 2, 0);
+  if (!rc) {
+    // hflags: img_bad[nimg] = 0, then the per-round queue lengths (all 0)
+    cudaMemcpyAsync(dimg.p, himg, nimg * sizeof(DevImg), cudaMemcpyHostToDevice, st);
+    cudaMemcpyAsync(dseg.p, hseg, nseg * sizeof(DevSeg), cudaMemcpyHostToDevice, st);
+    cudaMemcpyAsync(dsub.p, hsub, nsub * sizeof(int32_t), cudaMemcpyHostToDevice, st);
+    cudaMemcpyAsync(dbytes.p, hbytes, nbytes, cudaMemcpyHostToDevice, st);
+    cudaMemcpyAsync(dflags.p, hflags.data(), hflags.size() * sizeof(int32_t), cudaMemcpyHostToDevice, st);
+    cudaMemsetAsync(dcoef.p, 0, ncoef * sizeof(int32_t), st);
+    cudaMemsetAsync(dmark.p, 0, nsub * sizeof(int32_t), st);
+    Pass P{dimg.p, dseg.p, dsub.p, dbytes.p, nsub};
+    const unsigned grid = (unsigned)((nsub + 127) / 128);
+    int* img_bad = dflags.p;
+    int* changed = dflags.p + nimg;  // changed[r], r = 0 .. kSyncRounds
+    k_spec<<<grid, 128, 0, st>>>(P, dE0.p);
+    count_launch();
+    uint64_t* Ein = dE0.p;
+    // rounds: the first over every subsequence, then over the queue of those
+    // whose predecessor changed; after a chunk of rounds, one 4-byte readback
+    // of the queue length decides whether another chunk is needed
+    int32_t* qa = dq0.p;
+    int32_t* qb = dq1.p;
+    int* cnt = changed;  // cnt[r]: queue length produced by round r
+    const unsigned qgrid = (unsigned)std::min<int64_t>((nsub + 127) / 128, 148 * 8);
+    int r = 0;
+    for (int chunk = 0; chunk < kSyncChunks && !rc; ++chunk) {
+      for (int k = 0; k < kSyncRounds; ++k, ++r) {
+        k_round<<<r == 0 ? grid : qgrid, 128, 0, st>>>(P, Ein, qa, cnt + r, qb, cnt + r + 1, dmark.p, r + 1, r == 0);
+        count_launch();
+        std::swap(qa, qb);
+      }
+      int32_t last = 0;
+      cudaMemcpyAsync(&last, cnt + r, sizeof(int32_t), cudaMemcpyDeviceToHost, st);
+      if (cudaStreamSynchronize(st) != cudaSuccess) {
+        rc = set_error(FV_ECUDA, "fv_jpeg_decode_batch_gpu: %s", cudaGetErrorString(cudaGetLastError()));
+        break;
+      }
+      if (last == 0) break;
+      if (chunk + 1 == kSyncChunks) {  // still changing: those images go to the host decoder
+        k_verify<<<qgrid, 128, 0, st>>>(P, Ein, qa, cnt + r, img_bad);
+        count_launch();
+      }
+    }
+    timer.mark("speculative + sync rounds");
+    if (timer.on) {
+      std::vector<int32_t> ch(r + 1);
+      cudaMemcpy(ch.data(), changed, (r + 1) * sizeof(int32_t), cudaMemcpyDeviceToHost);
+      fprintf(stderr, "[fv_jpeg_gpu] %lld subsequences, changed per round:", (long long)nsub);
+      for (int q = 1; q <= r; ++q) fprintf(stderr, " %d", ch[q]);
+      fprintf(stderr, "\n");
+    }
+    k_count<<<grid, 128, 0, st>>>(P, Ein, dcnt.p);
+    k_scan<<<(unsigned)nseg, 256, 0, st>>>(dseg.p, (int32_t)nseg, dcnt.p, dbase.p);
+    k_write<<<grid, 128, 0, st>>>(P, Ein, dbase.p, dcoef.p, img_bad);
+    k_dcpred<<<dim3((unsigned)nseg, 3), 256, 0, st>>>(dimg.p, dseg.p, dcoef.p);
+    rc = check_launch("fv_jpeg_decode_batch_gpu passes");
+    count_launch();
+    count_launch();
+    count_launch();
+  }
+  timer.mark("count + write + dc");
+  if (!rc) {
+    // which images decoded cleanly (a second sync)
+    cudaMemcpyAsync(hflags.data(), dflags.p, nimg * sizeof(int32_t), cudaMemcpyDeviceToHost, st);
+    if (cudaStreamSynchronize(st) != cudaSuccess)
+      rc = set_error(FV_ECUDA, "fv_jpeg_decode_batch_gpu: %s", cudaGetErrorString(cudaGetLastError()));
+  }
+  if (!rc) {
+    for (int32_t i = 0; i < n && !rc; ++i) {
+      if (!plan[i].gpu || hflags[img_idx[i]]) continue;
+      FvJpegInfo f;
+      fill_info(*plan[i].s, f);
+      rc = reconstruct(f, dcoef.p + coef_off[i], 4, planes + plane_off[i], dst[i], dst_pitch[i], st);
+      if (!rc) status[i] = FV_OK;
+    }
+  }
+  timer.mark("flags + reconstruct launch");
+  dimg.release(st);
+  dseg.release(st);
+  dsub.release(st);
+  dcnt.release(st);
+  dbytes.release(st);
+  dE0.release(st);
+  dq0.release(st);
+  dq1.release(st);
+  dmark.release(st);
+  dbase.release(st);
+  dcoef.release(st);
+  dflags.release(st);
+  return rc;
+}
+
+}  // extern "C"

@@ -23,9 +23,13 @@ from typing import Sequence
 import torch
 
 from . import _native
-from .errors import CorruptStream, NativeError, UnsupportedDevice, UnsupportedJpegFeature
+from .errors import CorruptStream, NativeError, ShapeMismatch, UnsupportedDevice, UnsupportedJpegFeature
 
 _ERRORS = {_native.FV_ECORRUPT: CorruptStream, _native.FV_EUNSUPPORTED: UnsupportedJpegFeature}
+
+# images decoded per entropy path by decode_jpeg_batch (introspection for the
+# tests and the bench: the GPU path must be the one that runs)
+stats = {"gpu_entropy": 0, "host_entropy": 0}
 
 
 def _raise(rc: int, what: str) -> None:
@@ -127,13 +131,56 @@ class _Staging:
         return cls.buf
 
 
-def decode_jpeg_batch(streams: Sequence, device=None, threads: int | None = None) -> list:
-    """Decode many streams with the native batch runtime
-    (`fv_jpeg_info_batch` / `fv_jpeg_decode_batch`): headers and entropy
-    decoding on `threads` host threads (default: the usable cores); each
-    image's H2D copy and kernels are issued on the current stream as soon as
-    its coefficients are ready, in input order. Raises the first failing
-    stream's error (input order), as a loop of `decode_jpeg` calls would."""
+def _host_batch(bufs, infos, outs, planes, plane_off, threads, stream, dev):
+    """Host entropy decoding (native batch runtime) of `bufs` into `outs`:
+    raises the first failing stream's error, in order."""
+    n = len(bufs)
+    lib = _native.lib()
+    data = (ctypes.c_char_p * n)(*bufs)
+    lens = (ctypes.c_int64 * n)(*[len(b) for b in bufs])
+    info_arr = (_native.FvJpegInfo * n)(*infos)
+    status = (ctypes.c_int32 * n)()
+    word_off = []
+    c = 0
+    for f in infos:
+        word_off.append(c)
+        c += (int(f.coef_count) // 64 + int(f.sparse_words) + 31) // 32 * 32
+    words_dev = torch.empty(max(c, 1), dtype=torch.int32, device=dev)
+    with _Staging.lock:
+        host = _Staging.get(4 * c)
+        rc = lib.fv_jpeg_decode_batch(
+            data, lens, n, info_arr, host.data_ptr(), (ctypes.c_int64 * n)(*word_off), words_dev.data_ptr(),
+            planes.data_ptr(), (ctypes.c_int64 * n)(*plane_off), (ctypes.c_void_p * n)(*[o.data_ptr() for o in outs]),
+            (ctypes.c_int64 * n)(*[o.stride(0) for o in outs]), status, threads, stream.cuda_stream)
+        _Staging.event = torch.cuda.Event()
+        _Staging.event.record(stream)
+    if rc:
+        i = next(k for k in range(n) if status[k])
+        if status[i] != _native.FV_ERANGE:
+            decode_jpeg(bufs[i], dev)  # raises with the message
+            _raise(status[i], "fv_jpeg_decode_batch")
+        # a DC coefficient beyond int16: this image with int64 coefficients, then the rest
+        outs[i].copy_(decode_jpeg(bufs[i], dev))
+        if i + 1 < n:
+            _host_batch(bufs[i + 1:], infos[i + 1:], outs[i + 1:], planes, plane_off[i + 1:], threads, stream, dev)
+
+
+def decode_jpeg_batch(streams: Sequence, device=None, threads: int | None = None, entropy: str = "gpu",
+                      out: torch.Tensor | None = None) -> list:
+    """Decode many streams. entropy="gpu" (default): headers parsed and
+    segments unstuffed on `threads` host threads, Huffman decoding on the GPU
+    (`fv_jpeg_decode_batch_gpu`); streams outside its coverage or with a
+    corrupt entropy segment go through the host decoder. entropy="host": the
+    native host batch runtime (threaded entropy decoding, each image's H2D +
+    kernels issued as soon as it is ready). Either way the output is
+    bit-identical to `decode_jpeg`, and the first failing stream's error (in
+    input order) is raised, as a loop of `decode_jpeg` calls would.
+    out: optional (N, H, W, C) u8 CUDA tensor receiving image i in out[i]
+    (every stream must decode to (H, W, C)), e.g. to preprocess the whole
+    batch with one `resize_normalize_chw` launch; the returned list then
+    holds the views out[i]."""
+    if entropy not in ("gpu", "host"):
+        raise ValueError(f"entropy must be 'gpu' or 'host', got {entropy!r}")
     dev = _device(device)
     bufs = [_bytes(d) for d in streams]
     n = len(bufs)
@@ -146,36 +193,41 @@ def decode_jpeg_batch(streams: Sequence, device=None, threads: int | None = None
     infos = (_native.FvJpegInfo * n)()
     status = (ctypes.c_int32 * n)()
     lib.fv_jpeg_info_batch(data, lens, n, infos, status, threads)
-    for i in range(n):
-        if status[i]:
-            jpeg_info(bufs[i])  # raises with the message
-    word_off, plane_off = [], []
-    c = p = 0
-    for f in infos:
-        word_off.append(c)
+    k = next((i for i in range(n) if status[i]), n)  # images before the first header error
+    if out is not None:
+        if (out.device != dev or out.dtype != torch.uint8 or out.dim() != 4 or out.shape[0] != n
+                or out.stride(3) != 1 or out.stride(2) != out.shape[3]):
+            raise ShapeMismatch(f"out must be a ({n}, H, W, C) u8 tensor on {dev} with interleaved rows")
+        for i, f in enumerate(infos[:k]):
+            if tuple(out.shape[1:]) != (f.height, f.width, f.ncomp):
+                raise ShapeMismatch(f"stream {i} decodes to {(f.height, f.width, f.ncomp)}, out holds "
+                                    f"{tuple(out.shape[1:])}")
+    outs, plane_off = [], []
+    p = 0
+    for i, f in enumerate(infos[:k]):
+        outs.append(out[i] if out is not None else
+                    torch.empty((f.height, f.width, f.ncomp), dtype=torch.uint8, device=dev))
         plane_off.append(p)
-        c += (int(f.coef_count) // 64 + int(f.sparse_words) + 31) // 32 * 32
         p += (int(f.plane_bytes) + 255) // 256 * 256
-    outs = [torch.empty((f.height, f.width, f.ncomp), dtype=torch.uint8, device=dev) for f in infos]
-    words_dev = torch.empty(max(c, 1), dtype=torch.int32, device=dev)
     planes = torch.empty(max(p, 256), dtype=torch.uint8, device=dev)
     stream = torch.cuda.current_stream(dev)
-    with _Staging.lock:
-        host = _Staging.get(4 * c)
-        rc = lib.fv_jpeg_decode_batch(
-            data, lens, n, infos, host.data_ptr(), (ctypes.c_int64 * n)(*word_off), words_dev.data_ptr(),
-            planes.data_ptr(), (ctypes.c_int64 * n)(*plane_off), (ctypes.c_void_p * n)(*[o.data_ptr() for o in outs]),
-            (ctypes.c_int64 * n)(*[o.stride(0) for o in outs]), status, threads, stream.cuda_stream)
-        _Staging.event = torch.cuda.Event()
-        _Staging.event.record(stream)
-    if rc:
-        i = next(k for k in range(n) if status[k])
-        if status[i] != _native.FV_ERANGE:
-            decode_jpeg(bufs[i], dev)  # raises with the message
-            _raise(status[i], "fv_jpeg_decode_batch")
-        # a DC coefficient beyond int16: this image with int64 coefficients, then the rest
-        outs[i] = decode_jpeg(bufs[i], dev)
-        outs[i + 1:] = decode_jpeg_batch(bufs[i + 1:], dev, threads)
+    rest = list(range(k))
+    if entropy == "gpu" and k:
+        st = (ctypes.c_int32 * k)()
+        rc = lib.fv_jpeg_decode_batch_gpu(
+            data, lens, k, infos, planes.data_ptr(), (ctypes.c_int64 * k)(*plane_off),
+            (ctypes.c_void_p * k)(*[o.data_ptr() for o in outs]), (ctypes.c_int64 * k)(*[o.stride(0) for o in outs]),
+            st, threads, stream.cuda_stream)
+        if rc:
+            _raise(rc, "fv_jpeg_decode_batch_gpu")
+        rest = [i for i in range(k) if st[i] != 0]
+        stats["gpu_entropy"] += k - len(rest)
+    stats["host_entropy"] += len(rest)
+    if rest:
+        _host_batch([bufs[i] for i in rest], [infos[i] for i in rest], [outs[i] for i in rest], planes,
+                    [plane_off[i] for i in rest], threads, stream, dev)
+    if k < n:
+        jpeg_info(bufs[k])  # raises the header error of stream k
     return outs
 
 

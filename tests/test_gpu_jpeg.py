@@ -45,17 +45,78 @@ def test_rejects_like_the_reference(name):
         fio.decode_jpeg(stream(name))
 
 
-def test_batch_matches_single():
-    outs = fio.decode_jpeg_batch([stream(n) for n in DECODED], threads=8)
+@pytest.mark.parametrize("entropy", ["gpu", "host"])
+def test_batch_matches_single(entropy):
+    outs = fio.decode_jpeg_batch([stream(n) for n in DECODED], threads=8, entropy=entropy)
     for n, o in zip(DECODED, outs):
         assert np.array_equal(o.cpu().numpy(), _Z[n + "__out"]), n
 
 
-def test_batch_raises_first_error():
+def test_batch_into_out_tensor():
+    names = ["pil_ss0_q60", "pil_ss1_q85", "pil_ss2_q95"]  # same 77 x 129 x 3 frame
+    out = torch.zeros((3, 77, 129, 3), dtype=torch.uint8, device="cuda")
+    views = fio.decode_jpeg_batch([stream(n) for n in names], out=out)
+    for i, n in enumerate(names):
+        assert np.array_equal(out[i].cpu().numpy(), _Z[n + "__out"])
+        assert views[i].data_ptr() == out[i].data_ptr()
+    with pytest.raises(fv.ShapeMismatch):
+        fio.decode_jpeg_batch([stream("pil_photo_256")], out=out[:1])
+
+
+def test_gpu_entropy_path_really_runs():
+    """Every valid golden stream (4:4:4 / 4:2:2 / 4:2:0 / 4:4:0, gray,
+    restart markers, 16-bit tables, DC beyond int16) is decoded by the GPU
+    entropy path itself, not by the host fallback."""
+    g0, h0 = fio.stats["gpu_entropy"], fio.stats["host_entropy"]
+    outs = fio.decode_jpeg_batch([stream(n) for n in DECODED], entropy="gpu")
+    assert fio.stats["gpu_entropy"] - g0 == len(DECODED)
+    assert fio.stats["host_entropy"] == h0
+    for n, o in zip(DECODED, outs):
+        assert np.array_equal(o.cpu().numpy(), _Z[n + "__out"]), n
+
+
+@pytest.mark.parametrize("entropy", ["gpu", "host"])
+def test_batch_raises_first_error(entropy):
     with pytest.raises(fv.CorruptStream):
-        fio.decode_jpeg_batch([stream(DECODED[0]), stream("err_png")])
+        fio.decode_jpeg_batch([stream(DECODED[0]), stream("err_png")], entropy=entropy)
     with pytest.raises(fv.UnsupportedJpegFeature):  # header error vs entropy error: input order decides
-        fio.decode_jpeg_batch([stream("err_progressive"), stream("fuzz_mut_03")])
+        fio.decode_jpeg_batch([stream("err_progressive"), stream("fuzz_mut_03")], entropy=entropy)
+    with pytest.raises(fv.CorruptStream):  # entropy error first
+        fio.decode_jpeg_batch([stream("fuzz_mut_03"), stream("err_progressive")], entropy=entropy)
+
+
+@pytest.mark.parametrize("name", REJECTED)
+def test_gpu_entropy_rejects_like_the_reference(name):
+    """Every rejected golden stream, alone and behind a good one, through the
+    GPU entropy path: same exception class as the reference."""
+    ref = str(_Z[name + "__err"])
+    cls = fv.UnsupportedJpegFeature if ref == "UnsupportedJpegFeature" else fv.CorruptStream
+    with pytest.raises(cls):
+        fio.decode_jpeg_batch([stream(name)], entropy="gpu")
+    with pytest.raises(cls):
+        fio.decode_jpeg_batch([stream("pil_photo_256"), stream(name)], entropy="gpu")
+
+
+def test_gpu_entropy_fuzz_matches_host():
+    """Byte mutations of a restart-marker stream and of a plain one: the GPU
+    entropy path gives the host decoder's result (pixels or error class)."""
+    rng = np.random.default_rng(91)
+    for base_name in ("pil_restart_420", "pil_ss2_q85", "asm_440_q85"):
+        base = stream(base_name)
+        sos = base.find(b"\xff\xda")
+        for _ in range(40):
+            d = bytearray(base)
+            for _ in range(int(rng.integers(1, 4))):
+                d[int(rng.integers(sos + 14, len(d) - 2))] = int(rng.integers(0, 256))
+            d = bytes(d)
+            try:
+                ref = fio.decode_jpeg(d).cpu().numpy()
+            except fv.FoveaError as e:
+                with pytest.raises(type(e)):
+                    fio.decode_jpeg_batch([d], entropy="gpu")
+                continue
+            got = fio.decode_jpeg_batch([d], entropy="gpu")[0].cpu().numpy()
+            assert np.array_equal(got, ref)
 
 
 def test_batch_int16_overflow_image_and_repeats():
@@ -98,6 +159,27 @@ def test_full_frame_1080p(sub):
     data = _pil(smooth, quality=90, subsampling=sub)
     got = fio.decode_jpeg(data).cpu().numpy()
     assert np.array_equal(got, _oracle_from_coefficients(data))
+    # the GPU entropy path on the same frame (no restart markers: one segment
+    # of ~2000 self-synchronising subsequences), and with restart markers
+    assert np.array_equal(fio.decode_jpeg_batch([data], entropy="gpu")[0].cpu().numpy(), got)
+    data_rst = _pil(smooth, quality=90, subsampling=sub, restart_marker_blocks=5)
+    got_rst = fio.decode_jpeg_batch([data_rst, data], entropy="gpu")
+    assert np.array_equal(got_rst[0].cpu().numpy(), fio.decode_jpeg(data_rst).cpu().numpy())
+    assert np.array_equal(got_rst[1].cpu().numpy(), got)
+
+
+def test_gpu_entropy_smooth_and_noise_batch():
+    """64 frames (smooth q90 4:2:0 like the bench, noise q95 4:4:4) through
+    the GPU entropy path: identical to the single-image path."""
+    pytest.importorskip("PIL")
+    streams = []
+    for i in range(6):
+        streams.append(_pil(synth.seeded_smooth_u8_image(640 + 16 * i, 360 + 8 * i, 3, seed=i), quality=90,
+                            subsampling=2))
+        streams.append(_pil(synth.seeded_u8_image(320 + i, 200 + 3 * i, 3, seed=i), quality=95, subsampling=0))
+    outs = fio.decode_jpeg_batch(streams, entropy="gpu")
+    for d, o in zip(streams, outs):
+        assert np.array_equal(o.cpu().numpy(), fio.decode_jpeg(d).cpu().numpy())
 
 
 def test_odd_sizes_restart_and_gray_full_path():
