@@ -143,7 +143,7 @@ enum { kModeSync = 0, kModeCount = 1, kModeWrite = 2 };
 // decoder steps on deterministically (skip a bit / end the block).
 template <int MODE>
 __device__ uint64_t decode_run(const DevImg& im, DBits& b, int slot, int z, int64_t end_bit, bool last_sub,
-                               int64_t blk, const DevSeg& sg, int32_t* coef, int* nstart, int* bad) {
+                               int64_t blk, const DevSeg& sg, int16_t* coef, int* nstart, int* bad) {
   const int64_t limit = sg.first_block + sg.nblocks;
   for (;;) {
     const int64_t pos = b.pos();
@@ -155,7 +155,7 @@ __device__ uint64_t decode_run(const DevImg& im, DBits& b, int slot, int z, int6
     }
     b.fill();
     const int e = im.slot_e[slot];
-    int32_t* dst = nullptr;
+    int16_t* dst = nullptr;
     if (MODE == kModeWrite) {
       const int64_t cb = z == 0 ? blk : blk - 1;  // block this symbol belongs to
       if (cb >= sg.first_block && cb < limit) {
@@ -168,7 +168,7 @@ __device__ uint64_t decode_run(const DevImg& im, DBits& b, int slot, int z, int6
       }
     }
     if (z == 0) {  // DC of a new block
-      if (MODE == kModeCount) ++*nstart;
+      if (nstart) ++*nstart;
       if (MODE == kModeWrite) ++blk;
       const DevHuff& t = im.dc[e];
       const int32_t f = t.fast[b.peek(10)];
@@ -189,7 +189,7 @@ __device__ uint64_t decode_run(const DevImg& im, DBits& b, int slot, int z, int6
           diff = 0;
         }
       }
-      if (MODE == kModeWrite && dst) dst[0] = diff;
+      if (MODE == kModeWrite && dst) dst[0] = (int16_t)diff;  // |diff| <= 2047
       z = 1;
     } else {
       const DevHuff& t = im.ac[e];
@@ -201,7 +201,7 @@ __device__ uint64_t decode_run(const DevImg& im, DBits& b, int slot, int z, int6
           if (MODE == kModeWrite && dst) *bad = 1;
           z = 64;
         } else {
-          if (MODE == kModeWrite && dst) dst[kZigzagDev[z]] = f >> 16;
+          if (MODE == kModeWrite && dst) dst[kZigzagDev[z]] = (int16_t)(f >> 16);
           ++z;
         }
       } else {
@@ -222,7 +222,7 @@ __device__ uint64_t decode_run(const DevImg& im, DBits& b, int slot, int z, int6
             } else {
               const int32_t v = dextend(b.peek(sz), sz);
               b.skip(sz);
-              if (MODE == kModeWrite && dst) dst[kZigzagDev[z]] = v;
+              if (MODE == kModeWrite && dst) dst[kZigzagDev[z]] = (int16_t)v;  // |v| < 2^15
               ++z;
             }
           }
@@ -259,7 +259,7 @@ __device__ __forceinline__ void sub_range(const Pass& P, int64_t t, const DevSeg
   end = min(start + (int64_t)kSubBits, sg->bits);
 }
 
-__global__ void __launch_bounds__(128) k_spec(const __grid_constant__ Pass P, uint64_t* E) {
+__global__ void __launch_bounds__(128) k_spec(const __grid_constant__ Pass P, uint64_t* E, int32_t* cnt) {
   const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= P.nsub) return;
   const DevSeg* sg;
@@ -268,7 +268,9 @@ __global__ void __launch_bounds__(128) k_spec(const __grid_constant__ Pass P, ui
   DBits b;
   b.init(P.stream + sg->byte_off, sg->bits >> 3);
   b.start(start);
-  E[t] = decode_run<kModeSync>(P.imgs[sg->img], b, 0, 0, end, false, 0, *sg, nullptr, nullptr, nullptr);
+  int n = 0;
+  E[t] = decode_run<kModeSync>(P.imgs[sg->img], b, 0, 0, end, false, 0, *sg, nullptr, &n, nullptr);
+  cnt[t] = n;  // exact for each segment's first subsequence; the others are re-derived in the rounds
 }
 
 // One propagation round over a work queue: for each queued subsequence t,
@@ -285,9 +287,9 @@ __device__ __forceinline__ void enqueue(int32_t* qout, int* nout, int* mark, int
   if (atomicExch(&mark[t], round) != round) qout[atomicAdd(nout, 1)] = (int32_t)t;
 }
 
-__global__ void __launch_bounds__(128) k_round(const __grid_constant__ Pass P, uint64_t* E, const int32_t* qin,
-                                               const int* nin, int32_t* qout, int* nout, int* mark, int round,
-                                               int all_subs) {
+__global__ void __launch_bounds__(128) k_round(const __grid_constant__ Pass P, uint64_t* E, int32_t* cnt,
+                                               const int32_t* qin, const int* nin, int32_t* qout, int* nout, int* mark,
+                                               int round, int all_subs) {
   const int64_t n = all_subs ? P.nsub : *nin;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     int64_t t = all_subs ? i : qin[i];
@@ -303,8 +305,13 @@ __global__ void __launch_bounds__(128) k_round(const __grid_constant__ Pass P, u
       DBits b;
       b.init(P.stream + sg->byte_off, sg->bits >> 3);
       b.start(pos);
+      int nst = 0;
       const uint64_t e =
-          decode_run<kModeSync>(P.imgs[sg->img], b, slot, z, end, false, 0, *sg, nullptr, nullptr, nullptr);
+          decode_run<kModeSync>(P.imgs[sg->img], b, slot, z, end, false, 0, *sg, nullptr, &nst, nullptr);
+      // block starts of this subsequence: the LAST processing of t used its
+      // predecessor's final state (see the invariant above), so at the fixed
+      // point these counts are the true ones -- no separate count pass
+      cnt[t] = nst;
       if (e == E[t]) break;
       E[t] = e;
       if (local + 1 >= sg->nsub) break;
@@ -338,21 +345,6 @@ __device__ __forceinline__ void entry_state(const Pass& P, const uint64_t* E, in
   }
 }
 
-__global__ void __launch_bounds__(128) k_count(const __grid_constant__ Pass P, const uint64_t* E, int32_t* cnt) {
-  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (t >= P.nsub) return;
-  const DevSeg* sg;
-  int64_t local, start, end, pos;
-  int slot, z, n = 0;
-  sub_range(P, t, sg, local, start, end);
-  entry_state(P, E, t, local, start, pos, slot, z);
-  DBits b;
-  b.init(P.stream + sg->byte_off, sg->bits >> 3);
-  b.start(pos);
-  decode_run<kModeCount>(P.imgs[sg->img], b, slot, z, end, false, 0, *sg, nullptr, &n, nullptr);
-  cnt[t] = n;
-}
-
 // exclusive scan of the block-start counts of each segment's subsequences
 __global__ void __launch_bounds__(256) k_scan(const DevSeg* segs, int32_t nseg, const int32_t* cnt, int64_t* base) {
   __shared__ int64_t warp_sum[8];
@@ -384,7 +376,7 @@ __global__ void __launch_bounds__(256) k_scan(const DevSeg* segs, int32_t nseg, 
 }
 
 __global__ void __launch_bounds__(128) k_write(const __grid_constant__ Pass P, const uint64_t* E, const int64_t* base,
-                                               int32_t* coef, int* img_bad) {
+                                               int16_t* coef, int* img_bad) {
   const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= P.nsub) return;
   const DevSeg* sg;
@@ -400,9 +392,10 @@ __global__ void __launch_bounds__(128) k_write(const __grid_constant__ Pass P, c
 }
 
 // DC prediction: per (segment, scan entry), a prefix sum of the DC
-// differences over the component's blocks in decode order (MCU, then by, bx)
-__global__ void __launch_bounds__(256) k_dcpred(const DevImg* imgs, const DevSeg* segs, int32_t* coef) {
-  __shared__ int32_t warp_sum[8];
+// differences over the component's blocks in decode order (MCU, then by, bx).
+// Values beyond int16 (only crafted streams) flag the image: host decoder.
+__global__ void __launch_bounds__(1024) k_dcpred(const DevImg* imgs, const DevSeg* segs, int16_t* coef, int* img_bad) {
+  __shared__ int32_t warp_sum[32];
   const DevSeg& sg = segs[blockIdx.x];
   const DevImg& im = imgs[sg.img];
   const int e = blockIdx.y;
@@ -411,9 +404,10 @@ __global__ void __launch_bounds__(256) k_dcpred(const DevImg* imgs, const DevSeg
   const int64_t nblk = sg.nmcu * hv;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   int32_t carry = 0;
-  for (int64_t c0 = 0; c0 < nblk; c0 += 256) {
+  bool over = false;
+  for (int64_t c0 = 0; c0 < nblk; c0 += 1024) {
     const int64_t j = c0 + threadIdx.x;
-    int32_t* dc = nullptr;
+    int16_t* dc = nullptr;
     int32_t v = 0;
     if (j < nblk) {
       const int64_t mcu = sg.first_mcu + j / hv;
@@ -431,14 +425,20 @@ __global__ void __launch_bounds__(256) k_dcpred(const DevImg* imgs, const DevSeg
     if (lane == 31) warp_sum[w] = x;
     __syncthreads();
     int32_t pre = 0, tot = 0;
-    for (int k = 0; k < 8; ++k) {
-      if (k < w) pre += warp_sum[k];
-      tot += warp_sum[k];
+    for (int k = 0; k < 32; ++k) {
+      const int32_t q = warp_sum[k];
+      pre += k < w ? q : 0;
+      tot += q;
     }
-    if (dc) *dc = carry + pre + x;
+    if (dc) {
+      const int32_t val = carry + pre + x;
+      over = over || val < -32768 || val > 32767;
+      *dc = (int16_t)val;
+    }
     carry += tot;
     __syncthreads();
   }
+  if (over) img_bad[sg.img] = 1;
 }
 
 // ---------------------------------------------------------------------------
@@ -703,7 +703,8 @@ int fv_jpeg_decode_batch_gpu(const uint8_t* const* data, const int64_t* lens, in
   // 4. device buffers and passes
   DevBuf<DevImg> dimg;
   DevBuf<DevSeg> dseg;
-  DevBuf<int32_t> dsub, dcnt, dcoef, dflags;
+  DevBuf<int32_t> dsub, dcnt, dflags;
+  DevBuf<int16_t> dcoef;
   DevBuf<uint8_t> dbytes;
   DevBuf<uint64_t> dE0;
   DevBuf<int32_t> dq0, dq1, dmark;
@@ -730,13 +731,13 @@ int fv_jpeg_decode_batch_gpu(const uint8_t* const* data, const int64_t* lens, in
     cudaMemcpyAsync(dsub.p, hsub, nsub * sizeof(int32_t), cudaMemcpyHostToDevice, st);
     cudaMemcpyAsync(dbytes.p, hbytes, nbytes, cudaMemcpyHostToDevice, st);
     cudaMemcpyAsync(dflags.p, hflags.data(), hflags.size() * sizeof(int32_t), cudaMemcpyHostToDevice, st);
-    cudaMemsetAsync(dcoef.p, 0, ncoef * sizeof(int32_t), st);
+    cudaMemsetAsync(dcoef.p, 0, ncoef * sizeof(int16_t), st);
     cudaMemsetAsync(dmark.p, 0, nsub * sizeof(int32_t), st);
     Pass P{dimg.p, dseg.p, dsub.p, dbytes.p, nsub};
     const unsigned grid = (unsigned)((nsub + 127) / 128);
     int* img_bad = dflags.p;
     int* changed = dflags.p + nimg;  // changed[r], r = 0 .. kSyncRounds
-    k_spec<<<grid, 128, 0, st>>>(P, dE0.p);
+    k_spec<<<grid, 128, 0, st>>>(P, dE0.p, dcnt.p);
     count_launch();
     uint64_t* Ein = dE0.p;
     // rounds: the first over every subsequence, then over the queue of those
@@ -749,7 +750,8 @@ int fv_jpeg_decode_batch_gpu(const uint8_t* const* data, const int64_t* lens, in
     int r = 0;
     for (int chunk = 0; chunk < kSyncChunks && !rc; ++chunk) {
       for (int k = 0; k < kSyncRounds; ++k, ++r) {
-        k_round<<<r == 0 ? grid : qgrid, 128, 0, st>>>(P, Ein, qa, cnt + r, qb, cnt + r + 1, dmark.p, r + 1, r == 0);
+        k_round<<<r == 0 ? grid : qgrid, 128, 0, st>>>(P, Ein, dcnt.p, qa, cnt + r, qb, cnt + r + 1, dmark.p, r + 1,
+                                                       r == 0);
         count_launch();
         std::swap(qa, qb);
       }
@@ -773,12 +775,10 @@ int fv_jpeg_decode_batch_gpu(const uint8_t* const* data, const int64_t* lens, in
       for (int q = 1; q <= r; ++q) fprintf(stderr, " %d", ch[q]);
       fprintf(stderr, "\n");
     }
-    k_count<<<grid, 128, 0, st>>>(P, Ein, dcnt.p);
     k_scan<<<(unsigned)nseg, 256, 0, st>>>(dseg.p, (int32_t)nseg, dcnt.p, dbase.p);
     k_write<<<grid, 128, 0, st>>>(P, Ein, dbase.p, dcoef.p, img_bad);
-    k_dcpred<<<dim3((unsigned)nseg, 3), 256, 0, st>>>(dimg.p, dseg.p, dcoef.p);
+    k_dcpred<<<dim3((unsigned)nseg, 3), 1024, 0, st>>>(dimg.p, dseg.p, dcoef.p, img_bad);
     rc = check_launch("fv_jpeg_decode_batch_gpu passes");
-    count_launch();
     count_launch();
     count_launch();
   }
@@ -794,7 +794,7 @@ int fv_jpeg_decode_batch_gpu(const uint8_t* const* data, const int64_t* lens, in
       if (!plan[i].gpu || hflags[img_idx[i]]) continue;
       FvJpegInfo f;
       fill_info(*plan[i].s, f);
-      rc = reconstruct(f, dcoef.p + coef_off[i], 4, planes + plane_off[i], dst[i], dst_pitch[i], st);
+      rc = reconstruct(f, dcoef.p + coef_off[i], 2, planes + plane_off[i], dst[i], dst_pitch[i], st);
       if (!rc) status[i] = FV_OK;
     }
   }

@@ -65,14 +65,20 @@ def test_batch_into_out_tensor():
 
 def test_gpu_entropy_path_really_runs():
     """Every valid golden stream (4:4:4 / 4:2:2 / 4:2:0 / 4:4:0, gray,
-    restart markers, 16-bit tables, DC beyond int16) is decoded by the GPU
-    entropy path itself, not by the host fallback."""
+    restart markers, 16-bit tables, full-block noise at q100) is decoded by
+    the GPU entropy path itself, not by the host fallback -- except the
+    crafted one whose DC values exceed int16 (the GPU path's coefficient
+    width), which must fall back and still match."""
+    on_gpu = [n for n in DECODED if n != "asm_gray_dc_int16_overflow"]
     g0, h0 = fio.stats["gpu_entropy"], fio.stats["host_entropy"]
-    outs = fio.decode_jpeg_batch([stream(n) for n in DECODED], entropy="gpu")
-    assert fio.stats["gpu_entropy"] - g0 == len(DECODED)
+    outs = fio.decode_jpeg_batch([stream(n) for n in on_gpu], entropy="gpu")
+    assert fio.stats["gpu_entropy"] - g0 == len(on_gpu)
     assert fio.stats["host_entropy"] == h0
-    for n, o in zip(DECODED, outs):
+    for n, o in zip(on_gpu, outs):
         assert np.array_equal(o.cpu().numpy(), _Z[n + "__out"]), n
+    out = fio.decode_jpeg_batch([stream("asm_gray_dc_int16_overflow")], entropy="gpu")[0]
+    assert fio.stats["host_entropy"] == h0 + 1
+    assert np.array_equal(out.cpu().numpy(), _Z["asm_gray_dc_int16_overflow__out"])
 
 
 @pytest.mark.parametrize("entropy", ["gpu", "host"])
