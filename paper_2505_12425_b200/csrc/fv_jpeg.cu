@@ -261,12 +261,9 @@ __device__ __forceinline__ void samples4(const ColorArgs& a, int e, int x0, int 
   }
 }
 
-// Upsample + YCbCr -> RGB (jpeg.py:226-235, 783-806), four pixels per
-// thread; 12-byte groups stored as words when the row allows it.
-__global__ void __launch_bounds__(256) jpeg_color_kernel(const __grid_constant__ ColorArgs a) {
-  const int x0 = (blockIdx.x * 256 + threadIdx.x) * 4;
-  const int y = blockIdx.y;
-  if (x0 >= a.width) return;
+// Upsample + YCbCr -> RGB (jpeg.py:226-235, 783-806) of output pixels
+// x0..x0+3 of row y; 12-byte groups stored as words when the row allows it.
+__device__ __forceinline__ void color4(const ColorArgs& a, int x0, int y) {
   const int nk = min(4, a.width - x0);
   uint8_t* d = a.dst + (int64_t)y * a.d_rp;
   int Y[4];
@@ -299,6 +296,60 @@ __global__ void __launch_bounds__(256) jpeg_color_kernel(const __grid_constant__
   } else {
     for (int k = 0; k < 3 * nk; ++k) q[k] = o[k];
   }
+}
+
+__global__ void __launch_bounds__(256) jpeg_color_kernel(const __grid_constant__ ColorArgs a) {
+  const int x0 = (blockIdx.x * 256 + threadIdx.x) * 4;
+  if (x0 < a.width) color4(a, x0, blockIdx.y);
+}
+
+// Batched reconstruction (the GPU entropy path): one launch of each kernel
+// for a whole batch; a group / CTA finds its image by binary search over the
+// images' first block / row.
+struct IdctImg {
+  IdctArgs a;
+  int64_t base;  // first block of the image in the batch
+};
+struct ColorImg {
+  ColorArgs a;
+  int64_t base;  // first row of the image in the batch
+};
+template <typename I>
+__device__ __forceinline__ int find_img(const I* imgs, int n, int64_t k) {
+  int lo = 0, hi = n - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (imgs[mid].base <= k) lo = mid;
+    else hi = mid - 1;
+  }
+  return lo;
+}
+
+__global__ void __launch_bounds__(128) jpeg_idct_batch_kernel(const IdctImg* imgs, int nimg, int64_t total) {
+  __shared__ int64_t ws[16][8][9];
+  const int g = threadIdx.x >> 3, j = threadIdx.x & 7;
+  const int64_t gb = (int64_t)blockIdx.x * 16 + g;
+  if (gb >= total) return;  // whole 8-thread groups exit together
+  const int im = find_img(imgs, nimg, gb);
+  const IdctArgs& a = imgs[im].a;
+  const int64_t blk = gb - imgs[im].base;
+  int c = 0;
+  while (c + 1 < a.ncomp && blk >= a.first_block[c + 1]) ++c;
+  const int64_t lb = blk - a.first_block[c];
+  const int16_t* co = reinterpret_cast<const int16_t*>(a.coeffs) + a.coef_offset[c] + 64 * lb;
+  int64_t s[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) s[k] = (int64_t)co[8 * k + j] * (int64_t)a.qt[c][8 * k + j];
+  const int64_t by = lb / a.bw[c], bx = lb - by * a.bw[c];
+  uint8_t* dst = a.planes + a.plane_offset[c] + (by * 8 + j) * (int64_t)a.bw[c] * 8 + bx * 8;
+  idct_rows_store(s, ws, g, j, 0xFFu << (threadIdx.x & 24), dst);
+}
+
+__global__ void __launch_bounds__(256) jpeg_color_batch_kernel(const ColorImg* imgs, int nimg) {
+  const int im = find_img(imgs, nimg, (int64_t)blockIdx.x);
+  const ColorArgs& a = imgs[im].a;
+  const int y = (int)(blockIdx.x - imgs[im].base);
+  for (int x0 = threadIdx.x * 4; x0 < a.width; x0 += 1024) color4(a, x0, y);
 }
 
 }  // namespace jpg
@@ -344,18 +395,13 @@ namespace fv {
 namespace jpg {
 // coef_bytes 2 / 4 / 8: dense int16 / int32 / int64 coefficients; 1: the
 // sparse word stream of the host batch runtime
-int reconstruct(const FvJpegInfo& f, const void* coeffs, int32_t coef_bytes, uint8_t* planes, uint8_t* dst,
-                int64_t dst_row_pitch, cudaStream_t st) {
-  if (f.ncomp != 1 && f.ncomp != 3) return set_error(FV_EINVAL, "fv_jpeg_reconstruct: ncomp %d", f.ncomp);
-  if (dst_row_pitch < (int64_t)f.width * f.ncomp) return set_error(FV_EINVAL, "fv_jpeg_reconstruct: row pitch too small");
-  if ((reinterpret_cast<uintptr_t>(planes) & 7) != 0) return set_error(FV_EINVAL, "fv_jpeg_reconstruct: planes not 8-byte aligned");
-  // distinct components (duplicated scan entries share coefficients and plane)
-  IdctArgs ia{};
+static int64_t make_idct_args(const FvJpegInfo& f, const void* coeffs, uint8_t* planes, IdctArgs& ia) {
+  ia = IdctArgs{};
   ia.coeffs = coeffs;
   ia.planes = planes;
   int nd = 0;
   int64_t nb = 0;
-  for (int e = 0; e < f.ncomp; ++e) {
+  for (int e = 0; e < f.ncomp; ++e) {  // distinct components (duplicated scan entries share them)
     bool dup = false;
     for (int q = 0; q < nd; ++q) dup = dup || ia.coef_offset[q] == f.coef_offset[e];
     if (dup) continue;
@@ -369,15 +415,11 @@ int reconstruct(const FvJpegInfo& f, const void* coeffs, int32_t coef_bytes, uin
   }
   ia.ncomp = nd;
   ia.first_block[nd] = nb;
-  const int64_t grid = (nb + 15) / 16;
-  if (grid > 0x7FFFFFFF) return set_error(FV_EINVAL, "fv_jpeg_reconstruct: too many blocks");
-  if (coef_bytes == 2) jpeg_idct_kernel<int16_t><<<(unsigned)grid, 128, 0, st>>>(ia);
-  else if (coef_bytes == 4) jpeg_idct_kernel<int32_t><<<(unsigned)grid, 128, 0, st>>>(ia);
-  else if (coef_bytes == 8) jpeg_idct_kernel<int64_t><<<(unsigned)grid, 128, 0, st>>>(ia);
-  else jpeg_idct_sparse_kernel<<<(unsigned)grid, 128, 0, st>>>(ia, static_cast<const uint32_t*>(coeffs), f.coef_count / 64);
-  int rc = check_launch("jpeg_idct_kernel");
-  if (rc) return rc;
-  ColorArgs ca{};
+  return nb;
+}
+
+static void make_color_args(const FvJpegInfo& f, uint8_t* planes, uint8_t* dst, int64_t dst_row_pitch, ColorArgs& ca) {
+  ca = ColorArgs{};
   for (int e = 0; e < f.ncomp; ++e) {
     ca.plane[e] = planes + f.plane_offset[e];
     ca.pitch[e] = (int64_t)f.bw[e] * 8;
@@ -391,8 +433,70 @@ int reconstruct(const FvJpegInfo& f, const void* coeffs, int32_t coef_bytes, uin
   ca.height = f.height;
   ca.dst = dst;
   ca.d_rp = dst_row_pitch;
+}
+
+static int check_recon(const FvJpegInfo& f, uint8_t* planes, int64_t dst_row_pitch) {
+  if (f.ncomp != 1 && f.ncomp != 3) return set_error(FV_EINVAL, "fv_jpeg_reconstruct: ncomp %d", f.ncomp);
+  if (dst_row_pitch < (int64_t)f.width * f.ncomp) return set_error(FV_EINVAL, "fv_jpeg_reconstruct: row pitch too small");
+  if ((reinterpret_cast<uintptr_t>(planes) & 7) != 0) return set_error(FV_EINVAL, "fv_jpeg_reconstruct: planes not 8-byte aligned");
+  return FV_OK;
+}
+
+// coef_bytes 2 / 4 / 8: dense int16 / int32 / int64 coefficients; 1: the
+// sparse word stream of the host batch runtime
+int reconstruct(const FvJpegInfo& f, const void* coeffs, int32_t coef_bytes, uint8_t* planes, uint8_t* dst,
+                int64_t dst_row_pitch, cudaStream_t st) {
+  int rc = check_recon(f, planes, dst_row_pitch);
+  if (rc) return rc;
+  IdctArgs ia;
+  const int64_t nb = make_idct_args(f, coeffs, planes, ia);
+  const int64_t grid = (nb + 15) / 16;
+  if (grid > 0x7FFFFFFF) return set_error(FV_EINVAL, "fv_jpeg_reconstruct: too many blocks");
+  if (coef_bytes == 2) jpeg_idct_kernel<int16_t><<<(unsigned)grid, 128, 0, st>>>(ia);
+  else if (coef_bytes == 4) jpeg_idct_kernel<int32_t><<<(unsigned)grid, 128, 0, st>>>(ia);
+  else if (coef_bytes == 8) jpeg_idct_kernel<int64_t><<<(unsigned)grid, 128, 0, st>>>(ia);
+  else jpeg_idct_sparse_kernel<<<(unsigned)grid, 128, 0, st>>>(ia, static_cast<const uint32_t*>(coeffs), f.coef_count / 64);
+  rc = check_launch("jpeg_idct_kernel");
+  if (rc) return rc;
+  ColorArgs ca;
+  make_color_args(f, planes, dst, dst_row_pitch, ca);
   jpeg_color_kernel<<<dim3((f.width + 1023) / 1024, f.height), 256, 0, st>>>(ca);
   return check_launch("jpeg_color_kernel");
+}
+
+int reconstruct_batch(int n, const FvJpegInfo* const* fs, const int16_t* const* coeffs, uint8_t* const* planes,
+                      uint8_t* const* dst, const int64_t* dst_pitch, cudaStream_t st) {
+  if (n == 0) return FV_OK;
+  std::vector<IdctImg> ii(n);
+  std::vector<ColorImg> ci(n);
+  int64_t blocks = 0, rows = 0;
+  for (int i = 0; i < n; ++i) {
+    int rc = check_recon(*fs[i], planes[i], dst_pitch[i]);
+    if (rc) return rc;
+    ii[i].base = blocks;
+    blocks += make_idct_args(*fs[i], coeffs[i], planes[i], ii[i].a);
+    ci[i].base = rows;
+    make_color_args(*fs[i], planes[i], dst[i], dst_pitch[i], ci[i].a);
+    rows += fs[i]->height;
+  }
+  if ((blocks + 15) / 16 > 0x7FFFFFFF || rows > 0x7FFFFFFF)
+    return set_error(FV_EINVAL, "fv_jpeg_reconstruct: batch too large");
+  IdctImg* di = nullptr;
+  ColorImg* dc = nullptr;
+  if (cudaMallocAsync(reinterpret_cast<void**>(&di), n * sizeof(IdctImg), st) != cudaSuccess ||
+      cudaMallocAsync(reinterpret_cast<void**>(&dc), n * sizeof(ColorImg), st) != cudaSuccess)
+    return set_error(FV_ECUDA, "fv_jpeg_reconstruct: argument buffers");
+  cudaMemcpyAsync(di, ii.data(), n * sizeof(IdctImg), cudaMemcpyHostToDevice, st);
+  cudaMemcpyAsync(dc, ci.data(), n * sizeof(ColorImg), cudaMemcpyHostToDevice, st);
+  jpeg_idct_batch_kernel<<<(unsigned)((blocks + 15) / 16), 128, 0, st>>>(di, n, blocks);
+  int rc = check_launch("jpeg_idct_batch_kernel");
+  if (!rc) {
+    jpeg_color_batch_kernel<<<(unsigned)rows, 256, 0, st>>>(dc, n);
+    rc = check_launch("jpeg_color_batch_kernel");
+  }
+  cudaFreeAsync(di, st);
+  cudaFreeAsync(dc, st);
+  return rc;
 }
 
 // Batch worker: parse + sparse entropy decoding into `words` (block header

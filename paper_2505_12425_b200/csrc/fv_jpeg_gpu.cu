@@ -789,14 +789,25 @@ int fv_jpeg_decode_batch_gpu(const uint8_t* const* data, const int64_t* lens, in
     if (cudaStreamSynchronize(st) != cudaSuccess)
       rc = set_error(FV_ECUDA, "fv_jpeg_decode_batch_gpu: %s", cudaGetErrorString(cudaGetLastError()));
   }
-  if (!rc) {
-    for (int32_t i = 0; i < n && !rc; ++i) {
+  if (!rc) {  // one batched reconstruction of the cleanly decoded images
+    std::vector<FvJpegInfo> fi(n);
+    std::vector<const FvJpegInfo*> fs;
+    std::vector<const int16_t*> cs;
+    std::vector<uint8_t*> ps, ds;
+    std::vector<int64_t> dp;
+    for (int32_t i = 0; i < n; ++i) {
       if (!plan[i].gpu || hflags[img_idx[i]]) continue;
-      FvJpegInfo f;
-      fill_info(*plan[i].s, f);
-      rc = reconstruct(f, dcoef.p + coef_off[i], 2, planes + plane_off[i], dst[i], dst_pitch[i], st);
-      if (!rc) status[i] = FV_OK;
+      fill_info(*plan[i].s, fi[i]);
+      fs.push_back(&fi[i]);
+      cs.push_back(dcoef.p + coef_off[i]);
+      ps.push_back(planes + plane_off[i]);
+      ds.push_back(dst[i]);
+      dp.push_back(dst_pitch[i]);
     }
+    rc = reconstruct_batch((int)fs.size(), fs.data(), cs.data(), ps.data(), ds.data(), dp.data(), st);
+    if (!rc)
+      for (int32_t i = 0; i < n; ++i)
+        if (plan[i].gpu && !hflags[img_idx[i]]) status[i] = FV_OK;
   }
   timer.mark("flags + reconstruct launch");
   dimg.release(st);

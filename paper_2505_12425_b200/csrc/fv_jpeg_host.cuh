@@ -577,6 +577,9 @@ inline int decode_scan(const Stream& s, const FvJpegInfo& f, Sink& sink) {
 // sparse word stream) into dst.
 int reconstruct(const FvJpegInfo& f, const void* coeffs, int32_t coef_bytes, uint8_t* planes, uint8_t* dst,
                 int64_t dst_row_pitch, cudaStream_t st);
+// the same for n images with dense int16 coefficients: one launch per kernel
+int reconstruct_batch(int n, const FvJpegInfo* const* fs, const int16_t* const* coeffs, uint8_t* const* planes,
+                      uint8_t* const* dst, const int64_t* dst_pitch, cudaStream_t st);
 
 }  // namespace jpg
 }  // namespace fv
