@@ -224,6 +224,20 @@ int fv_jpeg_decode_batch_gpu(const uint8_t* const* data, const int64_t* lens, in
                              uint8_t* planes, const int64_t* plane_off, uint8_t* const* dst, const int64_t* dst_pitch,
                              int32_t* status, int32_t threads, void* stream);
 
+/* The same in two steps, so each stream is parsed once: fv_jpeg_batch_plan
+ * parses the n streams (status[i] = FV_OK or the header error, infos[i] the
+ * header when OK), unstuffs and stages the GPU path's inputs, and returns a
+ * handle; the caller allocates the outputs from `infos`; fv_jpeg_batch_run_gpu
+ * decodes (status[i] = FV_OK or FV_EFALLBACK as above; a NULL dst[i] skips
+ * image i, e.g. the images from the first header error on); fv_jpeg_batch_free
+ * releases the handle (it holds the library's pinned staging until then). The
+ * stream bytes must stay alive until the handle is freed. */
+int fv_jpeg_batch_plan(const uint8_t* const* data, const int64_t* lens, int32_t n, FvJpegInfo* infos, int32_t* status,
+                       int32_t threads, void** handle);
+int fv_jpeg_batch_run_gpu(void* handle, uint8_t* planes, const int64_t* plane_off, uint8_t* const* dst,
+                          const int64_t* dst_pitch, int32_t* status, void* stream);
+void fv_jpeg_batch_free(void* handle);
+
 /* ---- tuning / introspection ---------------------------------------------
  * Resize kernel selection: 0 = auto (default: exact 2:1 / 1:2 fast paths,
  * else the staged TMA strip kernel, else the direct-gather kernel),

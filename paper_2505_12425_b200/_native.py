@@ -71,6 +71,9 @@ SIGNATURES.update({
     "fv_jpeg_decode_batch": ([_P, _P, _I32, _c.POINTER(FvJpegInfo), _P, _P, _P, _P, _P, _P, _P, _P, _I32, _P],
                              _c.c_int),
     "fv_jpeg_decode_batch_gpu": ([_P, _P, _I32, _c.POINTER(FvJpegInfo), _P, _P, _P, _P, _P, _I32, _P], _c.c_int),
+    "fv_jpeg_batch_plan": ([_P, _P, _I32, _c.POINTER(FvJpegInfo), _P, _I32, _c.POINTER(_c.c_void_p)], _c.c_int),
+    "fv_jpeg_batch_run_gpu": ([_c.c_void_p, _P, _P, _P, _P, _P, _P], _c.c_int),
+    "fv_jpeg_batch_free": ([_c.c_void_p], None),
 })
 
 FV_ECORRUPT, FV_EUNSUPPORTED, FV_ERANGE, FV_EFALLBACK = -3, -4, -5, -6

@@ -564,19 +564,26 @@ struct PhaseTimer {  // FV_JPEG_TIMING=1: host phase times to stderr
 };
 }  // namespace
 
-extern "C" {
-
-int fv_jpeg_decode_batch_gpu(const uint8_t* const* data, const int64_t* lens, int32_t n, const FvJpegInfo* infos,
-                             uint8_t* planes, const int64_t* plane_off, uint8_t* const* dst, const int64_t* dst_pitch,
-                             int32_t* status, int32_t threads, void* stream) {
-  if (n < 0 || (n > 0 && (!data || !lens || !infos || !planes || !plane_off || !dst || !dst_pitch || !status)))
-    return set_error(FV_EINVAL, "fv_jpeg_decode_batch_gpu: bad arguments");
-  if (n == 0) return FV_OK;
-  cudaStream_t st = static_cast<cudaStream_t>(stream);
-  keep_pool_memory();
+// A planned batch: parsed streams, the GPU path's host staging (images,
+// segments, unstuffed bytes in pinned memory, whose lock it holds) and the
+// offsets; run_gpu() uploads and decodes it. Between plan and run the
+// caller allocates the outputs from the parsed headers.
+struct GpuBatch {
+  int32_t n = 0;
+  int nt = 1;
+  std::vector<Plan> plan;
+  std::vector<int64_t> seg_off, sub_off, byte_off, coef_off, img_idx;
+  int64_t nseg = 0, nsub = 0, nbytes = 0, ncoef = 0;
+  int32_t nimg = 0;
+  std::unique_lock<std::mutex> stage_lock;
+  DevImg* himg = nullptr;
+  DevSeg* hseg = nullptr;
+  int32_t* hsub = nullptr;
+  uint8_t* hbytes = nullptr;
   PhaseTimer timer;
-  const int nt = std::max(1, std::min<int>(threads, n));
-  auto parallel = [&](auto&& fn) {
+
+  template <class F>
+  void parallel(F&& fn) {
     std::atomic<int32_t> next{0};
     auto work = [&]() {
       for (int32_t i; (i = next.fetch_add(1)) < n;) fn(i);
@@ -585,9 +592,11 @@ int fv_jpeg_decode_batch_gpu(const uint8_t* const* data, const int64_t* lens, in
     for (int t = 1; t < nt; ++t) pool.emplace_back(work);
     work();
     for (auto& t : pool) t.join();
-  };
+  }
+
+  int make(const uint8_t* const* data, const int64_t* lens, FvJpegInfo* infos, int32_t* status) {
   // 1. parse, eligibility, sizes
-  std::vector<Plan> plan(n);
+  plan.resize(n);
   parallel([&](int32_t i) {
     Plan& p = plan[i];
     p.s.reset(new Stream());
@@ -608,11 +617,14 @@ int fv_jpeg_decode_batch_gpu(const uint8_t* const* data, const int64_t* lens, in
   });
   timer.mark("parse + plan");
   // 2. offsets
-  std::vector<int64_t> seg_off(n), sub_off(n), byte_off(n), coef_off(n), img_idx(n, -1);
-  int64_t nseg = 0, nsub = 0, nbytes = 0, ncoef = 0;
-  int32_t nimg = 0;
+  seg_off.assign(n, 0);
+  sub_off.assign(n, 0);
+  byte_off.assign(n, 0);
+  coef_off.assign(n, 0);
+  img_idx.assign(n, -1);
   for (int32_t i = 0; i < n; ++i) {
-    status[i] = FV_EFALLBACK;
+    status[i] = plan[i].rc;
+    if (plan[i].rc == FV_OK) fill_info(*plan[i].s, infos[i]);
     if (!plan[i].gpu) continue;
     img_idx[i] = nimg++;
     seg_off[i] = nseg;
@@ -627,17 +639,17 @@ int fv_jpeg_decode_batch_gpu(const uint8_t* const* data, const int64_t* lens, in
   if (nimg == 0) return FV_OK;
   // 3. host staging: images, segments, subsequence -> segment, unstuffed bytes
   PinnedStage& stage = pinned_stage();
-  std::lock_guard<std::mutex> stage_guard(stage.lock);
+  stage_lock = std::unique_lock<std::mutex>(stage.lock);  // held until the batch is freed
   const size_t o_img = 0, o_seg = o_img + ((nimg * sizeof(DevImg) + 255) & ~size_t(255));
   const size_t o_sub = o_seg + ((nseg * sizeof(DevSeg) + 255) & ~size_t(255));
   const size_t o_bytes = o_sub + ((nsub * sizeof(int32_t) + 255) & ~size_t(255));
   const size_t stage_bytes = o_bytes + nbytes + 16;
   uint8_t* sbase = stage.get(stage_bytes);
-  if (!sbase) return set_error(FV_ECUDA, "fv_jpeg_decode_batch_gpu: pinned staging of %zu bytes", stage_bytes);
-  DevImg* himg = reinterpret_cast<DevImg*>(sbase + o_img);
-  DevSeg* hseg = reinterpret_cast<DevSeg*>(sbase + o_seg);
-  int32_t* hsub = reinterpret_cast<int32_t*>(sbase + o_sub);
-  uint8_t* hbytes = sbase + o_bytes;
+  if (!sbase) return set_error(FV_ECUDA, "fv_jpeg_batch_plan: pinned staging of %zu bytes", stage_bytes);
+  himg = reinterpret_cast<DevImg*>(sbase + o_img);
+  hseg = reinterpret_cast<DevSeg*>(sbase + o_seg);
+  hsub = reinterpret_cast<int32_t*>(sbase + o_sub);
+  hbytes = sbase + o_bytes;
   parallel([&](int32_t i) {
     if (!plan[i].gpu) return;
     const Stream& s = *plan[i].s;
@@ -699,7 +711,14 @@ int fv_jpeg_decode_batch_gpu(const uint8_t* const* data, const int64_t* lens, in
       bo += (s.seg_len[k] + 15) / 16 * 16;  // 16-byte aligned, zero padded (DBits reads whole words)
     }
   });
-  timer.mark("unstuff + tables");
+    timer.mark("unstuff + tables");
+    return FV_OK;
+  }
+
+  int run(uint8_t* planes, const int64_t* plane_off, uint8_t* const* dst, const int64_t* dst_pitch, int32_t* status,
+          cudaStream_t st) {
+    for (int32_t i = 0; i < n; ++i) status[i] = FV_EFALLBACK;
+    if (nimg == 0) return FV_OK;
   // 4. device buffers and passes
   DevBuf<DevImg> dimg;
   DevBuf<DevSeg> dseg;
@@ -796,7 +815,7 @@ int fv_jpeg_decode_batch_gpu(const uint8_t* const* data, const int64_t* lens, in
     std::vector<uint8_t*> ps, ds;
     std::vector<int64_t> dp;
     for (int32_t i = 0; i < n; ++i) {
-      if (!plan[i].gpu || hflags[img_idx[i]]) continue;
+      if (!plan[i].gpu || hflags[img_idx[i]] || !dst[i]) continue;  // NULL dst: not wanted
       fill_info(*plan[i].s, fi[i]);
       fs.push_back(&fi[i]);
       cs.push_back(dcoef.p + coef_off[i]);
@@ -807,7 +826,7 @@ int fv_jpeg_decode_batch_gpu(const uint8_t* const* data, const int64_t* lens, in
     rc = reconstruct_batch((int)fs.size(), fs.data(), cs.data(), ps.data(), ds.data(), dp.data(), st);
     if (!rc)
       for (int32_t i = 0; i < n; ++i)
-        if (plan[i].gpu && !hflags[img_idx[i]]) status[i] = FV_OK;
+        if (plan[i].gpu && !hflags[img_idx[i]] && dst[i]) status[i] = FV_OK;
   }
   timer.mark("flags + reconstruct launch");
   dimg.release(st);
@@ -822,6 +841,46 @@ int fv_jpeg_decode_batch_gpu(const uint8_t* const* data, const int64_t* lens, in
   dbase.release(st);
   dcoef.release(st);
   dflags.release(st);
+    return rc;
+  }
+};
+
+extern "C" {
+
+int fv_jpeg_batch_plan(const uint8_t* const* data, const int64_t* lens, int32_t n, FvJpegInfo* infos, int32_t* status,
+                       int32_t threads, void** handle) {
+  if (!handle || n < 0 || (n > 0 && (!data || !lens || !infos || !status)))
+    return set_error(FV_EINVAL, "fv_jpeg_batch_plan: bad arguments");
+  keep_pool_memory();
+  std::unique_ptr<GpuBatch> b(new GpuBatch());
+  b->n = n;
+  b->nt = std::max(1, std::min<int>(threads, n));
+  const int rc = n ? b->make(data, lens, infos, status) : FV_OK;
+  if (rc) return rc;
+  *handle = b.release();
+  return FV_OK;
+}
+
+int fv_jpeg_batch_run_gpu(void* handle, uint8_t* planes, const int64_t* plane_off, uint8_t* const* dst,
+                          const int64_t* dst_pitch, int32_t* status, void* stream) {
+  GpuBatch* b = static_cast<GpuBatch*>(handle);
+  if (!b || (b->n > 0 && (!planes || !plane_off || !dst || !dst_pitch || !status)))
+    return set_error(FV_EINVAL, "fv_jpeg_batch_run_gpu: bad arguments");
+  return b->n ? b->run(planes, plane_off, dst, dst_pitch, status, static_cast<cudaStream_t>(stream)) : FV_OK;
+}
+
+void fv_jpeg_batch_free(void* handle) { delete static_cast<GpuBatch*>(handle); }
+
+int fv_jpeg_decode_batch_gpu(const uint8_t* const* data, const int64_t* lens, int32_t n, const FvJpegInfo* infos,
+                             uint8_t* planes, const int64_t* plane_off, uint8_t* const* dst, const int64_t* dst_pitch,
+                             int32_t* status, int32_t threads, void* stream) {
+  if (n < 0 || (n > 0 && (!data || !lens || !infos || !planes || !plane_off || !dst || !dst_pitch || !status)))
+    return set_error(FV_EINVAL, "fv_jpeg_decode_batch_gpu: bad arguments");
+  std::vector<FvJpegInfo> fi(n);
+  void* h = nullptr;
+  int rc = fv_jpeg_batch_plan(data, lens, n, fi.data(), status, threads, &h);
+  if (!rc) rc = fv_jpeg_batch_run_gpu(h, planes, plane_off, dst, dst_pitch, status, stream);
+  fv_jpeg_batch_free(h);
   return rc;
 }
 

@@ -192,40 +192,55 @@ def decode_jpeg_batch(streams: Sequence, device=None, threads: int | None = None
     lens = (ctypes.c_int64 * n)(*[len(b) for b in bufs])
     infos = (_native.FvJpegInfo * n)()
     status = (ctypes.c_int32 * n)()
-    lib.fv_jpeg_info_batch(data, lens, n, infos, status, threads)
-    k = next((i for i in range(n) if status[i]), n)  # images before the first header error
-    if out is not None:
-        if (out.device != dev or out.dtype != torch.uint8 or out.dim() != 4 or out.shape[0] != n
-                or out.stride(3) != 1 or out.stride(2) != out.shape[3]):
-            raise ShapeMismatch(f"out must be a ({n}, H, W, C) u8 tensor on {dev} with interleaved rows")
-        for i, f in enumerate(infos[:k]):
-            if tuple(out.shape[1:]) != (f.height, f.width, f.ncomp):
-                raise ShapeMismatch(f"stream {i} decodes to {(f.height, f.width, f.ncomp)}, out holds "
-                                    f"{tuple(out.shape[1:])}")
-    outs, plane_off = [], []
-    p = 0
-    for i, f in enumerate(infos[:k]):
-        outs.append(out[i] if out is not None else
-                    torch.empty((f.height, f.width, f.ncomp), dtype=torch.uint8, device=dev))
-        plane_off.append(p)
-        p += (int(f.plane_bytes) + 255) // 256 * 256
-    planes = torch.empty(max(p, 256), dtype=torch.uint8, device=dev)
-    stream = torch.cuda.current_stream(dev)
-    rest = list(range(k))
-    if entropy == "gpu" and k:
-        st = (ctypes.c_int32 * k)()
-        rc = lib.fv_jpeg_decode_batch_gpu(
-            data, lens, k, infos, planes.data_ptr(), (ctypes.c_int64 * k)(*plane_off),
-            (ctypes.c_void_p * k)(*[o.data_ptr() for o in outs]), (ctypes.c_int64 * k)(*[o.stride(0) for o in outs]),
-            st, threads, stream.cuda_stream)
+    handle = ctypes.c_void_p()
+    if entropy == "gpu":  # one parse: the plan also stages the GPU path's inputs
+        rc = lib.fv_jpeg_batch_plan(data, lens, n, infos, status, threads, ctypes.byref(handle))
         if rc:
-            _raise(rc, "fv_jpeg_decode_batch_gpu")
-        rest = [i for i in range(k) if st[i] != 0]
-        stats["gpu_entropy"] += k - len(rest)
-    stats["host_entropy"] += len(rest)
-    if rest:
-        _host_batch([bufs[i] for i in rest], [infos[i] for i in rest], [outs[i] for i in rest], planes,
-                    [plane_off[i] for i in rest], threads, stream, dev)
+            _raise(rc, "fv_jpeg_batch_plan")
+    else:
+        lib.fv_jpeg_info_batch(data, lens, n, infos, status, threads)
+    try:
+        k = next((i for i in range(n) if status[i]), n)  # images before the first header error
+        if out is not None:
+            if (out.device != dev or out.dtype != torch.uint8 or out.dim() != 4 or out.shape[0] != n
+                    or out.stride(3) != 1 or out.stride(2) != out.shape[3]):
+                raise ShapeMismatch(f"out must be a ({n}, H, W, C) u8 tensor on {dev} with interleaved rows")
+            for i, f in enumerate(infos[:k]):
+                if tuple(out.shape[1:]) != (f.height, f.width, f.ncomp):
+                    raise ShapeMismatch(f"stream {i} decodes to {(f.height, f.width, f.ncomp)}, out holds "
+                                        f"{tuple(out.shape[1:])}")
+        outs, plane_off = [], []
+        p = 0
+        for i in range(n):
+            f = infos[i]
+            ok = i < k
+            outs.append((out[i] if out is not None else
+                         torch.empty((f.height, f.width, f.ncomp), dtype=torch.uint8, device=dev)) if ok else None)
+            plane_off.append(p)
+            p += (int(f.plane_bytes) + 255) // 256 * 256 if ok else 0
+        planes = torch.empty(max(p, 256), dtype=torch.uint8, device=dev)
+        stream = torch.cuda.current_stream(dev)
+        rest = list(range(k))
+        if entropy == "gpu" and k:
+            st = (ctypes.c_int32 * n)()
+            # images from the first header error on: no target (NULL), not reconstructed
+            dst = [o.data_ptr() if o is not None else None for o in outs]
+            rc = lib.fv_jpeg_batch_run_gpu(
+                handle, planes.data_ptr(), (ctypes.c_int64 * n)(*plane_off), (ctypes.c_void_p * n)(*dst),
+                (ctypes.c_int64 * n)(*[o.stride(0) if o is not None else 0 for o in outs]), st,
+                stream.cuda_stream)
+            if rc:
+                _raise(rc, "fv_jpeg_batch_run_gpu")
+            rest = [i for i in range(k) if st[i] != 0]
+            stats["gpu_entropy"] += k - len(rest)
+        stats["host_entropy"] += len(rest)
+        if rest:
+            _host_batch([bufs[i] for i in rest], [infos[i] for i in rest], [outs[i] for i in rest], planes,
+                        [plane_off[i] for i in rest], threads, stream, dev)
+    finally:
+        if handle.value:
+            lib.fv_jpeg_batch_free(handle)
+    outs = outs[:k]
     if k < n:
         jpeg_info(bufs[k])  # raises the header error of stream k
     return outs

@@ -89,6 +89,12 @@ def test_batch_raises_first_error(entropy):
         fio.decode_jpeg_batch([stream("err_progressive"), stream("fuzz_mut_03")], entropy=entropy)
     with pytest.raises(fv.CorruptStream):  # entropy error first
         fio.decode_jpeg_batch([stream("fuzz_mut_03"), stream("err_progressive")], entropy=entropy)
+    # good streams after a header error are parsed but never written anywhere
+    canary = torch.full((1 << 20,), 0x5A, dtype=torch.uint8, device="cuda")
+    with pytest.raises(fv.CorruptStream):
+        fio.decode_jpeg_batch([stream("pil_ss2_q85"), stream("err_png"), stream("pil_photo_256")], entropy=entropy)
+    torch.cuda.synchronize()
+    assert bool((canary == 0x5A).all())
 
 
 @pytest.mark.parametrize("name", REJECTED)
