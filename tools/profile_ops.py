@@ -1,7 +1,7 @@
 """Run one BASELINE config's kernel(s) a few times at full size -- the short
 command that `ncu` wraps (see profiles/README.md). Not a benchmark: no timing.
 
-    python tools/profile_ops.py --op resize|down|up|gray|affine|persp|fused [--reps 2] [--images N]
+    python tools/profile_ops.py --op resize|down|up|gray|affine|persp|fused|jpeg [--reps 2] [--images N]
 """
 import argparse
 import os
@@ -55,6 +55,16 @@ def main():
         src = synth.device_u8_batch(n, 1080, 1920, 3, synth.SEED_FUSED, dev)
         dst = torch.zeros((n, 3, 640, 640), dtype=torch.float32, device=dev)
         runs.append(lambda: fv.resize_normalize_chw(src, dst, synth.MEAN, synth.STD))
+    elif a.op == "jpeg":  # decode -> preprocess: GPU entropy decoding + reconstruction of 64 1080p JPEGs
+        import bench
+        from paper_2505_12425_b200 import io as fio
+
+        n = a.images or 64
+        streams = bench.jpeg_streams(0, n)
+        frames = torch.empty((n, 1080, 1920, 3), dtype=torch.uint8, device=dev)
+        dst = torch.empty((n, 3, 640, 640), dtype=torch.float32, device=dev)
+        runs.append(lambda: (fio.decode_jpeg_batch(streams, dev, out=frames),
+                             fv.resize_normalize_chw(frames, dst, synth.MEAN, synth.STD)))
     else:
         raise SystemExit(f"unknown op {a.op}")
     for _ in range(a.reps):

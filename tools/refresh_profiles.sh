@@ -11,13 +11,13 @@ timeout 900 python bench.py > $out/${tag}_bench_full.json 2> $out/${tag}_bench_f
 echo "bench rc=$?"
 timeout 600 python bench.py --steps 2 --warmup 1 --no-cpu --no-e2e --soak 0 > /dev/null 2>&1 && \
   timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
-    -k "regex:resize_|warp_|gray_u8" --log-file $out/${tag}_launches.csv \
+    -k "regex:resize_|warp_|gray_u8|k_|jpeg_" --log-file $out/${tag}_launches.csv \
     python bench.py --steps 2 --warmup 1 --no-cpu --no-e2e --soak 0 > $out/${tag}_ncu_launch.log 2>&1
 echo "launch list rc=$?"
-for op in resize fused affine persp gray; do
-  n=1; [ $op = resize ] && n=2
+for op in resize fused affine persp gray jpeg; do
+  n=1; [ $op = resize ] && n=2; [ $op = jpeg ] && n=8
   timeout 300 python tools/profile_ops.py --op $op --reps 1 > /dev/null 2>&1 && \
-    timeout 900 ncu --set full --clock-control none --import-source on -k "regex:resize_|warp_|gray_u8" -c $n \
+    timeout 900 ncu --set full --clock-control none --import-source on -k "regex:resize_|warp_|gray_u8|k_spec|k_round|k_write|k_dcpred|jpeg_" -c $n \
       -o $out/${tag}_$op python tools/profile_ops.py --op $op --reps 1 > $out/${tag}_ncu_$op.log 2>&1
   echo "ncu $op rc=$?"
 done
