@@ -35,18 +35,25 @@ struct IdctArgs {
   uint16_t qt[3][64];
 };
 
-// One 8-point pass of the islow IDCT (jpeg.py:163-191), int64, outputs
-// before descaling in index order.
-__device__ __forceinline__ void idct8(const int64_t (&s)[8], int64_t (&o)[8]) {
-  const int64_t z1 = (s[2] + s[6]) * 4433;
-  const int64_t e2 = z1 - s[6] * 15137, e3 = z1 + s[2] * 6270;
-  const int64_t e0 = (s[0] + s[4]) * 8192, e1 = (s[0] - s[4]) * 8192;
-  const int64_t a10 = e0 + e3, a13 = e0 - e3, a11 = e1 + e2, a12 = e1 - e2;
-  const int64_t z5 = (s[7] + s[3] + s[5] + s[1]) * 9633;
-  const int64_t q1 = (s[7] + s[1]) * -7373, q2 = (s[5] + s[3]) * -20995;
-  const int64_t q3 = (s[7] + s[3]) * -16069 + z5, q4 = (s[5] + s[1]) * -3196 + z5;
-  const int64_t o0 = s[7] * 2446 + q1 + q3, o1 = s[5] * 16819 + q2 + q4;
-  const int64_t o2 = s[3] * 25172 + q2 + q3, o3 = s[1] * 12299 + q1 + q4;
+// One 8-point pass of the islow IDCT (jpeg.py:163-191), outputs before
+// descaling in index order. The reference computes in int64 (NumPy); T =
+// int32 gives the same integers whenever nothing overflows: every
+// intermediate is a signed sum of input multiples with total gain <= 178219
+// (triangle bound over the butterfly's terms; the outputs' exact L1 gain is
+// 61214), so |inputs| <= kIdct32Max keeps all of them below 2^31 - 2^17.
+constexpr int64_t kIdct32Max = 12000;
+
+template <typename T>
+__device__ __forceinline__ void idct8(const T (&s)[8], T (&o)[8]) {
+  const T z1 = (s[2] + s[6]) * 4433;
+  const T e2 = z1 - s[6] * 15137, e3 = z1 + s[2] * 6270;
+  const T e0 = (s[0] + s[4]) * 8192, e1 = (s[0] - s[4]) * 8192;
+  const T a10 = e0 + e3, a13 = e0 - e3, a11 = e1 + e2, a12 = e1 - e2;
+  const T z5 = (s[7] + s[3] + s[5] + s[1]) * 9633;
+  const T q1 = (s[7] + s[1]) * -7373, q2 = (s[5] + s[3]) * -20995;
+  const T q3 = (s[7] + s[3]) * -16069 + z5, q4 = (s[5] + s[1]) * -3196 + z5;
+  const T o0 = s[7] * 2446 + q1 + q3, o1 = s[5] * 16819 + q2 + q4;
+  const T o2 = s[3] * 25172 + q2 + q3, o3 = s[1] * 12299 + q1 + q4;
   o[0] = a10 + o3;
   o[1] = a11 + o2;
   o[2] = a12 + o1;
@@ -57,18 +64,35 @@ __device__ __forceinline__ void idct8(const int64_t (&s)[8], int64_t (&o)[8]) {
   o[7] = a10 - o3;
 }
 
+// the pass in int32 when this thread's inputs allow it, else in int64
+__device__ __forceinline__ void idct8_exact(const int64_t (&s)[8], int64_t (&o)[8]) {
+  bool small = true;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) small = small && s[k] >= -kIdct32Max && s[k] <= kIdct32Max;
+  if (small) {
+    int32_t a[8], b[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) a[k] = (int32_t)s[k];
+    idct8<int32_t>(a, b);
+#pragma unroll
+    for (int k = 0; k < 8; ++k) o[k] = b[k];
+  } else {
+    idct8<int64_t>(s, o);
+  }
+}
+
 // Second half of a block's IDCT, shared by the dense and sparse kernels:
 // s = the dequantised column j (vertical frequencies 0..7) of block g.
 __device__ __forceinline__ void idct_rows_store(int64_t (&s)[8], int64_t (&ws)[16][8][9], int g, int j, uint32_t mask,
                                                 uint8_t* dst) {
   int64_t o[8];
-  idct8(s, o);
+  idct8_exact(s, o);
 #pragma unroll
   for (int k = 0; k < 8; ++k) ws[g][k][j] = (o[k] + (1 << 10)) >> 11;
   __syncwarp(mask);
 #pragma unroll
   for (int k = 0; k < 8; ++k) s[k] = ws[g][j][k];
-  idct8(s, o);
+  idct8_exact(s, o);
   uint32_t w[2] = {0, 0};
 #pragma unroll
   for (int k = 0; k < 8; ++k) {
@@ -261,6 +285,31 @@ __device__ __forceinline__ void samples4(const ColorArgs& a, int e, int x0, int 
   }
 }
 
+// 4:2:0 chroma away from every edge: output columns x0..x0+3 need the
+// column sums of chroma columns j0-1 .. j0+2 (j0 = x0/2), read from each of
+// the two rows as one unaligned 4-byte window (two aligned words + a funnel
+// shift); no clamping, no edge formulas. Returns false when not interior.
+__device__ __forceinline__ bool chroma420_fast(const ColorArgs& a, int e, int x0, int y, int (&s)[4]) {
+  const int mw = a.cw[e], mh = a.ch[e];
+  const int j0 = x0 >> 1;
+  const int64_t pt = a.pitch[e];
+  if (mw <= 2 || x0 < 2 || j0 + 2 > mw - 1 || ((j0 - 1) & ~3) + 8 > pt) return false;
+  const int r = y >> 1, r2 = (y & 1) ? min(r + 1, mh - 1) : max(r - 1, 0);
+  const int base = (j0 - 1) & ~3, sh = 8 * ((j0 - 1) & 3);
+  const uint32_t* p0 = reinterpret_cast<const uint32_t*>(a.plane[e] + (int64_t)r * pt + base);
+  const uint32_t* p1 = reinterpret_cast<const uint32_t*>(a.plane[e] + (int64_t)r2 * pt + base);
+  const uint32_t w0 = __funnelshift_r(__ldg(p0), __ldg(p0 + 1), sh);
+  const uint32_t w1 = __funnelshift_r(__ldg(p1), __ldg(p1 + 1), sh);
+  int v[4];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) v[k] = 3 * (int)((w0 >> (8 * k)) & 0xFF) + (int)((w1 >> (8 * k)) & 0xFF);
+  s[0] = (3 * v[1] + v[0] + 8) >> 4;  // X = x0     (even, column j0)
+  s[1] = (3 * v[1] + v[2] + 7) >> 4;  // X = x0 + 1 (odd,  column j0)
+  s[2] = (3 * v[2] + v[1] + 8) >> 4;  // X = x0 + 2 (even, column j0 + 1)
+  s[3] = (3 * v[2] + v[3] + 7) >> 4;  // X = x0 + 3 (odd,  column j0 + 1)
+  return true;
+}
+
 // Upsample + YCbCr -> RGB (jpeg.py:226-235, 783-806) of output pixels
 // x0..x0+3 of row y; 12-byte groups stored as words when the row allows it.
 __device__ __forceinline__ void color4(const ColorArgs& a, int x0, int y) {
@@ -277,8 +326,11 @@ __device__ __forceinline__ void color4(const ColorArgs& a, int x0, int y) {
     return;
   }
   int B[4], R[4];
-  samples4(a, 1, x0, y, B);
-  samples4(a, 2, x0, y, R);
+  const bool h2v2 = a.fh[1] == 2 && a.fv[1] == 2 && a.fh[2] == 2 && a.fv[2] == 2;
+  if (!(h2v2 && nk == 4 && chroma420_fast(a, 1, x0, y, B) && chroma420_fast(a, 2, x0, y, R))) {
+    samples4(a, 1, x0, y, B);
+    samples4(a, 2, x0, y, R);
+  }
   uint8_t o[12];
 #pragma unroll
   for (int k = 0; k < 4; ++k) {

@@ -24,6 +24,9 @@
 #include <cstdlib>
 #include <mutex>
 #include <thread>
+#if defined(__x86_64__)
+#include <immintrin.h>
+#endif
 
 #include "fv_jpeg_host.cuh"
 
@@ -487,6 +490,33 @@ inline bool gpu_eligible(const Stream& s, const FvJpegInfo& f) {
   return f.coef_count > 0;
 }
 
+// Write back and evict a host range the planner threads just wrote to the
+// pinned staging. Measured on the GPU boxes: H2D DMA from pinned memory whose
+// lines sit dirty in many cores' private caches runs at 6-8 GB/s (every line
+// is snooped), against 54 GB/s once the writers flush them
+// (tools/probe/h2d_probe3.cu).
+#if defined(__x86_64__)
+__attribute__((target("clflushopt"))) static void flush_lines_opt(const void* p, size_t n) {
+  char* c = static_cast<char*>(const_cast<void*>(p));
+  for (size_t i = 0; i < n; i += 64) _mm_clflushopt(c + i);
+  if (n) _mm_clflushopt(c + n - 1);
+  _mm_sfence();
+}
+static void flush_lines(const void* p, size_t n) {
+  static const bool opt = __builtin_cpu_supports("clflushopt");
+  if (opt) {
+    flush_lines_opt(p, n);
+    return;
+  }
+  const char* c = static_cast<const char*>(p);
+  for (size_t i = 0; i < n; i += 64) _mm_clflush(c + i);
+  if (n) _mm_clflush(c + n - 1);
+  _mm_mfence();
+}
+#else
+static void flush_lines(const void*, size_t) {}
+#endif
+
 // Pinned host staging for the uploads, kept across calls (one caller at a
 // time: the call synchronises its stream before returning, so the buffer is
 // free again when the next call takes the lock).
@@ -552,8 +582,27 @@ using namespace fv;
 using namespace fv::jpg;
 
 namespace {
-struct PhaseTimer {  // FV_JPEG_TIMING=1: host phase times to stderr
+struct PhaseTimer {  // FV_JPEG_TIMING=1: host phase times (and GPU phase times) to stderr
   bool on = getenv("FV_JPEG_TIMING") != nullptr;
+  std::vector<std::pair<const char*, cudaEvent_t>> ev;
+  void gpu(const char* what, cudaStream_t st) {
+    if (!on) return;
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    cudaEventRecord(e, st);
+    ev.emplace_back(what, e);
+  }
+  void gpu_report() {
+    if (!on || ev.size() < 2) return;
+    cudaEventSynchronize(ev.back().second);
+    for (size_t k = 1; k < ev.size(); ++k) {
+      float ms = 0;
+      cudaEventElapsedTime(&ms, ev[k - 1].second, ev[k].second);
+      fprintf(stderr, "[fv_jpeg_gpu]   gpu %-22s %8.3f ms\n", ev[k].first, ms);
+    }
+    for (auto& x : ev) cudaEventDestroy(x.second);
+    ev.clear();
+  }
   std::chrono::steady_clock::time_point t0 = std::chrono::steady_clock::now();
   void mark(const char* what) {
     if (!on) return;
@@ -576,6 +625,8 @@ struct GpuBatch {
   int64_t nseg = 0, nsub = 0, nbytes = 0, ncoef = 0;
   int32_t nimg = 0;
   std::unique_lock<std::mutex> stage_lock;
+  uint8_t* stage_base = nullptr;
+  size_t o_img = 0, o_seg = 0, o_sub = 0, o_bytes = 0, stage_bytes = 0;  // one contiguous upload
   DevImg* himg = nullptr;
   DevSeg* hseg = nullptr;
   int32_t* hsub = nullptr;
@@ -640,12 +691,14 @@ struct GpuBatch {
   // 3. host staging: images, segments, subsequence -> segment, unstuffed bytes
   PinnedStage& stage = pinned_stage();
   stage_lock = std::unique_lock<std::mutex>(stage.lock);  // held until the batch is freed
-  const size_t o_img = 0, o_seg = o_img + ((nimg * sizeof(DevImg) + 255) & ~size_t(255));
-  const size_t o_sub = o_seg + ((nseg * sizeof(DevSeg) + 255) & ~size_t(255));
-  const size_t o_bytes = o_sub + ((nsub * sizeof(int32_t) + 255) & ~size_t(255));
-  const size_t stage_bytes = o_bytes + nbytes + 16;
+  o_img = 0;
+  o_seg = o_img + ((nimg * sizeof(DevImg) + 255) & ~size_t(255));
+  o_sub = o_seg + ((nseg * sizeof(DevSeg) + 255) & ~size_t(255));
+  o_bytes = o_sub + ((nsub * sizeof(int32_t) + 255) & ~size_t(255));
+  stage_bytes = o_bytes + nbytes + 16;
   uint8_t* sbase = stage.get(stage_bytes);
   if (!sbase) return set_error(FV_ECUDA, "fv_jpeg_batch_plan: pinned staging of %zu bytes", stage_bytes);
+  stage_base = sbase;
   himg = reinterpret_cast<DevImg*>(sbase + o_img);
   hseg = reinterpret_cast<DevSeg*>(sbase + o_seg);
   hsub = reinterpret_cast<int32_t*>(sbase + o_sub);
@@ -655,7 +708,10 @@ struct GpuBatch {
     const Stream& s = *plan[i].s;
     FvJpegInfo f;
     fill_info(s, f);
-    DevImg& d = himg[img_idx[i]];
+    // built locally, then written to the staging in one go (the staging is
+    // written sequentially and never read back by the host)
+    std::unique_ptr<DevImg> dp(new DevImg());
+    DevImg& d = *dp;
     memset(&d, 0, sizeof(d));
     int slot = 0;
     for (int e = 0; e < s.nscan; ++e) {
@@ -676,10 +732,12 @@ struct GpuBatch {
     d.nslots = slot;
     d.mcus_x = s.mcus_x;
     d.coef_base = coef_off[i];
+    memcpy(&himg[img_idx[i]], &d, sizeof(d));
+    flush_lines(&himg[img_idx[i]], sizeof(d));
     const int64_t total = (int64_t)s.mcus_x * s.mcus_y;
     int64_t bo = byte_off[i], so = sub_off[i];
     for (int64_t k = 0; k < plan[i].nseg; ++k) {
-      DevSeg& g = hseg[seg_off[i] + k];
+      DevSeg g{};
       g.img = (int32_t)img_idx[i];
       g.byte_off = bo;
       g.bits = 8 * s.seg_len[k];
@@ -689,7 +747,10 @@ struct GpuBatch {
       g.nblocks = g.nmcu * slot;
       g.first_sub = (int32_t)so;
       g.nsub = (int32_t)std::max<int64_t>(1, (g.bits + kSubBits - 1) / kSubBits);
+      hseg[seg_off[i] + k] = g;
+      flush_lines(&hseg[seg_off[i] + k], sizeof(g));
       for (int32_t q = 0; q < g.nsub; ++q) hsub[so + q] = (int32_t)(seg_off[i] + k);
+      flush_lines(&hsub[so], sizeof(int32_t) * (size_t)g.nsub);
       so += g.nsub;
       // unstuff the segment: copy runs between 0xFF bytes, FF 00 -> FF, drop fill FFs
       uint8_t* out = hbytes + bo;
@@ -708,6 +769,7 @@ struct GpuBatch {
         }
       }
       memset(out, 0, (size_t)((s.seg_len[k] + 15) / 16 * 16 - s.seg_len[k]));  // zero padding
+      flush_lines(hbytes + bo, (size_t)((s.seg_len[k] + 15) / 16 * 16));
       bo += (s.seg_len[k] + 15) / 16 * 16;  // 16-byte aligned, zero padded (DBits reads whole words)
     }
   });
@@ -720,20 +782,15 @@ struct GpuBatch {
     for (int32_t i = 0; i < n; ++i) status[i] = FV_EFALLBACK;
     if (nimg == 0) return FV_OK;
   // 4. device buffers and passes
-  DevBuf<DevImg> dimg;
-  DevBuf<DevSeg> dseg;
-  DevBuf<int32_t> dsub, dcnt, dflags;
+  DevBuf<uint8_t> dstage;  // images, segments, subsequence map, unstuffed bytes (the pinned staging's layout)
+  DevBuf<int32_t> dcnt, dflags;
   DevBuf<int16_t> dcoef;
-  DevBuf<uint8_t> dbytes;
   DevBuf<uint64_t> dE0;
   DevBuf<int32_t> dq0, dq1, dmark;
   DevBuf<int64_t> dbase;
   int rc = FV_OK;
-  rc = rc ? rc : dimg.alloc(nimg, st);
-  rc = rc ? rc : dseg.alloc(nseg, st);
-  rc = rc ? rc : dsub.alloc(nsub, st);
+  rc = rc ? rc : dstage.alloc(stage_bytes, st);
   rc = rc ? rc : dcnt.alloc(nsub, st);
-  rc = rc ? rc : dbytes.alloc(nbytes + 16, st);
   rc = rc ? rc : dE0.alloc(nsub, st);
   rc = rc ? rc : dq0.alloc(nsub, st);
   rc = rc ? rc : dq1.alloc(nsub, st);
@@ -745,18 +802,27 @@ struct GpuBatch {
   std::vector<int32_t> hflags(nimg + nrounds + 2, 0);
   if (!rc) {
     // hflags: img_bad[nimg] = 0, then the per-round queue lengths (all 0)
-    cudaMemcpyAsync(dimg.p, himg, nimg * sizeof(DevImg), cudaMemcpyHostToDevice, st);
-    cudaMemcpyAsync(dseg.p, hseg, nseg * sizeof(DevSeg), cudaMemcpyHostToDevice, st);
-    cudaMemcpyAsync(dsub.p, hsub, nsub * sizeof(int32_t), cudaMemcpyHostToDevice, st);
-    cudaMemcpyAsync(dbytes.p, hbytes, nbytes, cudaMemcpyHostToDevice, st);
+    timer.gpu("start", st);
+    cudaMemcpyAsync(dstage.p, stage_base, stage_bytes, cudaMemcpyHostToDevice, st);
+    timer.gpu("h2d staging", st);
+    if (timer.on && getenv("FV_JPEG_TIMING2")) {
+      cudaMemcpyAsync(dstage.p, stage_base, stage_bytes, cudaMemcpyHostToDevice, st);
+      timer.gpu("h2d staging (again)", st);
+    }
+    DevImg* const dimg_p = reinterpret_cast<DevImg*>(dstage.p + o_img);
+    DevSeg* const dseg_p = reinterpret_cast<DevSeg*>(dstage.p + o_seg);
+    const int32_t* const dsub_p = reinterpret_cast<const int32_t*>(dstage.p + o_sub);
+    const uint8_t* const dbytes_p = dstage.p + o_bytes;
     cudaMemcpyAsync(dflags.p, hflags.data(), hflags.size() * sizeof(int32_t), cudaMemcpyHostToDevice, st);
     cudaMemsetAsync(dcoef.p, 0, ncoef * sizeof(int16_t), st);
     cudaMemsetAsync(dmark.p, 0, nsub * sizeof(int32_t), st);
-    Pass P{dimg.p, dseg.p, dsub.p, dbytes.p, nsub};
+    Pass P{dimg_p, dseg_p, dsub_p, dbytes_p, nsub};
     const unsigned grid = (unsigned)((nsub + 127) / 128);
     int* img_bad = dflags.p;
     int* changed = dflags.p + nimg;  // changed[r], r = 0 .. kSyncRounds
+    timer.gpu("flags + memsets", st);
     k_spec<<<grid, 128, 0, st>>>(P, dE0.p, dcnt.p);
+    timer.gpu("speculative pass", st);
     count_launch();
     uint64_t* Ein = dE0.p;
     // rounds: the first over every subsequence, then over the queue of those
@@ -786,6 +852,7 @@ struct GpuBatch {
         count_launch();
       }
     }
+    timer.gpu("sync rounds", st);
     timer.mark("speculative + sync rounds");
     if (timer.on) {
       std::vector<int32_t> ch(r + 1);
@@ -794,9 +861,11 @@ struct GpuBatch {
       for (int q = 1; q <= r; ++q) fprintf(stderr, " %d", ch[q]);
       fprintf(stderr, "\n");
     }
-    k_scan<<<(unsigned)nseg, 256, 0, st>>>(dseg.p, (int32_t)nseg, dcnt.p, dbase.p);
+    k_scan<<<(unsigned)nseg, 256, 0, st>>>(dseg_p, (int32_t)nseg, dcnt.p, dbase.p);
     k_write<<<grid, 128, 0, st>>>(P, Ein, dbase.p, dcoef.p, img_bad);
-    k_dcpred<<<dim3((unsigned)nseg, 3), 1024, 0, st>>>(dimg.p, dseg.p, dcoef.p, img_bad);
+    timer.gpu("scan + write", st);
+    k_dcpred<<<dim3((unsigned)nseg, 3), 1024, 0, st>>>(dimg_p, dseg_p, dcoef.p, img_bad);
+    timer.gpu("dc prediction", st);
     rc = check_launch("fv_jpeg_decode_batch_gpu passes");
     count_launch();
     count_launch();
@@ -823,17 +892,17 @@ struct GpuBatch {
       ds.push_back(dst[i]);
       dp.push_back(dst_pitch[i]);
     }
+    timer.gpu("flags readback", st);
     rc = reconstruct_batch((int)fs.size(), fs.data(), cs.data(), ps.data(), ds.data(), dp.data(), st);
+    timer.gpu("idct + colour", st);
     if (!rc)
       for (int32_t i = 0; i < n; ++i)
         if (plan[i].gpu && !hflags[img_idx[i]] && dst[i]) status[i] = FV_OK;
   }
   timer.mark("flags + reconstruct launch");
-  dimg.release(st);
-  dseg.release(st);
-  dsub.release(st);
+  timer.gpu_report();
+  dstage.release(st);
   dcnt.release(st);
-  dbytes.release(st);
   dE0.release(st);
   dq0.release(st);
   dq1.release(st);
