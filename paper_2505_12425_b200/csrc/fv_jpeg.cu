@@ -614,6 +614,7 @@ int fv_jpeg_decode_batch(const uint8_t* const* data, const int64_t* lens, int32_
     for (int32_t i; (i = next.fetch_add(1)) < n;) {
       const int64_t cap = infos[i].coef_count / 64 + infos[i].sparse_words;
       const int rc = decode_one_sparse(data[i], lens[i], words_host + word_off[i], cap, &used[i]);
+      if (rc == FV_OK) flush_lines(words_host + word_off[i], (size_t)used[i] * 4);  // DMA-friendly (see flush_lines)
       done[i].store(rc, std::memory_order_release);
     }
   };

@@ -24,9 +24,6 @@
 #include <cstdlib>
 #include <mutex>
 #include <thread>
-#if defined(__x86_64__)
-#include <immintrin.h>
-#endif
 
 #include "fv_jpeg_host.cuh"
 
@@ -489,33 +486,6 @@ inline bool gpu_eligible(const Stream& s, const FvJpegInfo& f) {
   if (per_mcu > kMaxSlots) return false;
   return f.coef_count > 0;
 }
-
-// Write back and evict a host range the planner threads just wrote to the
-// pinned staging. Measured on the GPU boxes: H2D DMA from pinned memory whose
-// lines sit dirty in many cores' private caches runs at 6-8 GB/s (every line
-// is snooped), against 54 GB/s once the writers flush them
-// (tools/probe/h2d_probe3.cu).
-#if defined(__x86_64__)
-__attribute__((target("clflushopt"))) static void flush_lines_opt(const void* p, size_t n) {
-  char* c = static_cast<char*>(const_cast<void*>(p));
-  for (size_t i = 0; i < n; i += 64) _mm_clflushopt(c + i);
-  if (n) _mm_clflushopt(c + n - 1);
-  _mm_sfence();
-}
-static void flush_lines(const void* p, size_t n) {
-  static const bool opt = __builtin_cpu_supports("clflushopt");
-  if (opt) {
-    flush_lines_opt(p, n);
-    return;
-  }
-  const char* c = static_cast<const char*>(p);
-  for (size_t i = 0; i < n; i += 64) _mm_clflush(c + i);
-  if (n) _mm_clflush(c + n - 1);
-  _mm_mfence();
-}
-#else
-static void flush_lines(const void*, size_t) {}
-#endif
 
 // Pinned host staging for the uploads, kept across calls (one caller at a
 // time: the call synchronises its stream before returning, so the buffer is
