@@ -35,6 +35,8 @@ constexpr int kMaxSlots = 12;
 constexpr int kSyncRounds = 6;    // rounds per chunk (one 4-byte readback per chunk)
 constexpr int kSyncChunks = 32;   // cap: images still changing after this fall back
 constexpr int kChain = 8;         // subsequences one thread may carry a changed state through per round
+constexpr int kChain0 = 8;        // ... in the first (full) round
+constexpr int kWarm = 1;          // speculative pass: subsequences decoded before a thread's own, to synchronise
 
 __constant__ int kZigzagDev[64] = {0,  1,  8,  16, 9,  2,  3,  10, 17, 24, 32, 25, 18, 11, 4,  5,
                                    12, 19, 26, 33, 40, 48, 41, 34, 27, 20, 13, 6,  7,  14, 21, 28,
@@ -267,9 +269,17 @@ __global__ void __launch_bounds__(128) k_spec(const __grid_constant__ Pass P, ui
   sub_range(P, t, sg, local, start, end);
   DBits b;
   b.init(P.stream + sg->byte_off, sg->bits >> 3);
-  b.start(start);
+  int slot = 0, z = 0;
+  int64_t pos = start;
+  if (kWarm && local > 0) {  // warm up on the preceding bits: enter this subsequence (likely) in step
+    const int64_t w0 = start > (int64_t)kWarm * kSubBits ? start - (int64_t)kWarm * kSubBits : 0;
+    b.start(w0);
+    const uint64_t e = decode_run<kModeSync>(P.imgs[sg->img], b, 0, 0, start, false, 0, *sg, nullptr, nullptr, nullptr);
+    unpack_state(e, pos, slot, z);
+  }
+  b.start(pos);
   int n = 0;
-  E[t] = decode_run<kModeSync>(P.imgs[sg->img], b, 0, 0, end, false, 0, *sg, nullptr, &n, nullptr);
+  E[t] = decode_run<kModeSync>(P.imgs[sg->img], b, slot, z, end, false, 0, *sg, nullptr, &n, nullptr);
   cnt[t] = n;  // exact for each segment's first subsequence; the others are re-derived in the rounds
 }
 
@@ -289,7 +299,7 @@ __device__ __forceinline__ void enqueue(int32_t* qout, int* nout, int* mark, int
 
 __global__ void __launch_bounds__(128) k_round(const __grid_constant__ Pass P, uint64_t* E, int32_t* cnt,
                                                const int32_t* qin, const int* nin, int32_t* qout, int* nout, int* mark,
-                                               int round, int all_subs) {
+                                               int round, int all_subs, int chain) {
   const int64_t n = all_subs ? P.nsub : *nin;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     int64_t t = all_subs ? i : qin[i];
@@ -316,7 +326,7 @@ __global__ void __launch_bounds__(128) k_round(const __grid_constant__ Pass P, u
       E[t] = e;
       if (local + 1 >= sg->nsub) break;
       enqueue(qout, nout, mark, t + 1, round);  // re-derive t+1 next round, whatever happens below
-      if (step + 1 == kChain) break;
+      if (step + 1 == chain) break;
       in = e;
       ++t;
       ++local;
@@ -806,7 +816,8 @@ struct GpuBatch {
     for (int chunk = 0; chunk < kSyncChunks && !rc; ++chunk) {
       for (int k = 0; k < kSyncRounds; ++k, ++r) {
         k_round<<<r == 0 ? grid : qgrid, 128, 0, st>>>(P, Ein, dcnt.p, qa, cnt + r, qb, cnt + r + 1, dmark.p, r + 1,
-                                                       r == 0);
+                                                       r == 0, r == 0 ? kChain0 : kChain);
+        if (timer.on) timer.gpu(r == 0 ? "round 0 (all)" : "round k (queue)", st);
         count_launch();
         std::swap(qa, qb);
       }
