@@ -250,7 +250,7 @@ def build_ops(n_scale, world, rank, dev, include):
         step()
         on_gpu = fio.stats["gpu_entropy"] - gpu0
         ops["f4_jpeg_decode_preprocess_64x1080p"] = dict(
-            launches=[("jpeg_decode+preprocess (host entropy + GPU)", step, nbytes)],
+            launches=[("jpeg_decode+preprocess (GPU entropy + reconstruction + resize)", step, nbytes)],
             dst_px=(hi - lo) * 1920 * 1080, src_px=(hi - lo) * 1920 * 1080, images=n_total,
             l2="host JPEG bytes (q90 4:2:0, ~200 KB each)",
             extra={"mean_stream_kb": round(sum(len(b) for b in streams) / len(streams) / 1e3, 1),
