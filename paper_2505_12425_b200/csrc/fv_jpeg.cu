@@ -32,7 +32,7 @@ struct IdctArgs {
   int64_t coef_offset[3];
   int64_t plane_offset[3];
   int bw[3];
-  uint16_t qt[3][64];
+  alignas(16) uint16_t qt[3][64];  // rows are read as 16-byte vectors by the batch kernel
 };
 
 // One 8-point pass of the islow IDCT (jpeg.py:163-191), outputs before
@@ -362,6 +362,7 @@ struct IdctImg {
   IdctArgs a;
   int64_t base;  // first block of the image in the batch
 };
+static_assert(alignof(IdctArgs) >= 16 && sizeof(IdctImg) % 16 == 0, "16-byte quant rows");
 struct ColorImg {
   ColorArgs a;
   int64_t base;  // first row of the image in the batch
@@ -377,24 +378,45 @@ __device__ __forceinline__ int find_img(const I* imgs, int n, int64_t k) {
   return lo;
 }
 
-__global__ void __launch_bounds__(128) jpeg_idct_batch_kernel(const IdctImg* imgs, int nimg, int64_t total) {
+// Thread j of a block's 8-thread group loads coefficient row j and quant row
+// j as two 16-byte vectors, dequantises in int32 (|coef| < 2^15, q < 2^16:
+// exact), and the group transposes through shared memory for the column
+// pass; the image comes from a binary search over the compact `bases`.
+__global__ void __launch_bounds__(128) jpeg_idct_batch_kernel(const IdctImg* imgs, const int64_t* bases, int nimg,
+                                                              int64_t total) {
+  __shared__ int32_t rows[16][8][9];
   __shared__ int64_t ws[16][8][9];
   const int g = threadIdx.x >> 3, j = threadIdx.x & 7;
+  const uint32_t mask = 0xFFu << (threadIdx.x & 24);
   const int64_t gb = (int64_t)blockIdx.x * 16 + g;
   if (gb >= total) return;  // whole 8-thread groups exit together
-  const int im = find_img(imgs, nimg, gb);
-  const IdctArgs& a = imgs[im].a;
-  const int64_t blk = gb - imgs[im].base;
+  int lo = 0, hi = nimg - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (__ldg(bases + mid) <= gb) lo = mid;
+    else hi = mid - 1;
+  }
+  const IdctArgs& a = imgs[lo].a;
+  const int64_t blk = gb - __ldg(bases + lo);
   int c = 0;
   while (c + 1 < a.ncomp && blk >= a.first_block[c + 1]) ++c;
   const int64_t lb = blk - a.first_block[c];
   const int16_t* co = reinterpret_cast<const int16_t*>(a.coeffs) + a.coef_offset[c] + 64 * lb;
+  const uint4 cr = __ldg(reinterpret_cast<const uint4*>(co + 8 * j));
+  const uint4 qr = *reinterpret_cast<const uint4*>(&a.qt[c][8 * j]);
+  const uint32_t cw[4] = {cr.x, cr.y, cr.z, cr.w}, qw[4] = {qr.x, qr.y, qr.z, qr.w};
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    rows[g][j][2 * k] = (int32_t)(int16_t)(cw[k] & 0xFFFF) * (int32_t)(qw[k] & 0xFFFF);
+    rows[g][j][2 * k + 1] = ((int32_t)cw[k] >> 16) * (int32_t)(qw[k] >> 16);
+  }
+  __syncwarp(mask);
   int64_t s[8];
 #pragma unroll
-  for (int k = 0; k < 8; ++k) s[k] = (int64_t)co[8 * k + j] * (int64_t)a.qt[c][8 * k + j];
+  for (int k = 0; k < 8; ++k) s[k] = rows[g][k][j];
   const int64_t by = lb / a.bw[c], bx = lb - by * a.bw[c];
   uint8_t* dst = a.planes + a.plane_offset[c] + (by * 8 + j) * (int64_t)a.bw[c] * 8 + bx * 8;
-  idct_rows_store(s, ws, g, j, 0xFFu << (threadIdx.x & 24), dst);
+  idct_rows_store(s, ws, g, j, mask, dst);
 }
 
 __global__ void __launch_bounds__(256) jpeg_color_batch_kernel(const ColorImg* imgs, int nimg) {
@@ -533,14 +555,19 @@ int reconstruct_batch(int n, const FvJpegInfo* const* fs, const int16_t* const* 
   }
   if ((blocks + 15) / 16 > 0x7FFFFFFF || rows > 0x7FFFFFFF)
     return set_error(FV_EINVAL, "fv_jpeg_reconstruct: batch too large");
+  std::vector<int64_t> bases(n);
+  for (int i = 0; i < n; ++i) bases[i] = ii[i].base;
   IdctImg* di = nullptr;
   ColorImg* dc = nullptr;
+  int64_t* db = nullptr;
   if (cudaMallocAsync(reinterpret_cast<void**>(&di), n * sizeof(IdctImg), st) != cudaSuccess ||
-      cudaMallocAsync(reinterpret_cast<void**>(&dc), n * sizeof(ColorImg), st) != cudaSuccess)
+      cudaMallocAsync(reinterpret_cast<void**>(&dc), n * sizeof(ColorImg), st) != cudaSuccess ||
+      cudaMallocAsync(reinterpret_cast<void**>(&db), n * sizeof(int64_t), st) != cudaSuccess)
     return set_error(FV_ECUDA, "fv_jpeg_reconstruct: argument buffers");
   cudaMemcpyAsync(di, ii.data(), n * sizeof(IdctImg), cudaMemcpyHostToDevice, st);
   cudaMemcpyAsync(dc, ci.data(), n * sizeof(ColorImg), cudaMemcpyHostToDevice, st);
-  jpeg_idct_batch_kernel<<<(unsigned)((blocks + 15) / 16), 128, 0, st>>>(di, n, blocks);
+  cudaMemcpyAsync(db, bases.data(), n * sizeof(int64_t), cudaMemcpyHostToDevice, st);
+  jpeg_idct_batch_kernel<<<(unsigned)((blocks + 15) / 16), 128, 0, st>>>(di, db, n, blocks);
   int rc = check_launch("jpeg_idct_batch_kernel");
   if (!rc) {
     jpeg_color_batch_kernel<<<(unsigned)rows, 256, 0, st>>>(dc, n);
@@ -548,6 +575,7 @@ int reconstruct_batch(int n, const FvJpegInfo* const* fs, const int16_t* const* 
   }
   cudaFreeAsync(di, st);
   cudaFreeAsync(dc, st);
+  cudaFreeAsync(db, st);
   return rc;
 }
 
