@@ -246,8 +246,10 @@ void fv_jpeg_batch_free(void* handle);
 void fv_set_resize_path(int32_t mode);
 
 /* Affine warp kernel selection: 0 = auto (default: the SMEM-staged tile
- * kernel when rows are 16-byte aligned, with direct gathers for tiles whose
- * source box exceeds the staging budget), 1 = always the direct-gather
+ * kernel when rows are 16-byte aligned -- the source window loaded by one
+ * TMA tensor copy per tile, or by per-row bulk copies when no tensor map can
+ * be encoded -- with direct gathers for tiles whose source box exceeds the
+ * window), 1 = always the direct-gather kernel, 2 = the bulk-copy tile
  * kernel. Perspective warps always gather directly. */
 void fv_set_warp_path(int32_t mode);
 

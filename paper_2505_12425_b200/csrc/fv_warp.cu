@@ -12,6 +12,10 @@
 //     source reads the border value; blend in imgproc.py:118-123 order;
 //   * u8 images use the _resize_u8 recipe (app.py:64-78).
 // Output is bit-identical to the oracle.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+#include <mutex>
+
 #include "fv_common.cuh"
 
 namespace fv {
@@ -447,6 +451,127 @@ __global__ void __launch_bounds__(8 * TH, 128 / TH) warp_affine_tile_kernel(cons
   }
 }
 
+// ---------------------------------------------------------------------------
+// Affine, TMA-tensor staged: the same 32 x 16 tiles and gathers as
+// warp_affine_tile_kernel, but the source box is a FIXED 48 x 40 pixel
+// window loaded by ONE 3-D tensor copy (image, row, element) issued by thread
+// 0 -- no per-row copies serialised on warp 0 -- with the TMA's zero fill for
+// coordinates outside the image (taps there read the border anyway). Tiles
+// whose box exceeds the window take the direct gathers.
+// ---------------------------------------------------------------------------
+constexpr int TBH = 40;  // window rows
+// window width in ELEMENTS (a 16-byte multiple, <= 256); the window starts at
+// the box's first element rounded down to 16 bytes (the TMA faults on an
+// unaligned innermost start coordinate: tools/probe/tma_probe.cu)
+template <typename InT, int C>
+constexpr int tma_win_elems() {
+  return sizeof(InT) == 4 ? 48 * C : (C == 3 ? 192 : (C == 4 ? 256 : 64));
+}
+
+template <typename InT, int C>
+__global__ void __launch_bounds__(128, 8) warp_affine_tma_kernel(const __grid_constant__ CUtensorMap tmap,
+                                                                 const __grid_constant__ WarpArgs a,
+                                                                 const __grid_constant__ WarpMats mats) {
+  constexpr int PB = C * (int)sizeof(InT);
+  constexpr int ES = (int)sizeof(InT);
+  constexpr int TH = 16, RS = TH / 4;
+  constexpr int TBE = tma_win_elems<InT, C>();  // window row, elements
+  constexpr int AL = 16 / ES;                   // start alignment, elements
+  extern __shared__ __align__(128) uint8_t smem[];
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem);
+  int* box = reinterpret_cast<int*>(smem + 16);  // ex0 (window's first element), by0, staged
+  uint8_t* stage = smem + 128;
+  const int n = blockIdx.z;
+  const int lx = threadIdx.x, ly = threadIdx.y;
+  const int tx0 = blockIdx.x * AT, ty0 = blockIdx.y * TH;
+  double m[9];
+#pragma unroll
+  for (int i = 0; i < 6; ++i) m[i] = mats.m[n][i];
+  m[6] = m[7] = m[8] = 0.0;
+  if (lx == 0 && ly == 0) {
+    double xlo = 0, xhi = 0, ylo = 0, yhi = 0;
+    bool fin = true;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const double cx = (double)((k & 1) ? min(tx0 + AT, a.dw) - 1 : tx0);
+      const double cy = (double)((k & 2) ? min(ty0 + TH, a.dh) - 1 : ty0);
+      const double sx = __dadd_rn(__dmul_rn(m[0], cx), __dadd_rn(__dmul_rn(m[1], cy), m[2]));
+      const double sy = __dadd_rn(__dmul_rn(m[3], cx), __dadd_rn(__dmul_rn(m[4], cy), m[5]));
+      fin = fin && isfinite(sx) && isfinite(sy);
+      xlo = k ? fmin(xlo, sx) : sx;
+      xhi = k ? fmax(xhi, sx) : sx;
+      ylo = k ? fmin(ylo, sy) : sy;
+      yhi = k ? fmax(yhi, sy) : sy;
+    }
+    // every in-image tap of the tile lies in [floor(lo) - 2, floor(hi) + 3]
+    fin = fin && xlo > -1e9 && xhi < 1e9 && ylo > -1e9 && yhi < 1e9;
+    const int bx0 = fin ? (int)floor(xlo) - 2 : 0, by0 = fin ? (int)floor(ylo) - 2 : 0;
+    const int e0 = bx0 * C;
+    const int ex0 = (e0 >= 0 ? e0 : e0 - (AL - 1)) / AL * AL;  // floor to the alignment
+    const bool staged = fin && ((int)floor(xhi) + 4) * C - ex0 <= TBE && (int)floor(yhi) + 3 - by0 < TBH;
+    box[0] = ex0;
+    box[1] = by0;
+    box[2] = staged;
+    if (staged) {
+      mbar_init(bar, 1);
+      fence_mbar_init();
+      mbar_expect_tx(bar, (uint32_t)(TBE * TBH * ES));
+      asm volatile(
+          "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], "
+          "[%5];" ::"r"(smem_u32(stage)),
+          "l"(reinterpret_cast<uint64_t>(&tmap)), "r"(ex0), "r"(by0), "r"(n), "r"(smem_u32(bar))
+          : "memory");
+    }
+  }
+  __syncthreads();
+  const int ex0 = box[0], by0 = box[1];
+  const bool staged = box[2] != 0;
+  const int x = tx0 + lx;
+  const uint32_t bord = sizeof(InT) == 1 ? (0x4B000000u | (uint32_t)a.border_raw) : __float_as_uint(a.border_f);
+  // element e of row y at sb + (y * TBE + e) * ES
+  const uint32_t sb = smem_u32(stage) - (uint32_t)((by0 * TBE + ex0) * ES);
+  if (staged) mbar_wait_block(bar, 0);
+  if (x >= a.dw) return;
+#pragma unroll 1
+  for (int half = 0; half < 2; ++half) {
+    const int ya = ty0 + ly + 2 * RS * half, yb = ya + RS;
+    if (ya >= a.dh) break;
+    const bool okb = yb < a.dh;
+    WarpTap t[2];
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+      const double yd = (double)((k && okb) ? yb : ya);
+      const double rx = __dadd_rn(__dmul_rn(m[1], yd), m[2]);
+      const double ry = __dadd_rn(__dmul_rn(m[4], yd), m[5]);
+      t[k] = warp_tap<false>(m, rx, ry, 0.0, x, a.sw, a.sh);
+    }
+    uint32_t v00[2][C], v01[2][C], v10[2][C], v11[2][C];
+    if (staged) {
+#pragma unroll
+      for (int k = 0; k < 2; ++k) {
+        const WarpTap& q = t[k];
+        const bool ix0 = q.x0 >= 0 && q.x0 < a.sw, ix1 = q.x0 + 1 >= 0 && q.x0 + 1 < a.sw;
+        const bool iy0 = q.y0 >= 0 && q.y0 < a.sh, iy1 = q.y0 + 1 >= 0 && q.y0 + 1 < a.sh;
+        // in-image taps lie in the window; others read the border (never the SMEM)
+        const uint32_t o = sb + (uint32_t)((q.y0 * TBE + q.x0 * C) * ES);
+#pragma unroll
+        for (int c = 0; c < C; ++c) {
+          v00[k][c] = (q.finite && iy0 && ix0) ? lds_raw<InT>(o + c * ES) : bord;
+          v01[k][c] = (q.finite && iy0 && ix1) ? lds_raw<InT>(o + PB + c * ES) : bord;
+          v10[k][c] = (q.finite && iy1 && ix0) ? lds_raw<InT>(o + TBE * ES + c * ES) : bord;
+          v11[k][c] = (q.finite && iy1 && ix1) ? lds_raw<InT>(o + TBE * ES + PB + c * ES) : bord;
+        }
+      }
+    } else {
+#pragma unroll
+      for (int k = 0; k < 2; ++k) gather_raw<InT, C>(a, n, t[k], bord, v00[k], v01[k], v10[k], v11[k]);
+    }
+    InT* da = row_ptr_mut<InT>(a.dst, a.d_is, a.d_rp, n, ya) + x * C;
+    InT* db = row_ptr_mut<InT>(a.dst, a.d_is, a.d_rp, n, okb ? yb : ya) + x * C;
+    blend_store<InT, C>(a, t, v00, v01, v10, v11, da, db, okb);
+  }
+}
+
 // Any channel count: same sampler, channel loop at run time.
 template <typename InT, bool PERSP>
 __global__ void __launch_bounds__(256) warp_kernel_any(const __grid_constant__ WarpArgs a,
@@ -483,7 +608,8 @@ __global__ void __launch_bounds__(256) warp_kernel_any(const __grid_constant__ W
   }
 }
 
-static int g_warp_path = 0;  // 0 auto, 1 direct gathers only (fv_set_warp_path)
+static int g_warp_path = 0;  // 0 auto, 1 direct gathers only, 2 bulk-copy tiles (fv_set_warp_path)
+static int g_warp_tma = 1;   // TMA-tensor tiles when available (path 0)
 
 constexpr int AT_H = 16;  // tile height of the staged affine kernel (16: 24 KB stage, 8 CTAs / SM)
 
@@ -495,6 +621,44 @@ static int launch_tile(int dw, int dh, int nb, cudaStream_t st, const WarpArgs& 
   if (ensure_smem_attr(kern, smem, attr_mask) != FV_OK) return check_launch("warp_affine_tile_kernel (smem attribute)");
   dim3 grid((dw + AT - 1) / AT, (dh + AT_H - 1) / AT_H, nb);
   kern<<<grid, dim3(32, AT_H / 4), smem, st>>>(a, mats);
+  return FV_OK;
+}
+
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no
+// libcuda link); null when unavailable (then the bulk-copy tile kernel runs)
+static PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
+  static std::once_flag once;
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  });
+  return fn;
+}
+
+// 0 = launched, 1 = no tensor map (caller falls back), else error
+template <typename InT, int C>
+static int launch_tma(int dw, int dh, int nb, cudaStream_t st, const WarpArgs& a, const WarpMats& mats) {
+  auto enc = tensor_map_encoder();
+  if (!enc) return 1;
+  CUtensorMap tm;
+  const cuuint64_t dims[3] = {(cuuint64_t)a.sw * C, (cuuint64_t)a.sh, (cuuint64_t)nb};
+  const cuuint64_t strides[2] = {(cuuint64_t)a.s_rp, (cuuint64_t)(nb > 1 ? a.s_is : a.s_rp * a.sh)};
+  const cuuint32_t boxd[3] = {(cuuint32_t)tma_win_elems<InT, C>(), (cuuint32_t)TBH, 1};
+  const cuuint32_t estr[3] = {1, 1, 1};
+  if (enc(&tm, sizeof(InT) == 1 ? CU_TENSOR_MAP_DATA_TYPE_UINT8 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3,
+          const_cast<void*>(a.src), dims, strides, boxd, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+          CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+    return 1;
+  auto kern = warp_affine_tma_kernel<InT, C>;
+  const int smem = 128 + tma_win_elems<InT, C>() * TBH * (int)sizeof(InT);
+  static unsigned long long attr_mask[2] = {0, 0};  // per instantiation
+  if (ensure_smem_attr(kern, smem, attr_mask) != FV_OK) return check_launch("warp_affine_tma_kernel (smem attribute)");
+  dim3 grid((dw + AT - 1) / AT, (dh + 15) / 16, nb);
+  kern<<<grid, dim3(32, 4), smem, st>>>(tm, a, mats);  // the tensor map first: 64-byte aligned at offset 0
   return FV_OK;
 }
 
@@ -538,11 +702,20 @@ static int launch_warp(const InT* src, int64_t s_is, int64_t s_rp, int sh, int s
     const bool rows16 = (reinterpret_cast<uintptr_t>(a.src) & 15) == 0 && (s_rp & 15) == 0 &&
                         (nb == 1 || (s_is & 15) == 0) && ((pb * sw) & 15) == 0;
     if (!PERSP && g_warp_path == 0 && rows16 && (c == 1 || c == 3 || c == 4)) {
-      int rc = FV_OK;
-      switch (c) {
-        case 1: rc = launch_tile<InT, 1>(dw, dh, nb, st, a, mats); break;
-        case 3: rc = launch_tile<InT, 3>(dw, dh, nb, st, a, mats); break;
-        default: rc = launch_tile<InT, 4>(dw, dh, nb, st, a, mats); break;
+      int rc = 1;
+      if (g_warp_tma) {
+        switch (c) {
+          case 1: rc = launch_tma<InT, 1>(dw, dh, nb, st, a, mats); break;
+          case 3: rc = launch_tma<InT, 3>(dw, dh, nb, st, a, mats); break;
+          default: rc = launch_tma<InT, 4>(dw, dh, nb, st, a, mats); break;
+        }
+      }
+      if (rc == 1) {  // no tensor map: the bulk-copy staged kernel
+        switch (c) {
+          case 1: rc = launch_tile<InT, 1>(dw, dh, nb, st, a, mats); break;
+          case 3: rc = launch_tile<InT, 3>(dw, dh, nb, st, a, mats); break;
+          default: rc = launch_tile<InT, 4>(dw, dh, nb, st, a, mats); break;
+        }
       }
       if (rc) return rc;
       rc = check_launch(fn);
@@ -567,7 +740,10 @@ using namespace fv;
 
 extern "C" {
 
-void fv_set_warp_path(int32_t mode) { g_warp_path = mode; }
+void fv_set_warp_path(int32_t mode) {
+  g_warp_path = mode == 2 ? 0 : mode;
+  g_warp_tma = mode == 2 ? 0 : 1;
+}
 
 int fv_warp_affine_f32(const float* src, int64_t s_is, int64_t s_rp, int32_t sh, int32_t sw, float* dst,
                        int64_t d_is, int64_t d_rp, int32_t dh, int32_t dw, int32_t c, int32_t n,

@@ -235,7 +235,7 @@ class TestFused:
 # a8 / a9 warps
 # ---------------------------------------------------------------------------
 
-@pytest.fixture(params=[0, 1], ids=["tile", "direct"])
+@pytest.fixture(params=[0, 1, 2], ids=["tma_tile", "direct", "bulk_tile"])
 def warp_path(request):
     _native.lib().fv_set_warp_path(request.param)
     yield request.param
