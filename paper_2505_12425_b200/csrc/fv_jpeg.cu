@@ -164,47 +164,6 @@ struct ColorArgs {
   int64_t d_rp;
 };
 
-__device__ __forceinline__ int px(const uint8_t* p, int64_t pitch, int r, int c) { return p[r * pitch + c]; }
-
-// Horizontal x2 triangle (jpeg.py:809-821) at output column X of row r
-__device__ __forceinline__ int up_h2(const uint8_t* p, int64_t pitch, int r, int X, int m) {
-  if (m <= 2) return px(p, pitch, r, X >> 1);
-  const int jj = X >> 1;
-  if (X == 0) return px(p, pitch, r, 0);
-  if (X == 2 * m - 1) return px(p, pitch, r, m - 1);
-  if ((X & 1) == 0) return (3 * px(p, pitch, r, jj) + px(p, pitch, r, jj - 1) + 1) >> 2;
-  return (3 * px(p, pitch, r, jj) + px(p, pitch, r, jj + 1) + 2) >> 2;
-}
-// Vertical x2 (the reference transposes and reuses h2)
-__device__ __forceinline__ int up_v2(const uint8_t* p, int64_t pitch, int Y, int c, int m) {
-  if (m <= 2) return px(p, pitch, Y >> 1, c);
-  const int jj = Y >> 1;
-  if (Y == 0) return px(p, pitch, 0, c);
-  if (Y == 2 * m - 1) return px(p, pitch, m - 1, c);
-  if ((Y & 1) == 0) return (3 * px(p, pitch, jj, c) + px(p, pitch, jj - 1, c) + 1) >> 2;
-  return (3 * px(p, pitch, jj, c) + px(p, pitch, jj + 1, c) + 2) >> 2;
-}
-// 2x2 triangle (jpeg.py:824-841): 3:1 column sums, then 3:1 across, +8/+7
-__device__ __forceinline__ int up_h2v2(const uint8_t* p, int64_t pitch, int Y, int X, int mw, int mh) {
-  if (mw <= 2) return px(p, pitch, Y >> 1, X >> 1);
-  const int r = Y >> 1;
-  const int r2 = (Y & 1) ? min(r + 1, mh - 1) : max(r - 1, 0);
-  auto cs = [&](int c) { return 3 * px(p, pitch, r, c) + px(p, pitch, r2, c); };
-  const int jj = X >> 1;
-  if (X == 0) return (cs(0) * 4 + 8) >> 4;
-  if (X == 2 * mw - 1) return (cs(mw - 1) * 4 + 7) >> 4;
-  if ((X & 1) == 0) return (3 * cs(jj) + cs(jj - 1) + 8) >> 4;
-  return (3 * cs(jj) + cs(jj + 1) + 7) >> 4;
-}
-
-__device__ __forceinline__ int sample(const ColorArgs& a, int e, int x, int y) {
-  const uint8_t* p = a.plane[e];
-  const int64_t pt = a.pitch[e];
-  if (a.fh[e] == 2 && a.fv[e] == 2) return up_h2v2(p, pt, y, x, a.cw[e], a.ch[e]);
-  if (a.fh[e] == 2) return up_h2(p, pt, y, x, a.cw[e]);
-  if (a.fv[e] == 2) return up_v2(p, pt, y, x, a.ch[e]);
-  return px(p, pt, y, x);
-}
 
 __device__ __forceinline__ uint8_t clamp255(int v) { return (uint8_t)(v < 0 ? 0 : (v > 255 ? 255 : v)); }
 
