@@ -246,8 +246,51 @@ __global__ void __launch_bounds__(256, 4) warp_kernel(const __grid_constant__ Wa
   // WARP_ROWS rows per thread (stride 8): the per-warp setup (matrix, params,
   // indices) is amortised over 64 x WARP_ROWS pixels
   const int y_end = min(blockIdx.y * 8 * WARP_ROWS + 8 * WARP_ROWS, a.dh);
+  const int y_first = blockIdx.y * 8 * WARP_ROWS + threadIdx.y;
+  if (PERSP && a.zero_border && y_first < y_end) {
+    // Whole-warp early out: lanes 0-3 map the corners of the warp's region
+    // (64 columns x its rows). With W of one strict sign at all four corners
+    // (W is linear: no zero inside) the region maps onto the convex
+    // quadrilateral of the mapped corners; if all four lie beyond the same
+    // side of the source (margin 2 px + 1e-6 relative, far above the f64
+    // rounding of the per-pixel map), every tap of every pixel is outside and
+    // the output is exactly +0 -- no per-pixel coordinate work.
+    const unsigned am = __activemask();
+    const int lane = threadIdx.x;
+    const int y_last = y_first + 8 * ((y_end - 1 - y_first) / 8);
+    int bits = 0;
+    if (lane < 4) {
+      const double cx = (double)((lane & 1) ? min((int)blockIdx.x * 64 + 63, a.dw - 1) : (int)blockIdx.x * 64);
+      const double cy = (double)((lane & 2) ? y_last : y_first);
+      const double X = m[0] * cx + m[1] * cy + m[2], Y = m[3] * cx + m[4] * cy + m[5];
+      const double W = m[6] * cx + m[7] * cy + m[8];
+      const double sx = X / W, sy = Y / W;
+      const double mx = 2.0 + 1e-6 * fabs(sx), my = 2.0 + 1e-6 * fabs(sy);
+      if (isfinite(sx) && isfinite(sy)) {
+        bits |= (sx < -1.0 - mx) ? 1 : 0;
+        bits |= (sx > (double)a.sw + mx) ? 2 : 0;
+        bits |= (sy < -1.0 - my) ? 4 : 0;
+        bits |= (sy > (double)a.sh + my) ? 8 : 0;
+      }
+      bits |= W > 0.0 ? 16 : (W < 0.0 ? 32 : 0);
+    }
+    const int all = __shfl_sync(am, bits, 0) & __shfl_sync(am, bits, 1) & __shfl_sync(am, bits, 2) &
+                    __shfl_sync(am, bits, 3);
+    if ((all & 48) && (all & 15)) {
 #pragma unroll 1
-  for (int y = blockIdx.y * 8 * WARP_ROWS + threadIdx.y; y < y_end; y += 8) {
+      for (int y = y_first; y < y_end; y += 8) {
+        InT* d = row_ptr_mut<InT>(a.dst, a.d_is, a.d_rp, n, y) + x * C;
+#pragma unroll
+        for (int c = 0; c < C; ++c) {
+          d[c] = (InT)0;
+          if (two) d[32 * C + c] = (InT)0;
+        }
+      }
+      return;
+    }
+  }
+#pragma unroll 1
+  for (int y = y_first; y < y_end; y += 8) {
     const double yd = (double)y;
     const double rx = __dadd_rn(__dmul_rn(m[1], yd), m[2]);
     const double ry = __dadd_rn(__dmul_rn(m[4], yd), m[5]);
