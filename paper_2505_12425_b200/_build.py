@@ -3,6 +3,8 @@
 The library is built IN-TREE (git-ignored, but it travels to the GPU box with
 the gpurun snapshot). Rebuilds only when a source or header is newer than the
 library. `python -m paper_2505_12425_b200._build [--force] [--ptxas-v]`.
+FV_NVCC_EXTRA (space-separated nvcc flags, e.g. -D overrides of tuning
+constants) is for A/B experiments only; combine it with --force.
 """
 from __future__ import annotations
 
@@ -19,7 +21,8 @@ LIB = os.path.join(LIBDIR, "libfovea_b200.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
-FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O2", "--expt-relaxed-constexpr"]
+FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O2", "--expt-relaxed-constexpr",
+         *os.environ.get("FV_NVCC_EXTRA", "").split()]
 
 
 def sources() -> list[str]:

@@ -341,26 +341,39 @@ __device__ __forceinline__ int find_img(const I* imgs, int n, int64_t k) {
 // j as two 16-byte vectors, dequantises in int32 (|coef| < 2^15, q < 2^16:
 // exact), and the group transposes through shared memory for the column
 // pass; the image comes from a binary search over the compact `bases`.
+// Each pass runs in int32 when every input of the WARP (4 blocks) is within
+// kIdct32Max (a warp-uniform vote: no divergence), else in int64 -- the
+// same integers either way (see idct8). After an int32 first pass the
+// intermediate fits int32 (|o| <= 61214 * 12000 < 2^30), so only the
+// second pass may need int64.
+__device__ __forceinline__ bool idct_small(const int32_t (&s)[8]) {
+  bool ok = true;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) ok = ok && (uint32_t)(s[k] + (int32_t)kIdct32Max) <= (uint32_t)(2 * kIdct32Max);
+  return __all_sync(0xFFFFFFFFu, ok);
+}
+
 __global__ void __launch_bounds__(128) jpeg_idct_batch_kernel(const IdctImg* imgs, const int64_t* bases, int nimg,
                                                               int64_t total) {
   __shared__ int32_t rows[16][8][9];
+  __shared__ int32_t mid[16][8][9];
   __shared__ int64_t ws[16][8][9];
   const int g = threadIdx.x >> 3, j = threadIdx.x & 7;
-  const uint32_t mask = 0xFFu << (threadIdx.x & 24);
-  const int64_t gb = (int64_t)blockIdx.x * 16 + g;
-  if (gb >= total) return;  // whole 8-thread groups exit together
+  const int64_t gb0 = (int64_t)blockIdx.x * 16 + g;
+  const bool live = gb0 < total;
+  const int64_t gb = live ? gb0 : total - 1;  // the whole warp stays for the votes; dead groups do not store
   int lo = 0, hi = nimg - 1;
   while (lo < hi) {
-    const int mid = (lo + hi + 1) >> 1;
-    if (__ldg(bases + mid) <= gb) lo = mid;
-    else hi = mid - 1;
+    const int m = (lo + hi + 1) >> 1;
+    if (__ldg(bases + m) <= gb) lo = m;
+    else hi = m - 1;
   }
   const IdctArgs& a = imgs[lo].a;
   const int64_t blk = gb - __ldg(bases + lo);
   int c = 0;
   while (c + 1 < a.ncomp && blk >= a.first_block[c + 1]) ++c;
-  const int64_t lb = blk - a.first_block[c];
-  const int16_t* co = reinterpret_cast<const int16_t*>(a.coeffs) + a.coef_offset[c] + 64 * lb;
+  const uint32_t lb = (uint32_t)(blk - a.first_block[c]);  // < 2^31 blocks per image
+  const int16_t* co = reinterpret_cast<const int16_t*>(a.coeffs) + a.coef_offset[c] + 64 * (int64_t)lb;
   const uint4 cr = __ldg(reinterpret_cast<const uint4*>(co + 8 * j));
   const uint4 qr = *reinterpret_cast<const uint4*>(&a.qt[c][8 * j]);
   const uint32_t cw[4] = {cr.x, cr.y, cr.z, cr.w}, qw[4] = {qr.x, qr.y, qr.z, qr.w};
@@ -369,13 +382,62 @@ __global__ void __launch_bounds__(128) jpeg_idct_batch_kernel(const IdctImg* img
     rows[g][j][2 * k] = (int32_t)(int16_t)(cw[k] & 0xFFFF) * (int32_t)(qw[k] & 0xFFFF);
     rows[g][j][2 * k + 1] = ((int32_t)cw[k] >> 16) * (int32_t)(qw[k] >> 16);
   }
-  __syncwarp(mask);
-  int64_t s[8];
+  __syncwarp();
+  const uint32_t bw = (uint32_t)a.bw[c], by = lb / bw, bx = lb - by * bw;
+  uint8_t* dst = a.planes + a.plane_offset[c] + ((int64_t)by * 8 + j) * (int64_t)bw * 8 + (int64_t)bx * 8;
+  int32_t s[8];
 #pragma unroll
   for (int k = 0; k < 8; ++k) s[k] = rows[g][k][j];
-  const int64_t by = lb / a.bw[c], bx = lb - by * a.bw[c];
-  uint8_t* dst = a.planes + a.plane_offset[c] + (by * 8 + j) * (int64_t)a.bw[c] * 8 + bx * 8;
-  idct_rows_store(s, ws, g, j, mask, dst);
+  if (!idct_small(s)) {  // generic int64 path (crafted magnitudes)
+    int64_t t[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) t[k] = s[k];
+    int64_t o[8];
+    idct8_exact(t, o);
+#pragma unroll
+    for (int k = 0; k < 8; ++k) ws[g][k][j] = (o[k] + (1 << 10)) >> 11;
+    __syncwarp();
+#pragma unroll
+    for (int k = 0; k < 8; ++k) t[k] = ws[g][j][k];
+    idct8_exact(t, o);
+    uint32_t w[2] = {0, 0};
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      int64_t v = ((o[k] + (1 << 17)) >> 18) + 128;
+      v = v < 0 ? 0 : (v > 255 ? 255 : v);
+      w[k >> 2] |= (uint32_t)v << (8 * (k & 3));
+    }
+    if (live) *reinterpret_cast<uint2*>(dst) = make_uint2(w[0], w[1]);
+    return;
+  }
+  int32_t o[8];
+  idct8<int32_t>(s, o);
+#pragma unroll
+  for (int k = 0; k < 8; ++k) mid[g][k][j] = (o[k] + (1 << 10)) >> 11;
+  __syncwarp();
+#pragma unroll
+  for (int k = 0; k < 8; ++k) s[k] = mid[g][j][k];
+  uint32_t w[2] = {0, 0};
+  if (idct_small(s)) {
+    idct8<int32_t>(s, o);
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const int32_t v = min(max(((o[k] + (1 << 17)) >> 18) + 128, 0), 255);
+      w[k >> 2] |= (uint32_t)v << (8 * (k & 3));
+    }
+  } else {
+    int64_t t[8], q[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) t[k] = s[k];
+    idct8<int64_t>(t, q);
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      int64_t v = ((q[k] + (1 << 17)) >> 18) + 128;
+      v = v < 0 ? 0 : (v > 255 ? 255 : v);
+      w[k >> 2] |= (uint32_t)v << (8 * (k & 3));
+    }
+  }
+  if (live) *reinterpret_cast<uint2*>(dst) = make_uint2(w[0], w[1]);
 }
 
 __global__ void __launch_bounds__(256) jpeg_color_batch_kernel(const ColorImg* imgs, int nimg) {
@@ -481,6 +543,14 @@ int reconstruct(const FvJpegInfo& f, const void* coeffs, int32_t coef_bytes, uin
                 int64_t dst_row_pitch, cudaStream_t st) {
   int rc = check_recon(f, planes, dst_row_pitch);
   if (rc) return rc;
+  if (coef_bytes == 2 && (reinterpret_cast<uintptr_t>(coeffs) & 15) == 0) {  // the batch kernels, n = 1
+    const FvJpegInfo* fs[1] = {&f};
+    const int16_t* cs[1] = {static_cast<const int16_t*>(coeffs)};
+    uint8_t* ps[1] = {planes};
+    uint8_t* ds[1] = {dst};
+    const int64_t dp[1] = {dst_row_pitch};
+    return reconstruct_batch(1, fs, cs, ps, ds, dp, st);
+  }
   IdctArgs ia;
   const int64_t nb = make_idct_args(f, coeffs, planes, ia);
   const int64_t grid = (nb + 15) / 16;
@@ -521,8 +591,11 @@ int reconstruct_batch(int n, const FvJpegInfo* const* fs, const int16_t* const* 
   int64_t* db = nullptr;
   if (cudaMallocAsync(reinterpret_cast<void**>(&di), n * sizeof(IdctImg), st) != cudaSuccess ||
       cudaMallocAsync(reinterpret_cast<void**>(&dc), n * sizeof(ColorImg), st) != cudaSuccess ||
-      cudaMallocAsync(reinterpret_cast<void**>(&db), n * sizeof(int64_t), st) != cudaSuccess)
+      cudaMallocAsync(reinterpret_cast<void**>(&db), n * sizeof(int64_t), st) != cudaSuccess) {
+    for (void* q : {(void*)di, (void*)dc, (void*)db})
+      if (q) cudaFreeAsync(q, st);
     return set_error(FV_ECUDA, "fv_jpeg_reconstruct: argument buffers");
+  }
   cudaMemcpyAsync(di, ii.data(), n * sizeof(IdctImg), cudaMemcpyHostToDevice, st);
   cudaMemcpyAsync(dc, ci.data(), n * sizeof(ColorImg), cudaMemcpyHostToDevice, st);
   cudaMemcpyAsync(db, bases.data(), n * sizeof(int64_t), cudaMemcpyHostToDevice, st);

@@ -34,9 +34,22 @@ constexpr int kSubBits = 1024;
 constexpr int kMaxSlots = 12;
 constexpr int kSyncRounds = 6;    // rounds per chunk (one 4-byte readback per chunk)
 constexpr int kSyncChunks = 32;   // cap: images still changing after this fall back
-constexpr int kChain = 8;         // subsequences one thread may carry a changed state through per round
-constexpr int kChain0 = 8;        // ... in the first (full) round
-constexpr int kWarm = 1;          // speculative pass: subsequences decoded before a thread's own, to synchronise
+// tuning constants (overridable with -D for A/B builds)
+#ifndef FV_JPEG_CHAIN
+#define FV_JPEG_CHAIN 8
+#endif
+#ifndef FV_JPEG_CHAIN0
+#define FV_JPEG_CHAIN0 8
+#endif
+#ifndef FV_JPEG_WARM_BITS
+#define FV_JPEG_WARM_BITS 1024
+#endif
+#ifndef FV_JPEG_CP_BITS
+#define FV_JPEG_CP_BITS 64
+#endif
+constexpr int kChain = FV_JPEG_CHAIN;    // subsequences one thread may carry a changed state through per round
+constexpr int kChain0 = FV_JPEG_CHAIN0;  // ... in the first (full) round
+constexpr int kWarmBits = FV_JPEG_WARM_BITS;  // speculative pass: bits decoded before a thread's own, to synchronise
 
 __constant__ int kZigzagDev[64] = {0,  1,  8,  16, 9,  2,  3,  10, 17, 24, 32, 25, 18, 11, 4,  5,
                                    12, 19, 26, 33, 40, 48, 41, 34, 27, 20, 13, 6,  7,  14, 21, 28,
@@ -54,6 +67,7 @@ struct DevHuff {
 struct DevImg {
   DevHuff dc[3], ac[3];  // per scan entry
   int8_t slot_e[kMaxSlots], slot_bx[kMaxSlots], slot_by[kMaxSlots];
+  uint32_t slot_e2;  // slot_e packed, 2 bits per slot
   int32_t nslots, mcus_x;
   int32_t h[3], v[3], bw[3];
   int64_t coef_offset[3];  // within the image's dense int32 region
@@ -81,33 +95,39 @@ __device__ __forceinline__ void unpack_state(uint64_t s, int64_t& pos, int& slot
 
 // MSB-first reader over one unstuffed segment (16-byte aligned, zero padded
 // to a multiple of 16 bytes in the batch buffer): refills 32 bits at a time
-// from aligned words; words past the segment read as zero.
+// from aligned words; words past the segment read as zero. The next word is
+// loaded one refill ahead, so its latency overlaps the symbols decoded from
+// the current ones (a lone thread's decode in the sync rounds is
+// latency-bound).
 struct DBits {
   const uint32_t* w;  // the segment's words
   int64_t nw;         // words holding data (the rest of the segment's padding reads as zero too)
-  int64_t cur;        // next word to load
+  int64_t cur;        // index of `nxt`
   uint64_t acc;
+  uint32_t nxt;
   int nb;
   __device__ __forceinline__ void init(const uint8_t* seg, int64_t nbytes) {
     w = reinterpret_cast<const uint32_t*>(seg);
     nw = (nbytes + 3) >> 2;
   }
+  __device__ __forceinline__ uint32_t word(int64_t i) const {
+    return i < nw ? __byte_perm(__ldg(w + i), 0, 0x0123) : 0u;
+  }
+  // after fill(): at least 33 bits buffered (a symbol takes at most 16 + 15)
   __device__ __forceinline__ void fill() {
-    while (nb <= 32) {
-      const uint32_t x = cur < nw ? __byte_perm(__ldg(w + cur), 0, 0x0123) : 0u;
-      acc |= (uint64_t)x << (32 - nb);
+    if (nb <= 32) {
+      acc |= (uint64_t)nxt << (32 - nb);
       nb += 32;
-      ++cur;
+      nxt = word(++cur);
     }
   }
   __device__ __forceinline__ void start(int64_t bit) {
-    cur = bit >> 5;
-    acc = 0;
-    nb = 0;
-    fill();
-    acc <<= (bit & 31);
-    nb -= (int)(bit & 31);
-    fill();
+    const int64_t c = bit >> 5;
+    const int off = (int)(bit & 31);
+    acc = (((uint64_t)word(c) << 32) | word(c + 1)) << off;
+    nb = 64 - off;
+    cur = c + 2;
+    nxt = word(cur);
   }
   __device__ __forceinline__ uint32_t peek(int k) const { return (uint32_t)(acc >> (64 - k)); }
   __device__ __forceinline__ void skip(int k) {
@@ -139,14 +159,56 @@ __device__ __forceinline__ int32_t dextend(uint32_t v, int size) {
 
 enum { kModeSync = 0, kModeCount = 1, kModeWrite = 2 };
 
+// Checkpoints of the speculative decode: its state (and the blocks it started
+// so far) at the first symbol boundary at or past each mark start + k*kCpBits
+// of its own subsequence. A later decode of the same subsequence that reaches
+// a mark in exactly a recorded state has merged with the speculative
+// trajectory -- the decoder state is (bit position, slot, coefficient index)
+// and nothing else -- so its exit state and block count follow from the
+// speculative ones without decoding further. k = 0 is the subsequence entry:
+// a synchronised subsequence costs one compare in the rounds.
+constexpr int kCpBits = FV_JPEG_CP_BITS;
+constexpr int kCp = kSubBits / kCpBits;
+constexpr uint64_t kNoState = ~0ull;  // an unrecorded checkpoint (never equals a real state)
+enum { kCpNone = 0, kCpRecord = 1, kCpMatch = 2 };
+
+struct Ckpt {
+  uint64_t* st;    // [kCp][nsub] states
+  int32_t* n;      // [kCp][nsub] block starts before the checkpoint (speculative decode)
+  int64_t nsub, t;
+  int64_t mark;    // next mark (bit position)
+  int k;           // next checkpoint index
+  int hit;         // match mode: the checkpoint matched, or -1
+};
+
+// Destination of block `cb` (decode order) of segment `sg`, or nullptr for a
+// block outside the segment (a desynchronised decode can run past it).
+// Block indices of an image stay below 2^31 (65535^2 / 64 * 3).
+__device__ __forceinline__ int16_t* block_dst(const DevImg& im, const DevSeg& sg, int64_t cb, int16_t* coef) {
+  if (cb < sg.first_block || cb >= sg.first_block + sg.nblocks) return nullptr;
+  const uint32_t c = (uint32_t)cb, ns = (uint32_t)im.nslots;
+  const uint32_t mcu = c / ns, s = c - mcu * ns;
+  const int e = im.slot_e[s];
+  const uint32_t my = mcu / (uint32_t)im.mcus_x, mx = mcu - my * (uint32_t)im.mcus_x;
+  const int64_t r = ((int64_t)my * im.v[e] + im.slot_by[s]) * im.bw[e] + (int64_t)mx * im.h[e] + im.slot_bx[s];
+  return coef + im.coef_base + im.coef_offset[e] + 64 * r;
+}
+
 // Decode symbols starting before `end_bit` (write mode on the segment's last
 // subsequence: until the segment's last block is complete). Anomalies on the
 // true path (write mode, blocks of the segment) set *bad; elsewhere the
 // decoder steps on deterministically (skip a bit / end the block).
-template <int MODE>
+// Write mode: `zz` is the zigzag table (shared memory), the destination is
+// resolved once per block.
+template <int MODE, int CPM = kCpNone>
 __device__ uint64_t decode_run(const DevImg& im, DBits& b, int slot, int z, int64_t end_bit, bool last_sub,
-                               int64_t blk, const DevSeg& sg, int16_t* coef, int* nstart, int* bad) {
+                               int64_t blk, const DevSeg& sg, int16_t* coef, int* nstart, int* bad,
+                               Ckpt* ck = nullptr, const uint8_t* zz = nullptr) {
   const int64_t limit = sg.first_block + sg.nblocks;
+  const uint32_t slot_e = im.slot_e2;  // 2 bits per slot
+  const int nslots = im.nslots;
+  int16_t* dst = nullptr;
+  if (MODE == kModeWrite && z != 0) dst = block_dst(im, sg, blk - 1, coef);  // entered mid-block
   for (;;) {
     const int64_t pos = b.pos();
     if (MODE == kModeWrite && last_sub) {
@@ -155,23 +217,28 @@ __device__ uint64_t decode_run(const DevImg& im, DBits& b, int slot, int z, int6
     } else if (pos >= end_bit) {
       break;
     }
-    b.fill();
-    const int e = im.slot_e[slot];
-    int16_t* dst = nullptr;
-    if (MODE == kModeWrite) {
-      const int64_t cb = z == 0 ? blk : blk - 1;  // block this symbol belongs to
-      if (cb >= sg.first_block && cb < limit) {
-        const int64_t mcu = cb / im.nslots;
-        const int s = (int)(cb - mcu * im.nslots);
-        const int ee = im.slot_e[s];
-        const int64_t my = mcu / im.mcus_x, mx = mcu - my * im.mcus_x;
-        const int64_t r = (my * im.v[ee] + im.slot_by[s]) * im.bw[ee] + mx * im.h[ee] + im.slot_bx[s];
-        dst = coef + im.coef_base + im.coef_offset[ee] + 64 * r;
+    if (CPM != kCpNone && pos >= ck->mark && ck->k < kCp) {
+      const uint64_t st = pack_state(pos, slot, z);
+      if (CPM == kCpMatch) {
+        if (ck->st[ck->k * ck->nsub + ck->t] == st) {
+          ck->hit = ck->k;
+          break;
+        }
       }
+      do {  // every mark this boundary is the first at or past
+        if (CPM == kCpRecord) {
+          ck->st[ck->k * ck->nsub + ck->t] = st;
+          ck->n[ck->k * ck->nsub + ck->t] = *nstart;
+        }
+        ++ck->k;
+        ck->mark += kCpBits;
+      } while (ck->k < kCp && pos >= ck->mark);
     }
+    b.fill();
+    const int e = (slot_e >> (2 * slot)) & 3;
     if (z == 0) {  // DC of a new block
       if (nstart) ++*nstart;
-      if (MODE == kModeWrite) ++blk;
+      if (MODE == kModeWrite) dst = block_dst(im, sg, blk++, coef);
       const DevHuff& t = im.dc[e];
       const int32_t f = t.fast[b.peek(10)];
       int32_t diff;
@@ -203,7 +270,7 @@ __device__ uint64_t decode_run(const DevImg& im, DBits& b, int slot, int z, int6
           if (MODE == kModeWrite && dst) *bad = 1;
           z = 64;
         } else {
-          if (MODE == kModeWrite && dst) dst[kZigzagDev[z]] = (int16_t)(f >> 16);
+          if (MODE == kModeWrite && dst) dst[zz[z]] = (int16_t)(f >> 16);
           ++z;
         }
       } else {
@@ -224,7 +291,7 @@ __device__ uint64_t decode_run(const DevImg& im, DBits& b, int slot, int z, int6
             } else {
               const int32_t v = dextend(b.peek(sz), sz);
               b.skip(sz);
-              if (MODE == kModeWrite && dst) dst[kZigzagDev[z]] = (int16_t)v;  // |v| < 2^15
+              if (MODE == kModeWrite && dst) dst[zz[z]] = (int16_t)v;  // |v| < 2^15
               ++z;
             }
           }
@@ -233,7 +300,7 @@ __device__ uint64_t decode_run(const DevImg& im, DBits& b, int slot, int z, int6
     }
     if (z >= 64) {  // block complete
       z = 0;
-      slot = slot + 1 == im.nslots ? 0 : slot + 1;
+      slot = slot + 1 == nslots ? 0 : slot + 1;
       if (MODE == kModeWrite && blk == limit && b.pos() > sg.bits) *bad = 1;  // consumed padding
     }
   }
@@ -261,7 +328,8 @@ __device__ __forceinline__ void sub_range(const Pass& P, int64_t t, const DevSeg
   end = min(start + (int64_t)kSubBits, sg->bits);
 }
 
-__global__ void __launch_bounds__(128) k_spec(const __grid_constant__ Pass P, uint64_t* E, int32_t* cnt) {
+__global__ void __launch_bounds__(128) k_spec(const __grid_constant__ Pass P, uint64_t* E, int32_t* cnt,
+                                              uint64_t* Es, int32_t* cp_st_n, uint64_t* cp_st, int32_t* cp_n) {
   const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= P.nsub) return;
   const DevSeg* sg;
@@ -271,16 +339,22 @@ __global__ void __launch_bounds__(128) k_spec(const __grid_constant__ Pass P, ui
   b.init(P.stream + sg->byte_off, sg->bits >> 3);
   int slot = 0, z = 0;
   int64_t pos = start;
-  if (kWarm && local > 0) {  // warm up on the preceding bits: enter this subsequence (likely) in step
-    const int64_t w0 = start > (int64_t)kWarm * kSubBits ? start - (int64_t)kWarm * kSubBits : 0;
+  if (kWarmBits > 0 && local > 0) {  // warm up on the preceding bits: enter this subsequence (likely) in step
+    const int64_t w0 = start > (int64_t)kWarmBits ? start - (int64_t)kWarmBits : 0;
     b.start(w0);
     const uint64_t e = decode_run<kModeSync>(P.imgs[sg->img], b, 0, 0, start, false, 0, *sg, nullptr, nullptr, nullptr);
     unpack_state(e, pos, slot, z);
   }
   b.start(pos);
   int n = 0;
-  E[t] = decode_run<kModeSync>(P.imgs[sg->img], b, slot, z, end, false, 0, *sg, nullptr, &n, nullptr);
+  Ckpt ck{cp_st, cp_n, P.nsub, t, start, 0, -1};
+  const uint64_t e =
+      decode_run<kModeSync, kCpRecord>(P.imgs[sg->img], b, slot, z, end, false, 0, *sg, nullptr, &n, nullptr, &ck);
+  for (int k = ck.k; k < kCp; ++k) cp_st[k * P.nsub + t] = kNoState;
+  E[t] = e;
+  Es[t] = e;
   cnt[t] = n;  // exact for each segment's first subsequence; the others are re-derived in the rounds
+  cp_st_n[t] = n;
 }
 
 // One propagation round over a work queue: for each queued subsequence t,
@@ -299,7 +373,8 @@ __device__ __forceinline__ void enqueue(int32_t* qout, int* nout, int* mark, int
 
 __global__ void __launch_bounds__(128) k_round(const __grid_constant__ Pass P, uint64_t* E, int32_t* cnt,
                                                const int32_t* qin, const int* nin, int32_t* qout, int* nout, int* mark,
-                                               int round, int all_subs, int chain) {
+                                               int round, int all_subs, int chain, const uint64_t* Es,
+                                               const int32_t* sn, uint64_t* cp_st, int32_t* cp_n) {
   const int64_t n = all_subs ? P.nsub : *nin;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     int64_t t = all_subs ? i : qin[i];
@@ -309,15 +384,26 @@ __global__ void __launch_bounds__(128) k_round(const __grid_constant__ Pass P, u
     if (local == 0) continue;
     uint64_t in = E[t - 1];
     for (int step = 0;; ++step) {
-      int64_t pos;
-      int slot, z;
-      unpack_state(in, pos, slot, z);
-      DBits b;
-      b.init(P.stream + sg->byte_off, sg->bits >> 3);
-      b.start(pos);
+      uint64_t e;
       int nst = 0;
-      const uint64_t e =
-          decode_run<kModeSync>(P.imgs[sg->img], b, slot, z, end, false, 0, *sg, nullptr, &nst, nullptr);
+      if (in == cp_st[t]) {  // entered in the speculative decode's own entry state
+        e = Es[t];
+        nst = sn[t];
+      } else {
+        int64_t pos;
+        int slot, z;
+        unpack_state(in, pos, slot, z);
+        DBits b;
+        b.init(P.stream + sg->byte_off, sg->bits >> 3);
+        b.start(pos);
+        Ckpt ck{cp_st, cp_n, P.nsub, t, start, 0, -1};
+        e = decode_run<kModeSync, kCpMatch>(P.imgs[sg->img], b, slot, z, end, false, 0, *sg, nullptr, &nst, nullptr,
+                                            &ck);
+        if (ck.hit >= 0) {  // merged with the speculative decode: its exit, its remaining block starts
+          e = Es[t];
+          nst += sn[t] - cp_n[ck.hit * P.nsub + t];
+        }
+      }
       // block starts of this subsequence: the LAST processing of t used its
       // predecessor's final state (see the invariant above), so at the fixed
       // point these counts are the true ones -- no separate count pass
@@ -387,6 +473,9 @@ __global__ void __launch_bounds__(256) k_scan(const DevSeg* segs, int32_t nseg, 
 
 __global__ void __launch_bounds__(128) k_write(const __grid_constant__ Pass P, const uint64_t* E, const int64_t* base,
                                                int16_t* coef, int* img_bad) {
+  __shared__ uint8_t zz[64];
+  if (threadIdx.x < 64) zz[threadIdx.x] = (uint8_t)kZigzagDev[threadIdx.x];
+  __syncthreads();
   const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= P.nsub) return;
   const DevSeg* sg;
@@ -397,7 +486,8 @@ __global__ void __launch_bounds__(128) k_write(const __grid_constant__ Pass P, c
   DBits b;
   b.init(P.stream + sg->byte_off, sg->bits >> 3);
   b.start(pos);
-  decode_run<kModeWrite>(P.imgs[sg->img], b, slot, z, end, local == sg->nsub - 1, base[t], *sg, coef, nullptr, &bad);
+  decode_run<kModeWrite>(P.imgs[sg->img], b, slot, z, end, local == sg->nsub - 1, base[t], *sg, coef, nullptr, &bad,
+                         nullptr, zz);
   if (bad) img_bad[sg->img] = 1;
 }
 
@@ -419,11 +509,13 @@ __global__ void __launch_bounds__(1024) k_dcpred(const DevImg* imgs, const DevSe
     const int64_t j = c0 + threadIdx.x;
     int16_t* dc = nullptr;
     int32_t v = 0;
-    if (j < nblk) {
-      const int64_t mcu = sg.first_mcu + j / hv;
-      const int k = (int)(j % hv), by = k / im.h[e], bx = k - by * im.h[e];
-      const int64_t my = mcu / im.mcus_x, mx = mcu - my * im.mcus_x;
-      dc = coef + im.coef_base + im.coef_offset[e] + 64 * ((my * im.v[e] + by) * im.bw[e] + mx * im.h[e] + bx);
+    if (j < nblk) {  // 32-bit index arithmetic: an image has < 2^31 blocks
+      const uint32_t q = (uint32_t)j / (uint32_t)hv, k = (uint32_t)j - q * (uint32_t)hv;
+      const uint32_t mcu = (uint32_t)sg.first_mcu + q;
+      const uint32_t by = k / (uint32_t)im.h[e], bx = k - by * (uint32_t)im.h[e];
+      const uint32_t my = mcu / (uint32_t)im.mcus_x, mx = mcu - my * (uint32_t)im.mcus_x;
+      dc = coef + im.coef_base + im.coef_offset[e] +
+           64 * (((int64_t)my * im.v[e] + by) * im.bw[e] + (int64_t)mx * im.h[e] + bx);
       v = *dc;
     }
     int32_t x = v;
@@ -539,17 +631,26 @@ inline void keep_pool_memory() {
   done[dev >> 6] |= 1ull << (dev & 63);
 }
 
+// Stream-ordered scratch, returned to the pool (on the allocating stream)
+// when it goes out of scope.
 template <typename T>
 struct DevBuf {
   T* p = nullptr;
   size_t n = 0;
-  int alloc(size_t count, cudaStream_t st) {
+  cudaStream_t st = nullptr;
+  DevBuf() = default;
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+  ~DevBuf() { release(); }
+  int alloc(size_t count, cudaStream_t stream) {
+    release();
     n = count;
+    st = stream;
     return cudaMallocAsync(reinterpret_cast<void**>(&p), std::max<size_t>(count, 1) * sizeof(T), st) == cudaSuccess
                ? FV_OK
                : set_error(FV_ECUDA, "fv_jpeg_decode_batch_gpu: device allocation of %zu bytes", count * sizeof(T));
   }
-  void release(cudaStream_t st) {
+  void release() {
     if (p) cudaFreeAsync(p, st);
     p = nullptr;
   }
@@ -705,6 +806,7 @@ struct GpuBatch {
       for (int by = 0; by < c.v; ++by)
         for (int bx = 0; bx < c.h; ++bx, ++slot) {
           d.slot_e[slot] = (int8_t)e;
+          d.slot_e2 |= (uint32_t)e << (2 * slot);
           d.slot_bx[slot] = (int8_t)bx;
           d.slot_by[slot] = (int8_t)by;
         }
@@ -765,13 +867,17 @@ struct GpuBatch {
   DevBuf<uint8_t> dstage;  // images, segments, subsequence map, unstuffed bytes (the pinned staging's layout)
   DevBuf<int32_t> dcnt, dflags;
   DevBuf<int16_t> dcoef;
-  DevBuf<uint64_t> dE0;
-  DevBuf<int32_t> dq0, dq1, dmark;
+  DevBuf<uint64_t> dE0, dEs, dcp;
+  DevBuf<int32_t> dq0, dq1, dmark, dsn, dcpn;
   DevBuf<int64_t> dbase;
   int rc = FV_OK;
   rc = rc ? rc : dstage.alloc(stage_bytes, st);
   rc = rc ? rc : dcnt.alloc(nsub, st);
   rc = rc ? rc : dE0.alloc(nsub, st);
+  rc = rc ? rc : dEs.alloc(nsub, st);
+  rc = rc ? rc : dsn.alloc(nsub, st);
+  rc = rc ? rc : dcp.alloc((size_t)nsub * kCp, st);
+  rc = rc ? rc : dcpn.alloc((size_t)nsub * kCp, st);
   rc = rc ? rc : dq0.alloc(nsub, st);
   rc = rc ? rc : dq1.alloc(nsub, st);
   rc = rc ? rc : dmark.alloc(nsub, st);
@@ -801,7 +907,7 @@ struct GpuBatch {
     int* img_bad = dflags.p;
     int* changed = dflags.p + nimg;  // changed[r], r = 0 .. kSyncRounds
     timer.gpu("flags + memsets", st);
-    k_spec<<<grid, 128, 0, st>>>(P, dE0.p, dcnt.p);
+    k_spec<<<grid, 128, 0, st>>>(P, dE0.p, dcnt.p, dEs.p, dsn.p, dcp.p, dcpn.p);
     timer.gpu("speculative pass", st);
     count_launch();
     uint64_t* Ein = dE0.p;
@@ -816,7 +922,8 @@ struct GpuBatch {
     for (int chunk = 0; chunk < kSyncChunks && !rc; ++chunk) {
       for (int k = 0; k < kSyncRounds; ++k, ++r) {
         k_round<<<r == 0 ? grid : qgrid, 128, 0, st>>>(P, Ein, dcnt.p, qa, cnt + r, qb, cnt + r + 1, dmark.p, r + 1,
-                                                       r == 0, r == 0 ? kChain0 : kChain);
+                                                       r == 0, r == 0 ? kChain0 : kChain, dEs.p, dsn.p, dcp.p,
+                                                       dcpn.p);
         if (timer.on) timer.gpu(r == 0 ? "round 0 (all)" : "round k (queue)", st);
         count_launch();
         std::swap(qa, qb);
@@ -882,16 +989,7 @@ struct GpuBatch {
   }
   timer.mark("flags + reconstruct launch");
   timer.gpu_report();
-  dstage.release(st);
-  dcnt.release(st);
-  dE0.release(st);
-  dq0.release(st);
-  dq1.release(st);
-  dmark.release(st);
-  dbase.release(st);
-  dcoef.release(st);
-  dflags.release(st);
-    return rc;
+    return rc;  // the DevBufs return to the pool here
   }
 };
 

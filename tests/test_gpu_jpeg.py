@@ -228,3 +228,40 @@ def test_decode_then_preprocess():
     fv.resize_normalize_chw(img, dst, synth.MEAN, synth.STD)
     ref = FO.resize_normalize_chw(_Z["pil_photo_256__out"], 128, 96, synth.MEAN, synth.STD)
     assert np.array_equal(dst.cpu().numpy(), ref)
+
+
+@pytest.mark.parametrize("name", ["pil_photo_256", "pil_ss2_q85", "asm_440_q85", "pil_ss1_q85", "ref_gray_q92",
+                                  "pil_odd_33x31"])
+@pytest.mark.parametrize("width", [2, 8])
+def test_reconstruct_crafted_coefficients(name, width):
+    """Dequantisation + IDCT + upsampling + colour of crafted coefficients --
+    mostly small blocks, some blocks over the full int16 range, 8- and 16-bit
+    quantisers -- so that both IDCT passes take their int32 and their int64
+    branches (a warp-uniform choice in the batch kernel); int16 input goes
+    through the batch kernels, int64 input through the dense kernel; both
+    against the oracle's int64 arithmetic (jpeg.py:163-203)."""
+    data = stream(name)
+    info = fio.jpeg_info(data)
+    rng = np.random.default_rng(11 + width)
+    nblk = info.coef_count // 64
+    coef = rng.integers(-40, 41, (nblk, 64))
+    wild = rng.random(nblk) < 0.08
+    coef[wild] = rng.integers(-32768, 32768, (int(wild.sum()), 64))
+    coef = coef.reshape(-1)
+    hi = [255, 65535, 16]
+    for e in range(info.ncomp):
+        q = rng.integers(1, hi[e] + 1, 64)
+        for k in range(64):
+            info.qt[e][k] = int(q[k])
+    o = O.parse(data)
+    comps = []
+    for e, c in enumerate(o["comps"]):
+        c["bw"], c["bh"] = info.bw[e], info.bh[e]
+        c["q"] = np.array([info.qt[e][k] for k in range(64)], np.int64)
+        comps.append(coef[info.coef_offset[e]:info.coef_offset[e] + 64 * c["bw"] * c["bh"]].reshape(-1, 64))
+    planes = O.component_planes(o, comps)
+    ref = planes[0].astype(np.uint8)[:, :, None] if len(planes) == 1 else O.ycbcr_to_rgb(*planes)
+    host = torch.from_numpy(coef.astype(np.int16 if width == 2 else np.int64))
+    got = fio._reconstruct(info, host, width, torch.device("cuda", 0))
+    torch.cuda.synchronize()
+    assert np.array_equal(got.cpu().numpy(), ref)

@@ -3,5 +3,5 @@
 ops=$1; shift
 for lib in "$@"; do
   echo "== $lib"
-  FOVEA_B200_LIB=$lib timeout 300 python bench.py --ops "$ops" --no-cpu --no-e2e --steps 10 | python -c "import json,sys; d=json.loads(sys.stdin.read().splitlines()[-1]); [print(k, [(x['kernel'], x['ms'], x['frac']) for x in v['kernels']]) for k,v in d['ops'].items()]"
+  FOVEA_B200_LIB=$lib timeout 300 python bench.py --ops "$ops" --no-cpu --no-e2e --steps ${STEPS:-10} | python -c "import json,sys; d=json.loads(sys.stdin.read().splitlines()[-1]); [print(k, [(x['kernel'], x['ms'], x['frac']) for x in v['kernels']]) for k,v in d['ops'].items()]"
 done
