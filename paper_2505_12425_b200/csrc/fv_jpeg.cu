@@ -337,31 +337,59 @@ __device__ __forceinline__ int find_img(const I* imgs, int n, int64_t k) {
   return lo;
 }
 
-// Thread j of a block's 8-thread group loads coefficient row j and quant row
-// j as two 16-byte vectors, dequantises in int32 (|coef| < 2^15, q < 2^16:
-// exact), and the group transposes through shared memory for the column
-// pass; the image comes from a binary search over the compact `bases`.
-// Each pass runs in int32 when every input of the WARP (4 blocks) is within
-// kIdct32Max (a warp-uniform vote: no divergence), else in int64 -- the
-// same integers either way (see idct8). After an int32 first pass the
-// intermediate fits int32 (|o| <= 61214 * 12000 < 2^30), so only the
-// second pass may need int64.
-__device__ __forceinline__ bool idct_small(const int32_t (&s)[8]) {
-  bool ok = true;
+// One thread per JPEG block: the block's 64 coefficients come in as eight
+// 16-byte loads (a warp reads 32 consecutive blocks, 4 KB contiguous), are
+// dequantised in int32 (|coef| < 2^15, q < 2^16: exact) and stay in
+// registers for both passes; row r of the samples leaves as one 8-byte store
+// (a warp's stores of row r cover 32 consecutive blocks of a block row).
+// Each pass runs in int32 when every input of the WARP is within kIdct32Max
+// (a warp-uniform vote: no divergence), else in int64 -- the same integers
+// either way (see idct8). After an int32 first pass the intermediates fit
+// int32 (|o| <= 61214 * 12000 < 2^30), so the generic path only widens.
+__device__ __forceinline__ bool warp_all_small(const int32_t (&b)[64]) {
+  uint32_t bad = 0;
 #pragma unroll
-  for (int k = 0; k < 8; ++k) ok = ok && (uint32_t)(s[k] + (int32_t)kIdct32Max) <= (uint32_t)(2 * kIdct32Max);
-  return __all_sync(0xFFFFFFFFu, ok);
+  for (int k = 0; k < 64; ++k) bad |= (uint32_t)(b[k] + (int32_t)kIdct32Max) > (uint32_t)(2 * kIdct32Max);
+  return __all_sync(0xFFFFFFFFu, bad == 0);
+}
+
+__device__ __forceinline__ uint32_t pack4_u8(int32_t a, int32_t b, int32_t c, int32_t d) {
+  return __byte_perm(__byte_perm(a, b, 0x0040), __byte_perm(c, d, 0x0040), 0x5410);
+}
+
+// the rare path (crafted magnitudes): both passes in int64, column/row at a time
+__device__ __noinline__ void idct_block_int64(const int16_t* co, const uint16_t* qt, uint8_t* dst, int64_t pitch) {
+  int64_t ws[64];
+#pragma unroll 1
+  for (int j = 0; j < 8; ++j) {
+    int64_t s[8], o[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) s[k] = (int64_t)co[8 * k + j] * qt[8 * k + j];
+    idct8<int64_t>(s, o);
+#pragma unroll
+    for (int k = 0; k < 8; ++k) ws[8 * k + j] = (o[k] + (1 << 10)) >> 11;
+  }
+#pragma unroll 1
+  for (int r = 0; r < 8; ++r) {
+    int64_t s[8], o[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) s[k] = ws[8 * r + k];
+    idct8<int64_t>(s, o);
+    int32_t v[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const int64_t x = ((o[k] + (1 << 17)) >> 18) + 128;
+      v[k] = (int32_t)(x < 0 ? 0 : (x > 255 ? 255 : x));
+    }
+    *reinterpret_cast<uint2*>(dst + r * pitch) = make_uint2(pack4_u8(v[0], v[1], v[2], v[3]), pack4_u8(v[4], v[5], v[6], v[7]));
+  }
 }
 
 __global__ void __launch_bounds__(128) jpeg_idct_batch_kernel(const IdctImg* imgs, const int64_t* bases, int nimg,
                                                               int64_t total) {
-  __shared__ int32_t rows[16][8][9];
-  __shared__ int32_t mid[16][8][9];
-  __shared__ int64_t ws[16][8][9];
-  const int g = threadIdx.x >> 3, j = threadIdx.x & 7;
-  const int64_t gb0 = (int64_t)blockIdx.x * 16 + g;
+  const int64_t gb0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const bool live = gb0 < total;
-  const int64_t gb = live ? gb0 : total - 1;  // the whole warp stays for the votes; dead groups do not store
+  const int64_t gb = live ? gb0 : total - 1;  // the whole warp stays for the votes; dead lanes do not store
   int lo = 0, hi = nimg - 1;
   while (lo < hi) {
     const int m = (lo + hi + 1) >> 1;
@@ -373,78 +401,187 @@ __global__ void __launch_bounds__(128) jpeg_idct_batch_kernel(const IdctImg* img
   int c = 0;
   while (c + 1 < a.ncomp && blk >= a.first_block[c + 1]) ++c;
   const uint32_t lb = (uint32_t)(blk - a.first_block[c]);  // < 2^31 blocks per image
-  const int16_t* co = reinterpret_cast<const int16_t*>(a.coeffs) + a.coef_offset[c] + 64 * (int64_t)lb;
-  const uint4 cr = __ldg(reinterpret_cast<const uint4*>(co + 8 * j));
-  const uint4 qr = *reinterpret_cast<const uint4*>(&a.qt[c][8 * j]);
-  const uint32_t cw[4] = {cr.x, cr.y, cr.z, cr.w}, qw[4] = {qr.x, qr.y, qr.z, qr.w};
+  const uint4* co = reinterpret_cast<const uint4*>(reinterpret_cast<const int16_t*>(a.coeffs) + a.coef_offset[c] +
+                                                   64 * (int64_t)lb);
+  const uint4* qt = reinterpret_cast<const uint4*>(&a.qt[c][0]);
+  int32_t b[64];
 #pragma unroll
-  for (int k = 0; k < 4; ++k) {
-    rows[g][j][2 * k] = (int32_t)(int16_t)(cw[k] & 0xFFFF) * (int32_t)(qw[k] & 0xFFFF);
-    rows[g][j][2 * k + 1] = ((int32_t)cw[k] >> 16) * (int32_t)(qw[k] >> 16);
-  }
-  __syncwarp();
-  const uint32_t bw = (uint32_t)a.bw[c], by = lb / bw, bx = lb - by * bw;
-  uint8_t* dst = a.planes + a.plane_offset[c] + ((int64_t)by * 8 + j) * (int64_t)bw * 8 + (int64_t)bx * 8;
-  int32_t s[8];
+  for (int r = 0; r < 8; ++r) {
+    const uint4 cr = __ldg(co + r), qr = qt[r];
+    const uint32_t cw[4] = {cr.x, cr.y, cr.z, cr.w}, qw[4] = {qr.x, qr.y, qr.z, qr.w};
 #pragma unroll
-  for (int k = 0; k < 8; ++k) s[k] = rows[g][k][j];
-  if (!idct_small(s)) {  // generic int64 path (crafted magnitudes)
-    int64_t t[8];
-#pragma unroll
-    for (int k = 0; k < 8; ++k) t[k] = s[k];
-    int64_t o[8];
-    idct8_exact(t, o);
-#pragma unroll
-    for (int k = 0; k < 8; ++k) ws[g][k][j] = (o[k] + (1 << 10)) >> 11;
-    __syncwarp();
-#pragma unroll
-    for (int k = 0; k < 8; ++k) t[k] = ws[g][j][k];
-    idct8_exact(t, o);
-    uint32_t w[2] = {0, 0};
-#pragma unroll
-    for (int k = 0; k < 8; ++k) {
-      int64_t v = ((o[k] + (1 << 17)) >> 18) + 128;
-      v = v < 0 ? 0 : (v > 255 ? 255 : v);
-      w[k >> 2] |= (uint32_t)v << (8 * (k & 3));
+    for (int k = 0; k < 4; ++k) {
+      b[8 * r + 2 * k] = (int32_t)(int16_t)(cw[k] & 0xFFFF) * (int32_t)(qw[k] & 0xFFFF);
+      b[8 * r + 2 * k + 1] = ((int32_t)cw[k] >> 16) * (int32_t)(qw[k] >> 16);
     }
-    if (live) *reinterpret_cast<uint2*>(dst) = make_uint2(w[0], w[1]);
+  }
+  const uint32_t bw = (uint32_t)a.bw[c], by = lb / bw, bx = lb - by * bw;
+  const int64_t pitch = (int64_t)bw * 8;
+  uint8_t* dst = a.planes + a.plane_offset[c] + (int64_t)by * 8 * pitch + (int64_t)bx * 8;
+  if (!warp_all_small(b)) {
+    if (live) idct_block_int64(reinterpret_cast<const int16_t*>(co), &a.qt[c][0], dst, pitch);
     return;
   }
-  int32_t o[8];
-  idct8<int32_t>(s, o);
 #pragma unroll
-  for (int k = 0; k < 8; ++k) mid[g][k][j] = (o[k] + (1 << 10)) >> 11;
-  __syncwarp();
+  for (int j = 0; j < 8; ++j) {  // columns (vertical frequencies)
+    int32_t s[8], o[8];
 #pragma unroll
-  for (int k = 0; k < 8; ++k) s[k] = mid[g][j][k];
-  uint32_t w[2] = {0, 0};
-  if (idct_small(s)) {
+    for (int k = 0; k < 8; ++k) s[k] = b[8 * k + j];
     idct8<int32_t>(s, o);
 #pragma unroll
-    for (int k = 0; k < 8; ++k) {
-      const int32_t v = min(max(((o[k] + (1 << 17)) >> 18) + 128, 0), 255);
-      w[k >> 2] |= (uint32_t)v << (8 * (k & 3));
-    }
-  } else {
-    int64_t t[8], q[8];
-#pragma unroll
-    for (int k = 0; k < 8; ++k) t[k] = s[k];
-    idct8<int64_t>(t, q);
-#pragma unroll
-    for (int k = 0; k < 8; ++k) {
-      int64_t v = ((q[k] + (1 << 17)) >> 18) + 128;
-      v = v < 0 ? 0 : (v > 255 ? 255 : v);
-      w[k >> 2] |= (uint32_t)v << (8 * (k & 3));
-    }
+    for (int k = 0; k < 8; ++k) b[8 * k + j] = (o[k] + (1 << 10)) >> 11;
   }
-  if (live) *reinterpret_cast<uint2*>(dst) = make_uint2(w[0], w[1]);
+  const bool small2 = warp_all_small(b);
+#pragma unroll
+  for (int r = 0; r < 8; ++r) {  // rows
+    int32_t v[8];
+    if (small2) {
+      int32_t s[8], o[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) s[k] = b[8 * r + k];
+      idct8<int32_t>(s, o);
+#pragma unroll
+      for (int k = 0; k < 8; ++k) v[k] = min(max(((o[k] + (1 << 17)) >> 18) + 128, 0), 255);
+    } else {
+      int64_t s[8], o[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) s[k] = b[8 * r + k];
+      idct8<int64_t>(s, o);
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const int64_t x = ((o[k] + (1 << 17)) >> 18) + 128;
+        v[k] = (int32_t)(x < 0 ? 0 : (x > 255 ? 255 : x));
+      }
+    }
+    if (live)
+      *reinterpret_cast<uint2*>(dst + r * pitch) =
+          make_uint2(pack4_u8(v[0], v[1], v[2], v[3]), pack4_u8(v[4], v[5], v[6], v[7]));
+  }
 }
 
+// Chroma columns 4i-1 .. 4i+4 of one chroma row (the 8 output columns
+// 8i..8i+7 need them), column indices clamped to the plane: clamping is
+// exactly the reference's edge rule -- its first/last output column formulas
+// (jpeg.py:833-841) are the interior formula with the missing neighbour
+// replaced by the edge column itself. Interior groups read three aligned
+// words; edge groups read the six bytes one by one.
+__device__ __forceinline__ void chroma6(const uint8_t* row, int i, int mw, bool interior, int (&c)[6]) {
+  if (interior) {
+    const uint32_t* p = reinterpret_cast<const uint32_t*>(row) + i;
+    const uint32_t w0 = __ldg(p - 1), w1 = __ldg(p), w2 = __ldg(p + 1);
+    c[0] = (int)(w0 >> 24);
+#pragma unroll
+    for (int t = 1; t < 5; ++t) c[t] = (int)((w1 >> (8 * (t - 1))) & 0xFF);
+    c[5] = (int)(w2 & 0xFF);
+  } else {
+#pragma unroll
+    for (int t = 0; t < 6; ++t) c[t] = (int)__ldg(row + min(max(4 * i - 1 + t, 0), mw - 1));
+  }
+}
+
+// 4:2:0: the 8 upsampled samples of output columns 8i..8i+7 of one output
+// row from its two chroma rows (near = the row's own, far = the one above
+// for an even row, below for an odd row): column sums 3*near + far, then the
+// horizontal 3:1 filter with +8 / +7 (jpeg.py:824-841).
+__device__ __forceinline__ void upsample420_8(const int (&nr)[6], const int (&fr)[6], int (&s)[8]) {
+  int v[6];
+#pragma unroll
+  for (int t = 0; t < 6; ++t) v[t] = 3 * nr[t] + fr[t];
+#pragma unroll
+  for (int k = 0; k < 8; k += 2) {
+    const int t = (k >> 1) + 1;
+    s[k] = (3 * v[t] + v[t - 1] + 8) >> 4;
+    s[k + 1] = (3 * v[t] + v[t + 1] + 7) >> 4;
+  }
+}
+
+// YCbCr -> RGB of 8 pixels (jpeg.py:226-235), stored as 3*n bytes (n <= 8)
+__device__ __forceinline__ void store_rgb8(uint8_t* q, uint2 yv, const int (&cb)[8], const int (&cr)[8], int n) {
+  int o[24];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    const int y = (int)(((k < 4 ? yv.x : yv.y) >> (8 * (k & 3))) & 0xFF);
+    const int xb = cb[k] - 128, xr = cr[k] - 128;
+    o[3 * k] = min(max(y + ((91881 * xr + 32768) >> 16), 0), 255);
+    o[3 * k + 1] = min(max(y + ((-22554 * xb + 32768 - 46802 * xr) >> 16), 0), 255);
+    o[3 * k + 2] = min(max(y + ((116130 * xb + 32768) >> 16), 0), 255);
+  }
+  uint32_t w[6];
+#pragma unroll
+  for (int k = 0; k < 6; ++k) w[k] = pack4_u8(o[4 * k], o[4 * k + 1], o[4 * k + 2], o[4 * k + 3]);
+  const uintptr_t al = reinterpret_cast<uintptr_t>(q);
+  if (n == 8 && (al & 7) == 0) {
+#pragma unroll
+    for (int k = 0; k < 3; ++k) reinterpret_cast<uint2*>(q)[k] = make_uint2(w[2 * k], w[2 * k + 1]);
+  } else if (n == 8 && (al & 3) == 0) {
+#pragma unroll
+    for (int k = 0; k < 6; ++k) reinterpret_cast<uint32_t*>(q)[k] = w[k];
+  } else {
+#pragma unroll
+    for (int k = 0; k < 24; ++k)
+      if (k < 3 * n) q[k] = (uint8_t)(w[k >> 2] >> (8 * (k & 3)));
+  }
+}
+
+// Output rows 2m and 2m+1 (when present), columns 8i..8i+7 (those present),
+// of a 4:2:0 image with chroma width > 2: the three chroma rows m-1, m, m+1
+// (clamped: the reference's row replication) are read once for both rows.
+// The Y plane's rows are padded to whole blocks, so its 8-byte load never
+// leaves the row.
+__device__ __forceinline__ void color420_16(const ColorArgs& a, int i, int m) {
+  const int mw = a.cw[1], mh = a.ch[1];
+  const int x0 = 8 * i, n = min(8, a.width - x0);
+  const bool interior = i >= 1 && 4 * i + 4 <= mw - 1 && 4 * i + 8 <= a.pitch[1];
+  const int ru = max(m - 1, 0), rd = min(m + 1, mh - 1);
+  int b0[6], b1[6], b2[6], r0[6], r1[6], r2[6];
+  chroma6(a.plane[1] + (int64_t)ru * a.pitch[1], i, mw, interior, b0);
+  chroma6(a.plane[1] + (int64_t)m * a.pitch[1], i, mw, interior, b1);
+  chroma6(a.plane[1] + (int64_t)rd * a.pitch[1], i, mw, interior, b2);
+  chroma6(a.plane[2] + (int64_t)ru * a.pitch[2], i, mw, interior, r0);
+  chroma6(a.plane[2] + (int64_t)m * a.pitch[2], i, mw, interior, r1);
+  chroma6(a.plane[2] + (int64_t)rd * a.pitch[2], i, mw, interior, r2);
+  const int y0 = 2 * m;
+  {
+    int cb[8], cr[8];
+    upsample420_8(b1, b0, cb);
+    upsample420_8(r1, r0, cr);
+    const uint2 yv = __ldg(reinterpret_cast<const uint2*>(a.plane[0] + (int64_t)y0 * a.pitch[0] + x0));
+    store_rgb8(a.dst + (int64_t)y0 * a.d_rp + 3 * x0, yv, cb, cr, n);
+  }
+  if (y0 + 1 < a.height) {
+    int cb[8], cr[8];
+    upsample420_8(b1, b2, cb);
+    upsample420_8(r1, r2, cr);
+    const uint2 yv = __ldg(reinterpret_cast<const uint2*>(a.plane[0] + (int64_t)(y0 + 1) * a.pitch[0] + x0));
+    store_rgb8(a.dst + (int64_t)(y0 + 1) * a.d_rp + 3 * x0, yv, cb, cr, n);
+  }
+}
+
+// One CTA per 8 output rows (4 row pairs) of an image of the batch; thread
+// -> 8 columns of a row pair. The CTA's image and its arguments are looked
+// up once (thread 0) and shared.
+constexpr int kColorRows = 8;
 __global__ void __launch_bounds__(256) jpeg_color_batch_kernel(const ColorImg* imgs, int nimg) {
-  const int im = find_img(imgs, nimg, (int64_t)blockIdx.x);
-  const ColorArgs& a = imgs[im].a;
-  const int y = (int)(blockIdx.x - imgs[im].base);
-  for (int x0 = threadIdx.x * 4; x0 < a.width; x0 += 1024) color4(a, x0, y);
+  __shared__ ColorArgs sa;
+  __shared__ int s_row0;
+  if (threadIdx.x == 0) {
+    const int im = find_img(imgs, nimg, (int64_t)blockIdx.x);
+    sa = imgs[im].a;
+    s_row0 = (int)(blockIdx.x - imgs[im].base) * kColorRows;
+  }
+  __syncthreads();
+  const ColorArgs& a = sa;
+  const int row0 = s_row0, row1 = min(row0 + kColorRows, a.height);
+  const bool h2v2 = a.ncomp == 3 && a.fh[0] == 1 && a.fv[0] == 1 && a.fh[1] == 2 && a.fv[1] == 2 && a.fh[2] == 2 &&
+                    a.fv[2] == 2 && a.cw[1] == a.cw[2] && a.ch[1] == a.ch[2] && a.cw[1] > 2;
+  if (h2v2) {
+    const int groups = (a.width + 7) >> 3;
+    for (int y = row0; y < row1; y += 2)
+      for (int i = threadIdx.x; i < groups; i += blockDim.x) color420_16(a, i, y >> 1);
+    return;
+  }
+  for (int y = row0; y < row1; ++y)
+    for (int x0 = threadIdx.x * 4; x0 < a.width; x0 += 4 * blockDim.x) color4(a, x0, y);
 }
 
 }  // namespace jpg
@@ -580,7 +717,7 @@ int reconstruct_batch(int n, const FvJpegInfo* const* fs, const int16_t* const* 
     blocks += make_idct_args(*fs[i], coeffs[i], planes[i], ii[i].a);
     ci[i].base = rows;
     make_color_args(*fs[i], planes[i], dst[i], dst_pitch[i], ci[i].a);
-    rows += fs[i]->height;
+    rows += (fs[i]->height + kColorRows - 1) / kColorRows;  // the colour kernel's CTAs
   }
   if ((blocks + 15) / 16 > 0x7FFFFFFF || rows > 0x7FFFFFFF)
     return set_error(FV_EINVAL, "fv_jpeg_reconstruct: batch too large");
@@ -599,7 +736,7 @@ int reconstruct_batch(int n, const FvJpegInfo* const* fs, const int16_t* const* 
   cudaMemcpyAsync(di, ii.data(), n * sizeof(IdctImg), cudaMemcpyHostToDevice, st);
   cudaMemcpyAsync(dc, ci.data(), n * sizeof(ColorImg), cudaMemcpyHostToDevice, st);
   cudaMemcpyAsync(db, bases.data(), n * sizeof(int64_t), cudaMemcpyHostToDevice, st);
-  jpeg_idct_batch_kernel<<<(unsigned)((blocks + 15) / 16), 128, 0, st>>>(di, db, n, blocks);
+  jpeg_idct_batch_kernel<<<(unsigned)((blocks + 127) / 128), 128, 0, st>>>(di, db, n, blocks);
   int rc = check_launch("jpeg_idct_batch_kernel");
   if (!rc) {
     jpeg_color_batch_kernel<<<(unsigned)rows, 256, 0, st>>>(dc, n);
