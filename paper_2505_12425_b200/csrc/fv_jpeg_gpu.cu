@@ -68,6 +68,8 @@ struct DevImg {
   DevHuff dc[3], ac[3];  // per scan entry
   int8_t slot_e[kMaxSlots], slot_bx[kMaxSlots], slot_by[kMaxSlots];
   uint32_t slot_e2;  // slot_e packed, 2 bits per slot
+  int64_t slot_off[kMaxSlots];  // coefficient offset of each slot's block within its MCU (component region included)
+  int64_t mcu_row[3], mcu_col[3];  // coefficient strides of an MCU row / column per scan entry
   int32_t nslots, mcus_x;
   int32_t h[3], v[3], bw[3];
   int64_t coef_offset[3];  // within the image's dense int32 region
@@ -181,18 +183,32 @@ struct Ckpt {
   int hit;         // match mode: the checkpoint matched, or -1
 };
 
-// Destination of block `cb` (decode order) of segment `sg`, or nullptr for a
-// block outside the segment (a desynchronised decode can run past it).
-// Block indices of an image stay below 2^31 (65535^2 / 64 * 3).
-__device__ __forceinline__ int16_t* block_dst(const DevImg& im, const DevSeg& sg, int64_t cb, int16_t* coef) {
-  if (cb < sg.first_block || cb >= sg.first_block + sg.nblocks) return nullptr;
-  const uint32_t c = (uint32_t)cb, ns = (uint32_t)im.nslots;
-  const uint32_t mcu = c / ns, s = c - mcu * ns;
-  const int e = im.slot_e[s];
-  const uint32_t my = mcu / (uint32_t)im.mcus_x, mx = mcu - my * (uint32_t)im.mcus_x;
-  const int64_t r = ((int64_t)my * im.v[e] + im.slot_by[s]) * im.bw[e] + (int64_t)mx * im.h[e] + im.slot_bx[s];
-  return coef + im.coef_base + im.coef_offset[e] + 64 * r;
-}
+// Write mode's block addressing: the MCU position (mx, my) of the current
+// block is derived once from its decode-order index (block indices of an
+// image stay below 2^31: 65535^2 / 64 * 3) and then stepped as the decoder
+// wraps its slot; a block's coefficients start at
+//   coef_base + slot_off[slot] + my * mcu_row[e] + mx * mcu_col[e].
+struct BlockPos {
+  uint32_t mx, my;
+  __device__ __forceinline__ void init(const DevImg& im, int64_t cb) {
+    const uint32_t mcu = (uint32_t)cb / (uint32_t)im.nslots;
+    my = mcu / (uint32_t)im.mcus_x;
+    mx = mcu - my * (uint32_t)im.mcus_x;
+  }
+  __device__ __forceinline__ void next_mcu(const DevImg& im) {
+    if (++mx == (uint32_t)im.mcus_x) {
+      mx = 0;
+      ++my;
+    }
+  }
+  // block `cb` in slot `slot`, or nullptr outside the segment (a
+  // desynchronised decode can run past it)
+  __device__ __forceinline__ int16_t* dst(const DevImg& im, const DevSeg& sg, int64_t cb, int slot, int e,
+                                          int16_t* coef) const {
+    if (cb < sg.first_block || cb >= sg.first_block + sg.nblocks) return nullptr;
+    return coef + im.coef_base + im.slot_off[slot] + (int64_t)my * im.mcu_row[e] + (int64_t)mx * im.mcu_col[e];
+  }
+};
 
 // Decode symbols starting before `end_bit` (write mode on the segment's last
 // subsequence: until the segment's last block is complete). Anomalies on the
@@ -208,7 +224,11 @@ __device__ uint64_t decode_run(const DevImg& im, DBits& b, int slot, int z, int6
   const uint32_t slot_e = im.slot_e2;  // 2 bits per slot
   const int nslots = im.nslots;
   int16_t* dst = nullptr;
-  if (MODE == kModeWrite && z != 0) dst = block_dst(im, sg, blk - 1, coef);  // entered mid-block
+  BlockPos bp;
+  if (MODE == kModeWrite) {
+    bp.init(im, z != 0 ? blk - 1 : blk);
+    if (z != 0) dst = bp.dst(im, sg, blk - 1, slot, (slot_e >> (2 * slot)) & 3, coef);  // entered mid-block
+  }
   for (;;) {
     const int64_t pos = b.pos();
     if (MODE == kModeWrite && last_sub) {
@@ -238,7 +258,7 @@ __device__ uint64_t decode_run(const DevImg& im, DBits& b, int slot, int z, int6
     const int e = (slot_e >> (2 * slot)) & 3;
     if (z == 0) {  // DC of a new block
       if (nstart) ++*nstart;
-      if (MODE == kModeWrite) dst = block_dst(im, sg, blk++, coef);
+      if (MODE == kModeWrite) dst = bp.dst(im, sg, blk++, slot, e, coef);
       const DevHuff& t = im.dc[e];
       const int32_t f = t.fast[b.peek(10)];
       int32_t diff;
@@ -301,7 +321,10 @@ __device__ uint64_t decode_run(const DevImg& im, DBits& b, int slot, int z, int6
     if (z >= 64) {  // block complete
       z = 0;
       slot = slot + 1 == nslots ? 0 : slot + 1;
-      if (MODE == kModeWrite && blk == limit && b.pos() > sg.bits) *bad = 1;  // consumed padding
+      if (MODE == kModeWrite) {
+        if (slot == 0) bp.next_mcu(im);
+        if (blk == limit && b.pos() > sg.bits) *bad = 1;  // consumed padding
+      }
     }
   }
   return pack_state(b.pos(), slot, z);
@@ -813,6 +836,14 @@ struct GpuBatch {
     }
     d.nslots = slot;
     d.mcus_x = s.mcus_x;
+    for (int k = 0; k < slot; ++k) {
+      const int e = d.slot_e[k];
+      d.slot_off[k] = d.coef_offset[e] + 64 * ((int64_t)d.slot_by[k] * d.bw[e] + d.slot_bx[k]);
+    }
+    for (int e = 0; e < s.nscan; ++e) {
+      d.mcu_row[e] = 64 * (int64_t)d.v[e] * d.bw[e];
+      d.mcu_col[e] = 64 * (int64_t)d.h[e];
+    }
     d.coef_base = coef_off[i];
     memcpy(&himg[img_idx[i]], &d, sizeof(d));
     flush_lines(&himg[img_idx[i]], sizeof(d));
