@@ -779,19 +779,11 @@ int fv_jpeg_info_batch(const uint8_t* const* data, const int64_t* lens, int32_t 
                        int32_t* status, int32_t threads) {
   if (n < 0 || (n > 0 && (!data || !lens || !infos || !status)))
     return set_error(FV_EINVAL, "fv_jpeg_info_batch: bad arguments");
-  std::atomic<int32_t> next{0};
-  auto work = [&]() {
-    for (int32_t i; (i = next.fetch_add(1)) < n;) {
-      std::unique_ptr<Stream> s(new Stream());
-      status[i] = parse(data[i], lens[i], *s);
-      if (status[i] == FV_OK) fill_info(*s, infos[i]);
-    }
-  };
-  const int nt = std::max(1, std::min<int>(threads, n));
-  std::vector<std::thread> pool;
-  for (int t = 1; t < nt; ++t) pool.emplace_back(work);
-  work();
-  for (auto& t : pool) t.join();
+  WorkPool::get().run(n, std::max(1, threads), [&](int32_t i) {
+    std::unique_ptr<Stream> s(new Stream());
+    status[i] = parse(data[i], lens[i], *s);
+    if (status[i] == FV_OK) fill_info(*s, infos[i]);
+  });
   return FV_OK;
 }
 
@@ -806,18 +798,19 @@ int fv_jpeg_decode_batch(const uint8_t* const* data, const int64_t* lens, int32_
   std::vector<std::atomic<int32_t>> done(n);
   std::vector<int64_t> used(n, 0);
   for (auto& d : done) d.store(1, std::memory_order_relaxed);  // 1 = pending
-  std::atomic<int32_t> next{0};
-  auto work = [&]() {
-    for (int32_t i; (i = next.fetch_add(1)) < n;) {
-      const int64_t cap = infos[i].coef_count / 64 + infos[i].sparse_words;
-      const int rc = decode_one_sparse(data[i], lens[i], words_host + word_off[i], cap, &used[i]);
-      if (rc == FV_OK) flush_lines(words_host + word_off[i], (size_t)used[i] * 4);  // DMA-friendly (see flush_lines)
-      done[i].store(rc, std::memory_order_release);
-    }
+  // pool threads decode while this thread feeds the GPU (it finishes what
+  // no pool thread took before returning)
+  WorkPool& wp = WorkPool::get();
+  WorkPool::Job job;
+  job.fn = [&](int32_t i) {
+    const int64_t cap = infos[i].coef_count / 64 + infos[i].sparse_words;
+    const int rc = decode_one_sparse(data[i], lens[i], words_host + word_off[i], cap, &used[i]);
+    if (rc == FV_OK) flush_lines(words_host + word_off[i], (size_t)used[i] * 4);  // DMA-friendly (see flush_lines)
+    done[i].store(rc, std::memory_order_release);
   };
-  const int nt = std::max(1, std::min<int>(threads, n));
-  std::vector<std::thread> pool;
-  for (int t = 0; t < nt; ++t) pool.emplace_back(work);
+  job.n = n;
+  job.want = std::max(1, std::min(std::min<int>(threads, n), wp.size()));
+  wp.start(job);
   // in input order, as soon as an image's coefficients are ready: H2D of the
   // words it used, then its kernels
   int first = FV_OK;
@@ -841,7 +834,7 @@ int fv_jpeg_decode_batch(const uint8_t* const* data, const int64_t* lens, int32_
       status[i] = rc;
     }
   }
-  for (auto& t : pool) t.join();
+  wp.wait(job);
   return first;
 }
 

@@ -30,7 +30,10 @@
 namespace fv {
 namespace jpg {
 
-constexpr int kSubBits = 1024;
+#ifndef FV_JPEG_SUB_BITS
+#define FV_JPEG_SUB_BITS 1024
+#endif
+constexpr int kSubBits = FV_JPEG_SUB_BITS;
 constexpr int kMaxSlots = 12;
 constexpr int kSyncRounds = 6;    // rounds per chunk (one 4-byte readback per chunk)
 constexpr int kSyncChunks = 32;   // cap: images still changing after this fall back
@@ -65,7 +68,7 @@ struct DevHuff {
 };
 
 struct DevImg {
-  DevHuff dc[3], ac[3];  // per scan entry
+  int32_t dc_t[3], ac_t[3];  // per scan entry: index into the batch's (deduplicated) Huffman tables
   int8_t slot_e[kMaxSlots], slot_bx[kMaxSlots], slot_by[kMaxSlots];
   uint32_t slot_e2;  // slot_e packed, 2 bits per slot
   int64_t slot_off[kMaxSlots];  // coefficient offset of each slot's block within its MCU (component region included)
@@ -214,26 +217,31 @@ struct BlockPos {
 // subsequence: until the segment's last block is complete). Anomalies on the
 // true path (write mode, blocks of the segment) set *bad; elsewhere the
 // decoder steps on deterministically (skip a bit / end the block).
-// Write mode: `zz` is the zigzag table (shared memory), the destination is
-// resolved once per block.
+// Write mode: each block is written whole -- zeros included, so the
+// coefficient buffer needs no clearing -- by the thread whose range it
+// STARTS in: that thread decodes on past its end bit to finish its last
+// block, and a thread entering mid-block decodes the remainder without
+// writing. The block is assembled in the thread's shared-memory buffer `sb`
+// (64 int16, zero on entry and on exit) in natural order through `zz` (the
+// zigzag table, shared memory) and leaves as eight 16-byte stores.
 template <int MODE, int CPM = kCpNone>
-__device__ uint64_t decode_run(const DevImg& im, DBits& b, int slot, int z, int64_t end_bit, bool last_sub,
+__device__ uint64_t decode_run(const DevHuff* tabs, const DevImg& im, DBits& b, int slot, int z, int64_t end_bit, bool last_sub,
                                int64_t blk, const DevSeg& sg, int16_t* coef, int* nstart, int* bad,
-                               Ckpt* ck = nullptr, const uint8_t* zz = nullptr) {
+                               Ckpt* ck = nullptr, const uint8_t* zz = nullptr, int16_t* sb = nullptr) {
   const int64_t limit = sg.first_block + sg.nblocks;
   const uint32_t slot_e = im.slot_e2;  // 2 bits per slot
   const int nslots = im.nslots;
-  int16_t* dst = nullptr;
+  int16_t* dst = nullptr;  // the current block's destination when this thread writes it
+  const DevHuff* tac = tabs + im.ac_t[(slot_e >> (2 * slot)) & 3];  // the current block's AC table
   BlockPos bp;
-  if (MODE == kModeWrite) {
-    bp.init(im, z != 0 ? blk - 1 : blk);
-    if (z != 0) dst = bp.dst(im, sg, blk - 1, slot, (slot_e >> (2 * slot)) & 3, coef);  // entered mid-block
-  }
+  if (MODE == kModeWrite) bp.init(im, z != 0 ? blk - 1 : blk);
   for (;;) {
     const int64_t pos = b.pos();
     if (MODE == kModeWrite && last_sub) {
       if (blk >= limit && z == 0) break;              // the segment's blocks are done
       if (pos > sg.bits + 64 * 16) { *bad = 1; break; }  // decoding deep into padding: corrupt
+    } else if (MODE == kModeWrite) {
+      if (pos >= end_bit && z == 0) break;  // past the range and between blocks
     } else if (pos >= end_bit) {
       break;
     }
@@ -259,7 +267,8 @@ __device__ uint64_t decode_run(const DevImg& im, DBits& b, int slot, int z, int6
     if (z == 0) {  // DC of a new block
       if (nstart) ++*nstart;
       if (MODE == kModeWrite) dst = bp.dst(im, sg, blk++, slot, e, coef);
-      const DevHuff& t = im.dc[e];
+      const DevHuff& t = tabs[im.dc_t[e]];
+      tac = tabs + im.ac_t[e];
       const int32_t f = t.fast[b.peek(10)];
       int32_t diff;
       if (f & kFull) {
@@ -278,10 +287,10 @@ __device__ uint64_t decode_run(const DevImg& im, DBits& b, int slot, int z, int6
           diff = 0;
         }
       }
-      if (MODE == kModeWrite && dst) dst[0] = (int16_t)diff;  // |diff| <= 2047
+      if (MODE == kModeWrite && dst) sb[0] = (int16_t)diff;  // |diff| <= 2047
       z = 1;
     } else {
-      const DevHuff& t = im.ac[e];
+      const DevHuff& t = *tac;
       const int32_t f = t.fast[b.peek(10)];
       if (f & kFull) {
         b.skip(f & 31);
@@ -290,7 +299,7 @@ __device__ uint64_t decode_run(const DevImg& im, DBits& b, int slot, int z, int6
           if (MODE == kModeWrite && dst) *bad = 1;
           z = 64;
         } else {
-          if (MODE == kModeWrite && dst) dst[zz[z]] = (int16_t)(f >> 16);
+          if (MODE == kModeWrite && dst) sb[zz[z]] = (int16_t)(f >> 16);
           ++z;
         }
       } else {
@@ -311,7 +320,7 @@ __device__ uint64_t decode_run(const DevImg& im, DBits& b, int slot, int z, int6
             } else {
               const int32_t v = dextend(b.peek(sz), sz);
               b.skip(sz);
-              if (MODE == kModeWrite && dst) dst[zz[z]] = (int16_t)v;  // |v| < 2^15
+              if (MODE == kModeWrite && dst) sb[zz[z]] = (int16_t)v;  // |v| < 2^15
               ++z;
             }
           }
@@ -322,6 +331,16 @@ __device__ uint64_t decode_run(const DevImg& im, DBits& b, int slot, int z, int6
       z = 0;
       slot = slot + 1 == nslots ? 0 : slot + 1;
       if (MODE == kModeWrite) {
+        if (dst) {  // the finished block leaves whole; the buffer is cleared for the next one
+          uint4* sv = reinterpret_cast<uint4*>(sb);
+          uint4* dv = reinterpret_cast<uint4*>(dst);
+#pragma unroll
+          for (int k = 0; k < 8; ++k) {
+            dv[k] = sv[k];
+            sv[k] = make_uint4(0, 0, 0, 0);
+          }
+          dst = nullptr;
+        }
         if (slot == 0) bp.next_mcu(im);
         if (blk == limit && b.pos() > sg.bits) *bad = 1;  // consumed padding
       }
@@ -336,6 +355,7 @@ __device__ uint64_t decode_run(const DevImg& im, DBits& b, int slot, int z, int6
 // ---------------------------------------------------------------------------
 
 struct Pass {
+  const DevHuff* huff;  // the batch's distinct Huffman tables
   const DevImg* imgs;
   const DevSeg* segs;
   const int32_t* sub_seg;
@@ -365,14 +385,14 @@ __global__ void __launch_bounds__(128) k_spec(const __grid_constant__ Pass P, ui
   if (kWarmBits > 0 && local > 0) {  // warm up on the preceding bits: enter this subsequence (likely) in step
     const int64_t w0 = start > (int64_t)kWarmBits ? start - (int64_t)kWarmBits : 0;
     b.start(w0);
-    const uint64_t e = decode_run<kModeSync>(P.imgs[sg->img], b, 0, 0, start, false, 0, *sg, nullptr, nullptr, nullptr);
+    const uint64_t e = decode_run<kModeSync>(P.huff, P.imgs[sg->img], b, 0, 0, start, false, 0, *sg, nullptr, nullptr, nullptr);
     unpack_state(e, pos, slot, z);
   }
   b.start(pos);
   int n = 0;
   Ckpt ck{cp_st, cp_n, P.nsub, t, start, 0, -1};
   const uint64_t e =
-      decode_run<kModeSync, kCpRecord>(P.imgs[sg->img], b, slot, z, end, false, 0, *sg, nullptr, &n, nullptr, &ck);
+      decode_run<kModeSync, kCpRecord>(P.huff, P.imgs[sg->img], b, slot, z, end, false, 0, *sg, nullptr, &n, nullptr, &ck);
   for (int k = ck.k; k < kCp; ++k) cp_st[k * P.nsub + t] = kNoState;
   E[t] = e;
   Es[t] = e;
@@ -420,7 +440,7 @@ __global__ void __launch_bounds__(128) k_round(const __grid_constant__ Pass P, u
         b.init(P.stream + sg->byte_off, sg->bits >> 3);
         b.start(pos);
         Ckpt ck{cp_st, cp_n, P.nsub, t, start, 0, -1};
-        e = decode_run<kModeSync, kCpMatch>(P.imgs[sg->img], b, slot, z, end, false, 0, *sg, nullptr, &nst, nullptr,
+        e = decode_run<kModeSync, kCpMatch>(P.huff, P.imgs[sg->img], b, slot, z, end, false, 0, *sg, nullptr, &nst, nullptr,
                                             &ck);
         if (ck.hit >= 0) {  // merged with the speculative decode: its exit, its remaining block starts
           e = Es[t];
@@ -497,7 +517,13 @@ __global__ void __launch_bounds__(256) k_scan(const DevSeg* segs, int32_t nseg, 
 __global__ void __launch_bounds__(128) k_write(const __grid_constant__ Pass P, const uint64_t* E, const int64_t* base,
                                                int16_t* coef, int* img_bad) {
   __shared__ uint8_t zz[64];
+  // per-thread block buffers, 144-byte stride: a warp's 16-byte accesses to
+  // them spread over all banks
+  __shared__ __align__(16) int16_t bufs[128][72];
   if (threadIdx.x < 64) zz[threadIdx.x] = (uint8_t)kZigzagDev[threadIdx.x];
+  uint4* mine = reinterpret_cast<uint4*>(bufs[threadIdx.x]);
+#pragma unroll
+  for (int k = 0; k < 8; ++k) mine[k] = make_uint4(0, 0, 0, 0);
   __syncthreads();
   const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= P.nsub) return;
@@ -509,8 +535,8 @@ __global__ void __launch_bounds__(128) k_write(const __grid_constant__ Pass P, c
   DBits b;
   b.init(P.stream + sg->byte_off, sg->bits >> 3);
   b.start(pos);
-  decode_run<kModeWrite>(P.imgs[sg->img], b, slot, z, end, local == sg->nsub - 1, base[t], *sg, coef, nullptr, &bad,
-                         nullptr, zz);
+  decode_run<kModeWrite>(P.huff, P.imgs[sg->img], b, slot, z, end, local == sg->nsub - 1, base[t], *sg, coef, nullptr, &bad,
+                         nullptr, zz, bufs[threadIdx.x]);
   if (bad) img_bad[sg->img] = 1;
 }
 
@@ -586,7 +612,30 @@ struct Plan {
   int rc = FV_OK;
   bool gpu = false;
   int64_t nseg = 0, nsub = 0, bytes = 0, coefs = 0;
+  uint64_t hkey[6] = {};  // Huffman table hashes: DC, AC per scan entry
+  int32_t tab[6] = {};    // their indices among the batch's distinct tables
 };
+
+// Huffman tables are deduplicated across a batch (most encoders emit the
+// standard tables): one copy per distinct table keeps the decoders' table
+// lookups in L1. A table is defined by its codes and symbols (mincode,
+// maxcode, valptr, values) and its class (the fast entries differ for DC).
+inline uint64_t huff_key(const Huff& h, bool dc) {
+  uint64_t x = dc ? 0x9E3779B97F4A7C15ull : 0xC2B2AE3D27D4EB4Full;
+  auto mix = [&](const void* p, size_t n) {
+    const uint8_t* c = static_cast<const uint8_t*>(p);
+    for (size_t i = 0; i < n; ++i) x = (x ^ c[i]) * 0x100000001B3ull;
+  };
+  mix(h.mincode, sizeof(h.mincode));
+  mix(h.maxcode, sizeof(h.maxcode));
+  mix(h.valptr, sizeof(h.valptr));
+  mix(h.values, 256);
+  return x;
+}
+inline bool huff_same(const Huff& a, const Huff& b) {
+  return memcmp(a.mincode, b.mincode, sizeof(a.mincode)) == 0 && memcmp(a.maxcode, b.maxcode, sizeof(a.maxcode)) == 0 &&
+         memcmp(a.valptr, b.valptr, sizeof(a.valptr)) == 0 && memcmp(a.values, b.values, 256) == 0;
+}
 
 // Can the GPU path decode this stream exactly? (else: the host decoder)
 inline bool gpu_eligible(const Stream& s, const FvJpegInfo& f) {
@@ -730,7 +779,7 @@ struct GpuBatch {
   int32_t nimg = 0;
   std::unique_lock<std::mutex> stage_lock;
   uint8_t* stage_base = nullptr;
-  size_t o_img = 0, o_seg = 0, o_sub = 0, o_bytes = 0, stage_bytes = 0;  // one contiguous upload
+  size_t o_huff = 0, o_img = 0, o_seg = 0, o_sub = 0, o_bytes = 0, stage_bytes = 0;  // one contiguous upload
   DevImg* himg = nullptr;
   DevSeg* hseg = nullptr;
   int32_t* hsub = nullptr;
@@ -739,14 +788,7 @@ struct GpuBatch {
 
   template <class F>
   void parallel(F&& fn) {
-    std::atomic<int32_t> next{0};
-    auto work = [&]() {
-      for (int32_t i; (i = next.fetch_add(1)) < n;) fn(i);
-    };
-    std::vector<std::thread> pool;
-    for (int t = 1; t < nt; ++t) pool.emplace_back(work);
-    work();
-    for (auto& t : pool) t.join();
+    WorkPool::get().run(n, nt, std::forward<F>(fn));
   }
 
   int make(const uint8_t* const* data, const int64_t* lens, FvJpegInfo* infos, int32_t* status) {
@@ -769,6 +811,11 @@ struct GpuBatch {
       p.nsub += std::max<int64_t>(1, (8 * s.seg_len[k] + kSubBits - 1) / kSubBits);
     }
     p.coefs = f.coef_count;
+    for (int e = 0; e < s.nscan; ++e) {
+      const Comp& c = s.sof[s.scan_comp[e]];
+      p.hkey[2 * e] = huff_key(s.dc[c.td], true);
+      p.hkey[2 * e + 1] = huff_key(s.ac[c.ta], false);
+    }
   });
   timer.mark("parse + plan");
   // 2. offsets
@@ -792,10 +839,31 @@ struct GpuBatch {
     ncoef += plan[i].coefs;
   }
   if (nimg == 0) return FV_OK;
-  // 3. host staging: images, segments, subsequence -> segment, unstuffed bytes
+  // distinct Huffman tables
+  struct Uniq {
+    uint64_t key;
+    const Huff* h;
+  };
+  std::vector<Uniq> uniq;
+  for (int32_t i = 0; i < n; ++i) {
+    if (!plan[i].gpu) continue;
+    const Stream& s = *plan[i].s;
+    for (int e = 0; e < s.nscan; ++e)
+      for (int cls = 0; cls < 2; ++cls) {
+        const Comp& c = s.sof[s.scan_comp[e]];
+        const Huff& h = cls ? s.ac[c.ta] : s.dc[c.td];
+        const uint64_t key = plan[i].hkey[2 * e + cls];
+        size_t u = 0;
+        while (u < uniq.size() && !(uniq[u].key == key && huff_same(*uniq[u].h, h))) ++u;
+        if (u == uniq.size()) uniq.push_back({key, &h});
+        plan[i].tab[2 * e + cls] = (int32_t)u;
+      }
+  }
+  // 3. host staging: tables, images, segments, subsequence -> segment, unstuffed bytes
   PinnedStage& stage = pinned_stage();
   stage_lock = std::unique_lock<std::mutex>(stage.lock);  // held until the batch is freed
-  o_img = 0;
+  o_huff = 0;
+  o_img = o_huff + ((uniq.size() * sizeof(DevHuff) + 255) & ~size_t(255));
   o_seg = o_img + ((nimg * sizeof(DevImg) + 255) & ~size_t(255));
   o_sub = o_seg + ((nseg * sizeof(DevSeg) + 255) & ~size_t(255));
   o_bytes = o_sub + ((nsub * sizeof(int32_t) + 255) & ~size_t(255));
@@ -803,6 +871,16 @@ struct GpuBatch {
   uint8_t* sbase = stage.get(stage_bytes);
   if (!sbase) return set_error(FV_ECUDA, "fv_jpeg_batch_plan: pinned staging of %zu bytes", stage_bytes);
   stage_base = sbase;
+  {
+    DevHuff* hh = reinterpret_cast<DevHuff*>(sbase + o_huff);
+    std::unique_ptr<DevHuff> tmp(new DevHuff());
+    for (size_t u = 0; u < uniq.size(); ++u) {  // class: the first use's (the key includes it)
+      memset(tmp.get(), 0, sizeof(DevHuff));
+      to_dev_huff(*uniq[u].h, *tmp);
+      memcpy(&hh[u], tmp.get(), sizeof(DevHuff));
+    }
+    flush_lines(hh, uniq.size() * sizeof(DevHuff));
+  }
   himg = reinterpret_cast<DevImg*>(sbase + o_img);
   hseg = reinterpret_cast<DevSeg*>(sbase + o_seg);
   hsub = reinterpret_cast<int32_t*>(sbase + o_sub);
@@ -820,8 +898,8 @@ struct GpuBatch {
     int slot = 0;
     for (int e = 0; e < s.nscan; ++e) {
       const Comp& c = s.sof[s.scan_comp[e]];
-      to_dev_huff(s.dc[c.td], d.dc[e]);
-      to_dev_huff(s.ac[c.ta], d.ac[e]);
+      d.dc_t[e] = plan[i].tab[2 * e];
+      d.ac_t[e] = plan[i].tab[2 * e + 1];
       d.h[e] = c.h;
       d.v[e] = c.v;
       d.bw[e] = f.bw[e];
@@ -931,9 +1009,9 @@ struct GpuBatch {
     const int32_t* const dsub_p = reinterpret_cast<const int32_t*>(dstage.p + o_sub);
     const uint8_t* const dbytes_p = dstage.p + o_bytes;
     cudaMemcpyAsync(dflags.p, hflags.data(), hflags.size() * sizeof(int32_t), cudaMemcpyHostToDevice, st);
-    cudaMemsetAsync(dcoef.p, 0, ncoef * sizeof(int16_t), st);
+    // (no clearing of dcoef: the write pass stores every block whole)
     cudaMemsetAsync(dmark.p, 0, nsub * sizeof(int32_t), st);
-    Pass P{dimg_p, dseg_p, dsub_p, dbytes_p, nsub};
+    Pass P{reinterpret_cast<const DevHuff*>(dstage.p + o_huff), dimg_p, dseg_p, dsub_p, dbytes_p, nsub};
     const unsigned grid = (unsigned)((nsub + 127) / 128);
     int* img_bad = dflags.p;
     int* changed = dflags.p + nimg;  // changed[r], r = 0 .. kSyncRounds

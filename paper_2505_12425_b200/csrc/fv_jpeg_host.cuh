@@ -4,8 +4,16 @@
 // or sparse coefficient sinks. Shared by fv_jpeg.cu (host entropy path and
 // GPU reconstruction) and fv_jpeg_gpu.cu (GPU entropy path planning).
 #pragma once
+#include <sched.h>
+#include <unistd.h>
+
 #include <algorithm>
+#include <atomic>
+#include <condition_variable>
 #include <cstdarg>
+#include <functional>
+#include <mutex>
+#include <thread>
 #include <cstdio>
 #include <cstring>
 #include <memory>
@@ -601,6 +609,105 @@ inline void flush_lines(const void* p, size_t n) {
 #else
 inline void flush_lines(const void*, size_t) {}
 #endif
+
+// ---------------------------------------------------------------------------
+// host worker pool: the batch entry points run their per-image work (parse,
+// unstuff, entropy decoding) on persistent threads -- spawning and joining
+// a thread per worker costs tens of microseconds each, per call.
+// ---------------------------------------------------------------------------
+
+class WorkPool {
+ public:
+  // fn(i) for i in [0, n); `want` pool threads join (the caller may help)
+  struct Job {
+    std::function<void(int32_t)> fn;
+    int32_t n = 0;
+    int want = 0;
+    std::atomic<int32_t> next{0};
+    int joined = 0, running = 0;  // guarded by the pool mutex
+    void work() {
+      for (int32_t i; (i = next.fetch_add(1)) < n;) fn(i);
+    }
+  };
+
+  // the process's pool (re-created in a forked child, whose threads are gone)
+  static WorkPool& get() {
+    static std::mutex m;
+    static WorkPool* pool = nullptr;
+    std::lock_guard<std::mutex> g(m);
+    if (!pool || pool->pid_ != getpid()) pool = new WorkPool();  // never destroyed: no exit-time joins
+    return *pool;
+  }
+  int size() const { return (int)threads_.size(); }
+
+  void start(Job& j) {
+    if (j.want <= 0) return;
+    std::lock_guard<std::mutex> g(m_);
+    queue_.push_back(&j);
+    cv_.notify_all();
+  }
+  // all of j's iterations done and no pool thread still inside it (the
+  // caller finishes what no thread took)
+  void wait(Job& j) {
+    {
+      std::lock_guard<std::mutex> g(m_);
+      unqueue(&j);
+    }
+    j.work();
+    std::unique_lock<std::mutex> g(m_);
+    done_.wait(g, [&] { return j.running == 0; });
+  }
+  // run fn over [0, n) on `threads` threads (the caller is one of them)
+  void run(int32_t n, int threads, std::function<void(int32_t)> fn) {
+    Job j;
+    j.fn = std::move(fn);
+    j.n = n;
+    j.want = std::max(0, std::min(std::min(threads, (int)n) - 1, size()));
+    start(j);
+    j.work();
+    wait(j);
+  }
+
+ private:
+  WorkPool() : pid_(getpid()) {
+    // one thread per CPU this process may run on
+    int n = (int)std::thread::hardware_concurrency();
+    cpu_set_t cs;
+    if (sched_getaffinity(0, sizeof(cs), &cs) == 0) n = CPU_COUNT(&cs);
+    n = std::max(1, n);
+    for (int t = 0; t < n; ++t) threads_.emplace_back([this] { loop(); });
+    for (auto& t : threads_) t.detach();
+  }
+  void unqueue(Job* j) {
+    for (size_t k = 0; k < queue_.size(); ++k)
+      if (queue_[k] == j) {
+        queue_.erase(queue_.begin() + (long)k);
+        return;
+      }
+  }
+  void loop() {
+    for (;;) {
+      Job* j;
+      {
+        std::unique_lock<std::mutex> g(m_);
+        cv_.wait(g, [&] { return !queue_.empty(); });
+        j = queue_.front();
+        ++j->running;
+        if (++j->joined >= j->want) unqueue(j);
+      }
+      j->work();
+      {
+        std::lock_guard<std::mutex> g(m_);
+        if (--j->running == 0) done_.notify_all();
+      }
+    }
+  }
+  pid_t pid_;
+  std::mutex m_;
+  std::condition_variable cv_, done_;
+  std::vector<Job*> queue_;
+  std::vector<std::thread> threads_;
+};
 
 // GPU reconstruction (fv_jpeg.cu): dequantise + IDCT + upsample + colour of
 // one image's coefficients (coef_bytes 2/4/8 dense int16/int32/int64, 1 the
