@@ -129,6 +129,7 @@ struct DBits {
   __device__ __forceinline__ void start(int64_t bit) {
     const int64_t c = bit >> 5;
     const int off = (int)(bit & 31);
+    if (c + 32 < nw) asm volatile("prefetch.global.L1 [%0];" ::"l"(w + c + 32));  // the next line's words
     acc = (((uint64_t)word(c) << 32) | word(c + 1)) << off;
     nb = 64 - off;
     cur = c + 2;
@@ -177,9 +178,26 @@ constexpr int kCp = kSubBits / kCpBits;
 constexpr uint64_t kNoState = ~0ull;  // an unrecorded checkpoint (never equals a real state)
 enum { kCpNone = 0, kCpRecord = 1, kCpMatch = 2 };
 
+// What a subsequence contributes to the scan: the blocks that start in it
+// and the sums of their DC differences per scan entry. (In write mode the d
+// fields carry the running DC predictions instead.)
+struct Tally {
+  int32_t n = 0, d0 = 0, d1 = 0, d2 = 0;
+  __device__ __forceinline__ int32_t add_dc(int e, int32_t diff) {
+    return e == 0 ? (d0 += diff) : (e == 1 ? (d1 += diff) : (d2 += diff));
+  }
+  __device__ __forceinline__ int4 v() const { return make_int4(n, d0, d1, d2); }
+  __device__ __forceinline__ void add(int4 a, int4 b) {  // += a - b
+    n += a.x - b.x;
+    d0 += a.y - b.y;
+    d1 += a.z - b.z;
+    d2 += a.w - b.w;
+  }
+};
+
 struct Ckpt {
   uint64_t* st;    // [kCp][nsub] states
-  int32_t* n;      // [kCp][nsub] block starts before the checkpoint (speculative decode)
+  int4* tal;       // [kCp][nsub] the speculative decode's tally before the checkpoint
   int64_t nsub, t;
   int64_t mark;    // next mark (bit position)
   int k;           // next checkpoint index
@@ -192,24 +210,31 @@ struct Ckpt {
 // wraps its slot; a block's coefficients start at
 //   coef_base + slot_off[slot] + my * mcu_row[e] + mx * mcu_col[e].
 struct BlockPos {
-  uint32_t mx, my;
-  __device__ __forceinline__ void init(const DevImg& im, int64_t cb) {
+  uint32_t mx, my, mcus_x;
+  int64_t first, limit;  // the segment's blocks (decode order)
+  int16_t* base;         // the image's coefficient region
+  // (register copies: the block stores to global memory would otherwise make
+  // the compiler reload the segment / image fields after each block)
+  __device__ __forceinline__ void init(const DevImg& im, const DevSeg& sg, int64_t cb, int16_t* coef) {
+    mcus_x = (uint32_t)im.mcus_x;
+    first = sg.first_block;
+    limit = sg.first_block + sg.nblocks;
+    base = coef + im.coef_base;
     const uint32_t mcu = (uint32_t)cb / (uint32_t)im.nslots;
-    my = mcu / (uint32_t)im.mcus_x;
-    mx = mcu - my * (uint32_t)im.mcus_x;
+    my = mcu / mcus_x;
+    mx = mcu - my * mcus_x;
   }
-  __device__ __forceinline__ void next_mcu(const DevImg& im) {
-    if (++mx == (uint32_t)im.mcus_x) {
+  __device__ __forceinline__ void next_mcu() {
+    if (++mx == mcus_x) {
       mx = 0;
       ++my;
     }
   }
   // block `cb` in slot `slot`, or nullptr outside the segment (a
   // desynchronised decode can run past it)
-  __device__ __forceinline__ int16_t* dst(const DevImg& im, const DevSeg& sg, int64_t cb, int slot, int e,
-                                          int16_t* coef) const {
-    if (cb < sg.first_block || cb >= sg.first_block + sg.nblocks) return nullptr;
-    return coef + im.coef_base + im.slot_off[slot] + (int64_t)my * im.mcu_row[e] + (int64_t)mx * im.mcu_col[e];
+  __device__ __forceinline__ int16_t* dst(const DevImg& im, int64_t cb, int slot, int e) const {
+    if (cb < first || cb >= limit) return nullptr;
+    return base + __ldg(&im.slot_off[slot]) + (int64_t)my * __ldg(&im.mcu_row[e]) + (int64_t)mx * __ldg(&im.mcu_col[e]);
   }
 };
 
@@ -226,20 +251,20 @@ struct BlockPos {
 // zigzag table, shared memory) and leaves as eight 16-byte stores.
 template <int MODE, int CPM = kCpNone>
 __device__ uint64_t decode_run(const DevHuff* tabs, const DevImg& im, DBits& b, int slot, int z, int64_t end_bit, bool last_sub,
-                               int64_t blk, const DevSeg& sg, int16_t* coef, int* nstart, int* bad,
+                               int64_t blk, const DevSeg& sg, int16_t* coef, Tally* tal, int* bad,
                                Ckpt* ck = nullptr, const uint8_t* zz = nullptr, int16_t* sb = nullptr) {
-  const int64_t limit = sg.first_block + sg.nblocks;
+  const int64_t limit = sg.first_block + sg.nblocks, seg_bits = sg.bits;
   const uint32_t slot_e = im.slot_e2;  // 2 bits per slot
   const int nslots = im.nslots;
   int16_t* dst = nullptr;  // the current block's destination when this thread writes it
   const DevHuff* tac = tabs + im.ac_t[(slot_e >> (2 * slot)) & 3];  // the current block's AC table
   BlockPos bp;
-  if (MODE == kModeWrite) bp.init(im, z != 0 ? blk - 1 : blk);
+  if (MODE == kModeWrite) bp.init(im, sg, z != 0 ? blk - 1 : blk, coef);
   for (;;) {
     const int64_t pos = b.pos();
     if (MODE == kModeWrite && last_sub) {
       if (blk >= limit && z == 0) break;              // the segment's blocks are done
-      if (pos > sg.bits + 64 * 16) { *bad = 1; break; }  // decoding deep into padding: corrupt
+      if (pos > seg_bits + 64 * 16) { *bad = 1; break; }  // decoding deep into padding: corrupt
     } else if (MODE == kModeWrite) {
       if (pos >= end_bit && z == 0) break;  // past the range and between blocks
     } else if (pos >= end_bit) {
@@ -256,7 +281,7 @@ __device__ uint64_t decode_run(const DevHuff* tabs, const DevImg& im, DBits& b, 
       do {  // every mark this boundary is the first at or past
         if (CPM == kCpRecord) {
           ck->st[ck->k * ck->nsub + ck->t] = st;
-          ck->n[ck->k * ck->nsub + ck->t] = *nstart;
+          ck->tal[ck->k * ck->nsub + ck->t] = tal->v();
         }
         ++ck->k;
         ck->mark += kCpBits;
@@ -265,8 +290,8 @@ __device__ uint64_t decode_run(const DevHuff* tabs, const DevImg& im, DBits& b, 
     b.fill();
     const int e = (slot_e >> (2 * slot)) & 3;
     if (z == 0) {  // DC of a new block
-      if (nstart) ++*nstart;
-      if (MODE == kModeWrite) dst = bp.dst(im, sg, blk++, slot, e, coef);
+      if (MODE != kModeWrite && tal) ++tal->n;
+      if (MODE == kModeWrite) dst = bp.dst(im, blk++, slot, e);
       const DevHuff& t = tabs[im.dc_t[e]];
       tac = tabs + im.ac_t[e];
       const int32_t f = t.fast[b.peek(10)];
@@ -287,7 +312,15 @@ __device__ uint64_t decode_run(const DevHuff* tabs, const DevImg& im, DBits& b, 
           diff = 0;
         }
       }
-      if (MODE == kModeWrite && dst) sb[0] = (int16_t)diff;  // |diff| <= 2047
+      if (MODE == kModeWrite) {
+        if (dst) {  // the DC prediction: the running sum from the segment's prefix (k_scan)
+          const int32_t dc = tal->add_dc(e, diff);
+          if (dc < -32768 || dc > 32767) *bad = 1;  // beyond int16 (crafted streams): host decoder
+          sb[0] = (int16_t)dc;
+        }
+      } else if (tal) {
+        tal->add_dc(e, diff);
+      }
       z = 1;
     } else {
       const DevHuff& t = *tac;
@@ -341,8 +374,8 @@ __device__ uint64_t decode_run(const DevHuff* tabs, const DevImg& im, DBits& b, 
           }
           dst = nullptr;
         }
-        if (slot == 0) bp.next_mcu(im);
-        if (blk == limit && b.pos() > sg.bits) *bad = 1;  // consumed padding
+        if (slot == 0) bp.next_mcu();
+        if (blk == limit && b.pos() > seg_bits) *bad = 1;  // consumed padding
       }
     }
   }
@@ -371,8 +404,8 @@ __device__ __forceinline__ void sub_range(const Pass& P, int64_t t, const DevSeg
   end = min(start + (int64_t)kSubBits, sg->bits);
 }
 
-__global__ void __launch_bounds__(128) k_spec(const __grid_constant__ Pass P, uint64_t* E, int32_t* cnt,
-                                              uint64_t* Es, int32_t* cp_st_n, uint64_t* cp_st, int32_t* cp_n) {
+__global__ void __launch_bounds__(128) k_spec(const __grid_constant__ Pass P, uint64_t* E, int4* tally,
+                                              uint64_t* Es, int4* spec_tally, uint64_t* cp_st, int4* cp_tal) {
   const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= P.nsub) return;
   const DevSeg* sg;
@@ -389,15 +422,15 @@ __global__ void __launch_bounds__(128) k_spec(const __grid_constant__ Pass P, ui
     unpack_state(e, pos, slot, z);
   }
   b.start(pos);
-  int n = 0;
-  Ckpt ck{cp_st, cp_n, P.nsub, t, start, 0, -1};
+  Tally tl;
+  Ckpt ck{cp_st, cp_tal, P.nsub, t, start, 0, -1};
   const uint64_t e =
-      decode_run<kModeSync, kCpRecord>(P.huff, P.imgs[sg->img], b, slot, z, end, false, 0, *sg, nullptr, &n, nullptr, &ck);
+      decode_run<kModeSync, kCpRecord>(P.huff, P.imgs[sg->img], b, slot, z, end, false, 0, *sg, nullptr, &tl, nullptr, &ck);
   for (int k = ck.k; k < kCp; ++k) cp_st[k * P.nsub + t] = kNoState;
   E[t] = e;
   Es[t] = e;
-  cnt[t] = n;  // exact for each segment's first subsequence; the others are re-derived in the rounds
-  cp_st_n[t] = n;
+  tally[t] = tl.v();  // exact for each segment's first subsequence; the others are re-derived in the rounds
+  spec_tally[t] = tl.v();
 }
 
 // One propagation round over a work queue: for each queued subsequence t,
@@ -414,10 +447,10 @@ __device__ __forceinline__ void enqueue(int32_t* qout, int* nout, int* mark, int
   if (atomicExch(&mark[t], round) != round) qout[atomicAdd(nout, 1)] = (int32_t)t;
 }
 
-__global__ void __launch_bounds__(128) k_round(const __grid_constant__ Pass P, uint64_t* E, int32_t* cnt,
+__global__ void __launch_bounds__(128) k_round(const __grid_constant__ Pass P, uint64_t* E, int4* tally,
                                                const int32_t* qin, const int* nin, int32_t* qout, int* nout, int* mark,
                                                int round, int all_subs, int chain, const uint64_t* Es,
-                                               const int32_t* sn, uint64_t* cp_st, int32_t* cp_n) {
+                                               const int4* spec_tally, uint64_t* cp_st, int4* cp_tal) {
   const int64_t n = all_subs ? P.nsub : *nin;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     int64_t t = all_subs ? i : qin[i];
@@ -428,10 +461,10 @@ __global__ void __launch_bounds__(128) k_round(const __grid_constant__ Pass P, u
     uint64_t in = E[t - 1];
     for (int step = 0;; ++step) {
       uint64_t e;
-      int nst = 0;
+      Tally tl;
       if (in == cp_st[t]) {  // entered in the speculative decode's own entry state
         e = Es[t];
-        nst = sn[t];
+        tl.add(spec_tally[t], make_int4(0, 0, 0, 0));
       } else {
         int64_t pos;
         int slot, z;
@@ -439,18 +472,18 @@ __global__ void __launch_bounds__(128) k_round(const __grid_constant__ Pass P, u
         DBits b;
         b.init(P.stream + sg->byte_off, sg->bits >> 3);
         b.start(pos);
-        Ckpt ck{cp_st, cp_n, P.nsub, t, start, 0, -1};
-        e = decode_run<kModeSync, kCpMatch>(P.huff, P.imgs[sg->img], b, slot, z, end, false, 0, *sg, nullptr, &nst, nullptr,
+        Ckpt ck{cp_st, cp_tal, P.nsub, t, start, 0, -1};
+        e = decode_run<kModeSync, kCpMatch>(P.huff, P.imgs[sg->img], b, slot, z, end, false, 0, *sg, nullptr, &tl, nullptr,
                                             &ck);
-        if (ck.hit >= 0) {  // merged with the speculative decode: its exit, its remaining block starts
+        if (ck.hit >= 0) {  // merged with the speculative decode: its exit, the rest of its tally
           e = Es[t];
-          nst += sn[t] - cp_n[ck.hit * P.nsub + t];
+          tl.add(spec_tally[t], cp_tal[ck.hit * P.nsub + t]);
         }
       }
-      // block starts of this subsequence: the LAST processing of t used its
+      // this subsequence's tally: the LAST processing of t used its
       // predecessor's final state (see the invariant above), so at the fixed
-      // point these counts are the true ones -- no separate count pass
-      cnt[t] = nst;
+      // point these are the true ones -- no separate count pass
+      tally[t] = tl.v();
       if (e == E[t]) break;
       E[t] = e;
       if (local + 1 >= sg->nsub) break;
@@ -484,38 +517,70 @@ __device__ __forceinline__ void entry_state(const Pass& P, const uint64_t* E, in
   }
 }
 
-// exclusive scan of the block-start counts of each segment's subsequences
-__global__ void __launch_bounds__(256) k_scan(const DevSeg* segs, int32_t nseg, const int32_t* cnt, int64_t* base) {
-  __shared__ int64_t warp_sum[8];
+// exclusive scan of the tallies of each segment's subsequences: the first
+// block of every subsequence and the DC predictions it starts from
+__global__ void __launch_bounds__(256) k_scan(const DevSeg* segs, int32_t nseg, const int4* tally, int64_t* base,
+                                              int4* dcb) {
+  __shared__ int64_t warp_n[8];
+  __shared__ int32_t warp_d[3][8];
   const int sgi = blockIdx.x;
   if (sgi >= nseg) return;
   const DevSeg& sg = segs[sgi];
   int64_t carry = sg.first_block;
+  int32_t c0d = 0, c1d = 0, c2d = 0;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   for (int64_t c0 = 0; c0 < sg.nsub; c0 += 256) {
     const int64_t i = c0 + threadIdx.x;
-    const int64_t v = i < sg.nsub ? cnt[sg.first_sub + i] : 0;
-    int64_t x = v;
+    const int4 v = i < sg.nsub ? tally[sg.first_sub + i] : make_int4(0, 0, 0, 0);
+    int64_t x = v.x;
+    int32_t y0 = v.y, y1 = v.z, y2 = v.w;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
-      const int64_t y = __shfl_up_sync(0xffffffffu, x, o);
-      if (lane >= o) x += y;
+      const int64_t a = __shfl_up_sync(0xffffffffu, x, o);
+      const int32_t b0 = __shfl_up_sync(0xffffffffu, y0, o), b1 = __shfl_up_sync(0xffffffffu, y1, o),
+                    b2 = __shfl_up_sync(0xffffffffu, y2, o);
+      if (lane >= o) {
+        x += a;
+        y0 += b0;
+        y1 += b1;
+        y2 += b2;
+      }
     }
-    if (lane == 31) warp_sum[w] = x;
+    if (lane == 31) {
+      warp_n[w] = x;
+      warp_d[0][w] = y0;
+      warp_d[1][w] = y1;
+      warp_d[2][w] = y2;
+    }
     __syncthreads();
     int64_t pre = 0, tot = 0;
+    int32_t p0 = 0, p1 = 0, p2 = 0, t0 = 0, t1 = 0, t2 = 0;
     for (int k = 0; k < 8; ++k) {
-      if (k < w) pre += warp_sum[k];
-      tot += warp_sum[k];
+      if (k < w) {
+        pre += warp_n[k];
+        p0 += warp_d[0][k];
+        p1 += warp_d[1][k];
+        p2 += warp_d[2][k];
+      }
+      tot += warp_n[k];
+      t0 += warp_d[0][k];
+      t1 += warp_d[1][k];
+      t2 += warp_d[2][k];
     }
-    if (i < sg.nsub) base[sg.first_sub + i] = carry + pre + x - v;
+    if (i < sg.nsub) {
+      base[sg.first_sub + i] = carry + pre + x - v.x;
+      dcb[sg.first_sub + i] = make_int4(0, c0d + p0 + y0 - v.y, c1d + p1 + y1 - v.z, c2d + p2 + y2 - v.w);
+    }
     carry += tot;
+    c0d += t0;
+    c1d += t1;
+    c2d += t2;
     __syncthreads();
   }
 }
 
 __global__ void __launch_bounds__(128) k_write(const __grid_constant__ Pass P, const uint64_t* E, const int64_t* base,
-                                               int16_t* coef, int* img_bad) {
+                                               const int4* dcb, int16_t* coef, int* img_bad) {
   __shared__ uint8_t zz[64];
   // per-thread block buffers, 144-byte stride: a warp's 16-byte accesses to
   // them spread over all banks
@@ -535,61 +600,14 @@ __global__ void __launch_bounds__(128) k_write(const __grid_constant__ Pass P, c
   DBits b;
   b.init(P.stream + sg->byte_off, sg->bits >> 3);
   b.start(pos);
-  decode_run<kModeWrite>(P.huff, P.imgs[sg->img], b, slot, z, end, local == sg->nsub - 1, base[t], *sg, coef, nullptr, &bad,
+  const int4 d = dcb[t];
+  Tally run;
+  run.d0 = d.y;
+  run.d1 = d.z;
+  run.d2 = d.w;
+  decode_run<kModeWrite>(P.huff, P.imgs[sg->img], b, slot, z, end, local == sg->nsub - 1, base[t], *sg, coef, &run, &bad,
                          nullptr, zz, bufs[threadIdx.x]);
   if (bad) img_bad[sg->img] = 1;
-}
-
-// DC prediction: per (segment, scan entry), a prefix sum of the DC
-// differences over the component's blocks in decode order (MCU, then by, bx).
-// Values beyond int16 (only crafted streams) flag the image: host decoder.
-__global__ void __launch_bounds__(1024) k_dcpred(const DevImg* imgs, const DevSeg* segs, int16_t* coef, int* img_bad) {
-  __shared__ int32_t warp_sum[32];
-  const DevSeg& sg = segs[blockIdx.x];
-  const DevImg& im = imgs[sg.img];
-  const int e = blockIdx.y;
-  if (e >= 3 || im.h[e] == 0) return;
-  const int hv = im.h[e] * im.v[e];
-  const int64_t nblk = sg.nmcu * hv;
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  int32_t carry = 0;
-  bool over = false;
-  for (int64_t c0 = 0; c0 < nblk; c0 += 1024) {
-    const int64_t j = c0 + threadIdx.x;
-    int16_t* dc = nullptr;
-    int32_t v = 0;
-    if (j < nblk) {  // 32-bit index arithmetic: an image has < 2^31 blocks
-      const uint32_t q = (uint32_t)j / (uint32_t)hv, k = (uint32_t)j - q * (uint32_t)hv;
-      const uint32_t mcu = (uint32_t)sg.first_mcu + q;
-      const uint32_t by = k / (uint32_t)im.h[e], bx = k - by * (uint32_t)im.h[e];
-      const uint32_t my = mcu / (uint32_t)im.mcus_x, mx = mcu - my * (uint32_t)im.mcus_x;
-      dc = coef + im.coef_base + im.coef_offset[e] +
-           64 * (((int64_t)my * im.v[e] + by) * im.bw[e] + (int64_t)mx * im.h[e] + bx);
-      v = *dc;
-    }
-    int32_t x = v;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const int32_t y = __shfl_up_sync(0xffffffffu, x, o);
-      if (lane >= o) x += y;
-    }
-    if (lane == 31) warp_sum[w] = x;
-    __syncthreads();
-    int32_t pre = 0, tot = 0;
-    for (int k = 0; k < 32; ++k) {
-      const int32_t q = warp_sum[k];
-      pre += k < w ? q : 0;
-      tot += q;
-    }
-    if (dc) {
-      const int32_t val = carry + pre + x;
-      over = over || val < -32768 || val > 32767;
-      *dc = (int16_t)val;
-    }
-    carry += tot;
-    __syncthreads();
-  }
-  if (over) img_bad[sg.img] = 1;
 }
 
 // ---------------------------------------------------------------------------
@@ -974,19 +992,21 @@ struct GpuBatch {
     if (nimg == 0) return FV_OK;
   // 4. device buffers and passes
   DevBuf<uint8_t> dstage;  // images, segments, subsequence map, unstuffed bytes (the pinned staging's layout)
-  DevBuf<int32_t> dcnt, dflags;
+  DevBuf<int4> dtally, dstally, dcptal, ddcb;
+  DevBuf<int32_t> dflags;
   DevBuf<int16_t> dcoef;
   DevBuf<uint64_t> dE0, dEs, dcp;
-  DevBuf<int32_t> dq0, dq1, dmark, dsn, dcpn;
+  DevBuf<int32_t> dq0, dq1, dmark;
   DevBuf<int64_t> dbase;
   int rc = FV_OK;
   rc = rc ? rc : dstage.alloc(stage_bytes, st);
-  rc = rc ? rc : dcnt.alloc(nsub, st);
+  rc = rc ? rc : dtally.alloc(nsub, st);
+  rc = rc ? rc : dstally.alloc(nsub, st);
+  rc = rc ? rc : ddcb.alloc(nsub, st);
   rc = rc ? rc : dE0.alloc(nsub, st);
   rc = rc ? rc : dEs.alloc(nsub, st);
-  rc = rc ? rc : dsn.alloc(nsub, st);
   rc = rc ? rc : dcp.alloc((size_t)nsub * kCp, st);
-  rc = rc ? rc : dcpn.alloc((size_t)nsub * kCp, st);
+  rc = rc ? rc : dcptal.alloc((size_t)nsub * kCp, st);
   rc = rc ? rc : dq0.alloc(nsub, st);
   rc = rc ? rc : dq1.alloc(nsub, st);
   rc = rc ? rc : dmark.alloc(nsub, st);
@@ -1016,7 +1036,7 @@ struct GpuBatch {
     int* img_bad = dflags.p;
     int* changed = dflags.p + nimg;  // changed[r], r = 0 .. kSyncRounds
     timer.gpu("flags + memsets", st);
-    k_spec<<<grid, 128, 0, st>>>(P, dE0.p, dcnt.p, dEs.p, dsn.p, dcp.p, dcpn.p);
+    k_spec<<<grid, 128, 0, st>>>(P, dE0.p, dtally.p, dEs.p, dstally.p, dcp.p, dcptal.p);
     timer.gpu("speculative pass", st);
     count_launch();
     uint64_t* Ein = dE0.p;
@@ -1030,9 +1050,9 @@ struct GpuBatch {
     int r = 0;
     for (int chunk = 0; chunk < kSyncChunks && !rc; ++chunk) {
       for (int k = 0; k < kSyncRounds; ++k, ++r) {
-        k_round<<<r == 0 ? grid : qgrid, 128, 0, st>>>(P, Ein, dcnt.p, qa, cnt + r, qb, cnt + r + 1, dmark.p, r + 1,
-                                                       r == 0, r == 0 ? kChain0 : kChain, dEs.p, dsn.p, dcp.p,
-                                                       dcpn.p);
+        k_round<<<r == 0 ? grid : qgrid, 128, 0, st>>>(P, Ein, dtally.p, qa, cnt + r, qb, cnt + r + 1, dmark.p, r + 1,
+                                                       r == 0, r == 0 ? kChain0 : kChain, dEs.p, dstally.p, dcp.p,
+                                                       dcptal.p);
         if (timer.on) timer.gpu(r == 0 ? "round 0 (all)" : "round k (queue)", st);
         count_launch();
         std::swap(qa, qb);
@@ -1058,16 +1078,14 @@ struct GpuBatch {
       for (int q = 1; q <= r; ++q) fprintf(stderr, " %d", ch[q]);
       fprintf(stderr, "\n");
     }
-    k_scan<<<(unsigned)nseg, 256, 0, st>>>(dseg_p, (int32_t)nseg, dcnt.p, dbase.p);
-    k_write<<<grid, 128, 0, st>>>(P, Ein, dbase.p, dcoef.p, img_bad);
+    k_scan<<<(unsigned)nseg, 256, 0, st>>>(dseg_p, (int32_t)nseg, dtally.p, dbase.p, ddcb.p);
+    k_write<<<grid, 128, 0, st>>>(P, Ein, dbase.p, ddcb.p, dcoef.p, img_bad);
     timer.gpu("scan + write", st);
-    k_dcpred<<<dim3((unsigned)nseg, 3), 1024, 0, st>>>(dimg_p, dseg_p, dcoef.p, img_bad);
-    timer.gpu("dc prediction", st);
     rc = check_launch("fv_jpeg_decode_batch_gpu passes");
     count_launch();
     count_launch();
   }
-  timer.mark("count + write + dc");
+  timer.mark("scan + write");
   if (!rc) {
     // which images decoded cleanly (a second sync)
     cudaMemcpyAsync(hflags.data(), dflags.p, nimg * sizeof(int32_t), cudaMemcpyDeviceToHost, st);

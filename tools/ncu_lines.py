@@ -1,18 +1,21 @@
-"""Aggregate an ncu report's SASS instruction counts by CUDA source line:
-    python tools/ncu_lines.py report.ncu-rep kernel_regex [top]"""
+"""Aggregate an ncu report's SASS instruction counts (or, with --stalls, warp
+stall samples) by CUDA source line:
+    python tools/ncu_lines.py report.ncu-rep kernel_regex [top] [--stalls]"""
 import collections
 import csv
 import io
 import subprocess
 import sys
 
-rep, kern = sys.argv[1], sys.argv[2]
-top = int(sys.argv[3]) if len(sys.argv) > 3 else 30
+args = [a for a in sys.argv[1:] if not a.startswith("--")]
+rep, kern = args[0], args[1]
+top = int(args[2]) if len(args) > 2 else 30
+col = "Warp Stall Sampling (All Samples)" if "--stalls" in sys.argv else "Instructions Executed"
 out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "-k", kern, "--print-source", "sass,cuda"],
                      capture_output=True, text=True).stdout
 rows = list(csv.reader(io.StringIO(out)))
-hdr = next(r for r in rows if "Instructions Executed" in r)
-ei = hdr.index("Instructions Executed")
+hdr = next(r for r in rows if col in r)
+ei = hdr.index(col)
 agg = collections.Counter()
 text = {}
 cur = None
