@@ -5,20 +5,23 @@
 // self-synchronising: a decoder started at an arbitrary bit soon falls into
 // step with the true decode. Each restart segment's (unstuffed) bits are cut
 // into kSubBits subsequences, one thread each:
-//   1. speculative pass: thread t decodes from the start of its subsequence
-//      with a guessed context (block slot 0, coefficient 0) and records the
-//      state at which it leaves the subsequence (bit position, slot, z);
+//   1. speculative pass: thread t warms up on subsequence t-1 from a guessed
+//      context (block slot 0, coefficient 0), then decodes its own bits and
+//      records its exit state (bit position, slot, coefficient index), its
+//      tally (blocks started, DC-difference sums per component) and, every
+//      kCpBits, checkpoints of its state -- of its own decode and of its
+//      warm-up over t-1 (two independent trajectories through each range);
 //   2. sync rounds: E_t = decode(E_{t-1}, subsequence t) until no state
 //      changes -- a fixed point is the true decode by induction (subsequence
-//      0 of a segment starts exact); unconverged images fall back;
-//   3. count pass: blocks started per subsequence -> exclusive scan -> the
-//      first block index of every subsequence;
-//   4. write pass: coefficients (DC as differences) into a zeroed dense int32
-//      buffer; DC prediction is a per-(segment, component) prefix sum.
-// Any anomaly on the true path (invalid code, DC size > 11, AC run past the
-// block, bits consumed past the segment) or a stream the GPU path does not
-// cover sends that image to the host decoder, which reproduces the
-// reference's exact error -- results are bit-identical either way.
+//      0 of a segment starts exact). A round decode stops as soon as it
+//      meets a recorded checkpoint state (the rest follows from the record),
+//      and a thread whose state changed carries it on through up to kChain
+//      following subsequences; unconverged images fall back;
+//   3. scan: per segment, exclusive sums of the tallies -> the first block
+//      and the DC predictions every subsequence starts from;
+//   4. write pass: every block is written whole (zeros included, DC
+//      prediction applied) by the thread it starts in, assembled in shared
+//      memory -- the coefficient buffer needs no clearing and no second pass.
 #include <atomic>
 #include <chrono>
 #include <cstdlib>
@@ -48,7 +51,7 @@ constexpr int kSyncChunks = 32;   // cap: images still changing after this fall 
 #define FV_JPEG_WARM_BITS 1024
 #endif
 #ifndef FV_JPEG_CP_BITS
-#define FV_JPEG_CP_BITS 64
+#define FV_JPEG_CP_BITS 128
 #endif
 constexpr int kChain = FV_JPEG_CHAIN;    // subsequences one thread may carry a changed state through per round
 constexpr int kChain0 = FV_JPEG_CHAIN0;  // ... in the first (full) round
@@ -195,13 +198,30 @@ struct Tally {
   }
 };
 
+// The speculative pass's records for subsequence t, of two trajectories
+// through t's bits: 0 = t's own decode, 1 = the warm-up decode of thread t+1
+// (which starts at t's first bit with a guessed context, so it is an
+// independent second chance to be in step). A round decode of t that meets
+// either at a checkpoint is done: exit state and tally follow from that
+// trajectory's records. Meeting trajectory 1 also ends a propagation chain
+// at once: its exit state is where t+1's own decode started.
+struct SpecRec {
+  uint64_t* st[2];    // [kCp][nsub] states at the checkpoints (kNoState: none)
+  int4* tal[2];       // [kCp][nsub] tallies from the range's start to the checkpoint
+  uint64_t* exit[2];  // [nsub] states at the range's end
+  int4* tot[2];       // [nsub] tallies over the range
+};
+constexpr bool kDual = kWarmBits == kSubBits;  // the warm-up covers exactly the preceding subsequence
+
 struct Ckpt {
-  uint64_t* st;    // [kCp][nsub] states
-  int4* tal;       // [kCp][nsub] the speculative decode's tally before the checkpoint
+  uint64_t* st0;   // record: the trajectory's states; match: trajectory 0's
+  uint64_t* st1;   // match: trajectory 1's states
+  int4* tal;       // record: the trajectory's tallies
   int64_t nsub, t;
   int64_t mark;    // next mark (bit position)
   int k;           // next checkpoint index
   int hit;         // match mode: the checkpoint matched, or -1
+  int traj;        // match mode: the trajectory matched
 };
 
 // Write mode's block addressing: the MCU position (mx, my) of the current
@@ -273,14 +293,16 @@ __device__ uint64_t decode_run(const DevHuff* tabs, const DevImg& im, DBits& b, 
     if (CPM != kCpNone && pos >= ck->mark && ck->k < kCp) {
       const uint64_t st = pack_state(pos, slot, z);
       if (CPM == kCpMatch) {
-        if (ck->st[ck->k * ck->nsub + ck->t] == st) {
+        const int64_t idx = ck->k * ck->nsub + ck->t;
+        if (ck->st0[idx] == st || ck->st1[idx] == st) {
           ck->hit = ck->k;
+          ck->traj = ck->st0[idx] == st ? 0 : 1;
           break;
         }
       }
       do {  // every mark this boundary is the first at or past
         if (CPM == kCpRecord) {
-          ck->st[ck->k * ck->nsub + ck->t] = st;
+          ck->st0[ck->k * ck->nsub + ck->t] = st;
           ck->tal[ck->k * ck->nsub + ck->t] = tal->v();
         }
         ++ck->k;
@@ -405,7 +427,7 @@ __device__ __forceinline__ void sub_range(const Pass& P, int64_t t, const DevSeg
 }
 
 __global__ void __launch_bounds__(128) k_spec(const __grid_constant__ Pass P, uint64_t* E, int4* tally,
-                                              uint64_t* Es, int4* spec_tally, uint64_t* cp_st, int4* cp_tal) {
+                                              const __grid_constant__ SpecRec R) {
   const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= P.nsub) return;
   const DevSeg* sg;
@@ -415,22 +437,32 @@ __global__ void __launch_bounds__(128) k_spec(const __grid_constant__ Pass P, ui
   b.init(P.stream + sg->byte_off, sg->bits >> 3);
   int slot = 0, z = 0;
   int64_t pos = start;
+  if (local + 1 == sg->nsub)  // no thread warms up over this subsequence: no trajectory 1
+    for (int k = 0; k < kCp; ++k) R.st[1][k * P.nsub + t] = kNoState;
   if (kWarmBits > 0 && local > 0) {  // warm up on the preceding bits: enter this subsequence (likely) in step
     const int64_t w0 = start > (int64_t)kWarmBits ? start - (int64_t)kWarmBits : 0;
     b.start(w0);
-    const uint64_t e = decode_run<kModeSync>(P.huff, P.imgs[sg->img], b, 0, 0, start, false, 0, *sg, nullptr, nullptr, nullptr);
+    Tally wt;
+    Ckpt wk{R.st[1], nullptr, R.tal[1], P.nsub, t - 1, w0, 0, -1, 0};  // trajectory 1 of subsequence t-1
+    const uint64_t e = kDual ? decode_run<kModeSync, kCpRecord>(P.huff, P.imgs[sg->img], b, 0, 0, start, false, 0, *sg,
+                                                                nullptr, &wt, nullptr, &wk)
+                             : decode_run<kModeSync>(P.huff, P.imgs[sg->img], b, 0, 0, start, false, 0, *sg, nullptr,
+                                                     nullptr, nullptr);
+    for (int k = kDual ? wk.k : 0; k < kCp; ++k) R.st[1][k * P.nsub + t - 1] = kNoState;
+    R.exit[1][t - 1] = e;
+    R.tot[1][t - 1] = wt.v();
     unpack_state(e, pos, slot, z);
   }
   b.start(pos);
   Tally tl;
-  Ckpt ck{cp_st, cp_tal, P.nsub, t, start, 0, -1};
+  Ckpt ck{R.st[0], nullptr, R.tal[0], P.nsub, t, start, 0, -1, 0};
   const uint64_t e =
       decode_run<kModeSync, kCpRecord>(P.huff, P.imgs[sg->img], b, slot, z, end, false, 0, *sg, nullptr, &tl, nullptr, &ck);
-  for (int k = ck.k; k < kCp; ++k) cp_st[k * P.nsub + t] = kNoState;
+  for (int k = ck.k; k < kCp; ++k) R.st[0][k * P.nsub + t] = kNoState;
   E[t] = e;
-  Es[t] = e;
+  R.exit[0][t] = e;
   tally[t] = tl.v();  // exact for each segment's first subsequence; the others are re-derived in the rounds
-  spec_tally[t] = tl.v();
+  R.tot[0][t] = tl.v();
 }
 
 // One propagation round over a work queue: for each queued subsequence t,
@@ -449,8 +481,7 @@ __device__ __forceinline__ void enqueue(int32_t* qout, int* nout, int* mark, int
 
 __global__ void __launch_bounds__(128) k_round(const __grid_constant__ Pass P, uint64_t* E, int4* tally,
                                                const int32_t* qin, const int* nin, int32_t* qout, int* nout, int* mark,
-                                               int round, int all_subs, int chain, const uint64_t* Es,
-                                               const int4* spec_tally, uint64_t* cp_st, int4* cp_tal) {
+                                               int round, int all_subs, int chain, const __grid_constant__ SpecRec R) {
   const int64_t n = all_subs ? P.nsub : *nin;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     int64_t t = all_subs ? i : qin[i];
@@ -462,9 +493,9 @@ __global__ void __launch_bounds__(128) k_round(const __grid_constant__ Pass P, u
     for (int step = 0;; ++step) {
       uint64_t e;
       Tally tl;
-      if (in == cp_st[t]) {  // entered in the speculative decode's own entry state
-        e = Es[t];
-        tl.add(spec_tally[t], make_int4(0, 0, 0, 0));
+      if (in == R.st[0][t]) {  // entered in the speculative decode's own entry state
+        e = R.exit[0][t];
+        tl.add(R.tot[0][t], make_int4(0, 0, 0, 0));
       } else {
         int64_t pos;
         int slot, z;
@@ -472,12 +503,12 @@ __global__ void __launch_bounds__(128) k_round(const __grid_constant__ Pass P, u
         DBits b;
         b.init(P.stream + sg->byte_off, sg->bits >> 3);
         b.start(pos);
-        Ckpt ck{cp_st, cp_tal, P.nsub, t, start, 0, -1};
+        Ckpt ck{R.st[0], R.st[1], nullptr, P.nsub, t, start, 0, -1, 0};
         e = decode_run<kModeSync, kCpMatch>(P.huff, P.imgs[sg->img], b, slot, z, end, false, 0, *sg, nullptr, &tl, nullptr,
                                             &ck);
-        if (ck.hit >= 0) {  // merged with the speculative decode: its exit, the rest of its tally
-          e = Es[t];
-          tl.add(spec_tally[t], cp_tal[ck.hit * P.nsub + t]);
+        if (ck.hit >= 0) {  // merged with a speculative trajectory: its exit, the rest of its tally
+          e = R.exit[ck.traj][t];
+          tl.add(R.tot[ck.traj][t], R.tal[ck.traj][ck.hit * P.nsub + t]);
         }
       }
       // this subsequence's tally: the LAST processing of t used its
@@ -992,21 +1023,25 @@ struct GpuBatch {
     if (nimg == 0) return FV_OK;
   // 4. device buffers and passes
   DevBuf<uint8_t> dstage;  // images, segments, subsequence map, unstuffed bytes (the pinned staging's layout)
-  DevBuf<int4> dtally, dstally, dcptal, ddcb;
+  DevBuf<int4> dtally, dtot0, dtot1, dcptal0, dcptal1, ddcb;
   DevBuf<int32_t> dflags;
   DevBuf<int16_t> dcoef;
-  DevBuf<uint64_t> dE0, dEs, dcp;
+  DevBuf<uint64_t> dE0, dEs0, dEs1, dcp0, dcp1;
   DevBuf<int32_t> dq0, dq1, dmark;
   DevBuf<int64_t> dbase;
   int rc = FV_OK;
   rc = rc ? rc : dstage.alloc(stage_bytes, st);
   rc = rc ? rc : dtally.alloc(nsub, st);
-  rc = rc ? rc : dstally.alloc(nsub, st);
+  rc = rc ? rc : dtot0.alloc(nsub, st);
+  rc = rc ? rc : dtot1.alloc(nsub, st);
   rc = rc ? rc : ddcb.alloc(nsub, st);
   rc = rc ? rc : dE0.alloc(nsub, st);
-  rc = rc ? rc : dEs.alloc(nsub, st);
-  rc = rc ? rc : dcp.alloc((size_t)nsub * kCp, st);
-  rc = rc ? rc : dcptal.alloc((size_t)nsub * kCp, st);
+  rc = rc ? rc : dEs0.alloc(nsub, st);
+  rc = rc ? rc : dEs1.alloc(nsub, st);
+  rc = rc ? rc : dcp0.alloc((size_t)nsub * kCp, st);
+  rc = rc ? rc : dcp1.alloc((size_t)nsub * kCp, st);
+  rc = rc ? rc : dcptal0.alloc((size_t)nsub * kCp, st);
+  rc = rc ? rc : dcptal1.alloc((size_t)nsub * kCp, st);
   rc = rc ? rc : dq0.alloc(nsub, st);
   rc = rc ? rc : dq1.alloc(nsub, st);
   rc = rc ? rc : dmark.alloc(nsub, st);
@@ -1036,7 +1071,8 @@ struct GpuBatch {
     int* img_bad = dflags.p;
     int* changed = dflags.p + nimg;  // changed[r], r = 0 .. kSyncRounds
     timer.gpu("flags + memsets", st);
-    k_spec<<<grid, 128, 0, st>>>(P, dE0.p, dtally.p, dEs.p, dstally.p, dcp.p, dcptal.p);
+    const SpecRec R{{dcp0.p, dcp1.p}, {dcptal0.p, dcptal1.p}, {dEs0.p, dEs1.p}, {dtot0.p, dtot1.p}};
+    k_spec<<<grid, 128, 0, st>>>(P, dE0.p, dtally.p, R);
     timer.gpu("speculative pass", st);
     count_launch();
     uint64_t* Ein = dE0.p;
@@ -1051,8 +1087,7 @@ struct GpuBatch {
     for (int chunk = 0; chunk < kSyncChunks && !rc; ++chunk) {
       for (int k = 0; k < kSyncRounds; ++k, ++r) {
         k_round<<<r == 0 ? grid : qgrid, 128, 0, st>>>(P, Ein, dtally.p, qa, cnt + r, qb, cnt + r + 1, dmark.p, r + 1,
-                                                       r == 0, r == 0 ? kChain0 : kChain, dEs.p, dstally.p, dcp.p,
-                                                       dcptal.p);
+                                                       r == 0, r == 0 ? kChain0 : kChain, R);
         if (timer.on) timer.gpu(r == 0 ? "round 0 (all)" : "round k (queue)", st);
         count_launch();
         std::swap(qa, qb);
