@@ -17,7 +17,7 @@ echo "launch list rc=$?"
 for op in resize fused affine persp gray jpeg; do
   n=1; kre="regex:resize_|warp_|gray_u8"
   [ $op = resize ] && n=2
-  [ $op = jpeg ] && n=5 && kre="regex:k_spec|k_write|k_dcpred|jpeg_idct_batch|jpeg_color_batch"
+  [ $op = jpeg ] && n=10 && kre="regex:k_spec|k_round|k_write|jpeg_idct_batch|jpeg_color_batch"
   timeout 300 python tools/profile_ops.py --op $op --reps 1 > /dev/null 2>&1 && \
     timeout 900 ncu --set full --clock-control none --import-source on -k "$kre" -c $n \
       -o $out/${tag}_$op python tools/profile_ops.py --op $op --reps 1 > $out/${tag}_ncu_$op.log 2>&1
