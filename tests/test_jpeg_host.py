@@ -125,3 +125,59 @@ def test_implausible_header_rejected_before_allocation():
 def test_not_bytes_rejected():
     with pytest.raises(fv.CorruptStream):
         fio.jpeg_info("not bytes")
+
+
+def _info_batch(streams, threads):
+    import ctypes
+    from paper_2505_12425_b200 import _native
+    n = len(streams)
+    data = (ctypes.c_char_p * n)(*streams)
+    lens = (ctypes.c_int64 * n)(*[len(b) for b in streams])
+    infos = (_native.FvJpegInfo * n)()
+    status = (ctypes.c_int32 * n)()
+    assert _native.lib().fv_jpeg_info_batch(data, lens, n, infos, status, threads) == 0
+    return [(status[i], infos[i].width, infos[i].height, infos[i].ncomp, infos[i].coef_count) for i in range(n)]
+
+
+def test_worker_pool_concurrent_batches():
+    """The batch entry points share one persistent worker pool: concurrent
+    callers (ctypes drops the GIL) each get their own complete results."""
+    import threading
+    streams = [stream(n) for n in NAMES] * 4
+    want = _info_batch(streams, 1)
+    assert any(s == 0 for s, *_ in want) and any(s != 0 for s, *_ in want)
+    got, errs = {}, []
+
+    def run(k):
+        try:
+            for _ in range(20):
+                got[k] = _info_batch(streams, 1 + k % 5)
+                assert got[k] == want
+        except Exception as e:  # surfaced below
+            errs.append(e)
+
+    ts = [threading.Thread(target=run, args=(k,)) for k in range(6)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    assert not errs, errs
+    assert len(got) == 6
+
+
+@pytest.mark.skipif(not hasattr(os, "fork"), reason="fork")
+@pytest.mark.filterwarnings("ignore::DeprecationWarning")  # forking a multi-threaded process is the point
+def test_worker_pool_after_fork():
+    """A forked child (data-loader workers) gets a fresh pool: the parent's
+    threads do not exist there."""
+    streams = [stream(n) for n in NAMES]
+    want = _info_batch(streams, 4)  # the parent's pool exists now
+    pid = os.fork()
+    if pid == 0:  # child: must finish, and agree
+        try:
+            code = 0 if _info_batch(streams, 4) == want else 3
+        except BaseException:
+            code = 4
+        os._exit(code)
+    _, st = os.waitpid(pid, 0)
+    assert os.WIFEXITED(st) and os.WEXITSTATUS(st) == 0
