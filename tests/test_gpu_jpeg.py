@@ -52,6 +52,36 @@ def test_batch_matches_single(entropy):
         assert np.array_equal(o.cpu().numpy(), _Z[n + "__out"]), n
 
 
+def test_concurrent_batches_on_separate_streams():
+    """Several host threads decoding batches at once, each on its own CUDA
+    stream: the planner's worker pool, the pinned staging and the scratch
+    pool are shared; every result must still be exact."""
+    import threading
+    names = DECODED
+    data = [stream(n) for n in names]  # (the npz archive is read here: its lazy reader is not thread-safe)
+    want = [_Z[n + "__out"] for n in names]
+    errs = []
+
+    def run(k):
+        try:
+            s = torch.cuda.Stream()
+            with torch.cuda.stream(s):
+                for _ in range(4):
+                    outs = fio.decode_jpeg_batch(data, threads=1 + k)
+                    s.synchronize()
+                    for n, o, w in zip(names, outs, want):
+                        assert np.array_equal(o.cpu().numpy(), w), n
+        except Exception as e:  # surfaced below
+            errs.append(e)
+
+    ts = [threading.Thread(target=run, args=(k,)) for k in range(4)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    assert not errs, errs
+
+
 def test_batch_into_out_tensor():
     names = ["pil_ss0_q60", "pil_ss1_q85", "pil_ss2_q95"]  # same 77 x 129 x 3 frame
     out = torch.zeros((3, 77, 129, 3), dtype=torch.uint8, device="cuda")
