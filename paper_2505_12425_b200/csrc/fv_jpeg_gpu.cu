@@ -710,13 +710,24 @@ inline bool gpu_eligible(const Stream& s, const FvJpegInfo& f) {
   return f.coef_count > 0;
 }
 
-// Pinned host staging for the uploads, kept across calls (one caller at a
-// time: the call synchronises its stream before returning, so the buffer is
-// free again when the next call takes the lock).
+// Pinned host staging for the uploads and its device copy, kept across
+// calls (one caller at a time: the lock is held from the plan until the batch
+// is freed, and a call synchronises after the last pass that reads the device
+// copy, so both are free again when the next call takes the lock). The upload
+// runs on a per-device copy stream, so it can overlap whatever the caller's
+// stream is still executing (e.g. the previous batch's reconstruction).
 struct PinnedStage {
+  static constexpr int kMaxDev = 64;
+  struct Dev {
+    uint8_t* p = nullptr;
+    size_t cap = 0;
+    cudaStream_t copy = nullptr;
+    cudaEvent_t done = nullptr;
+  };
   std::mutex lock;
   uint8_t* p = nullptr;
   size_t cap = 0;
+  Dev dev[kMaxDev];
   uint8_t* get(size_t bytes) {
     if (bytes > cap) {
       if (p) cudaFreeHost(p);
@@ -727,6 +738,24 @@ struct PinnedStage {
       }
     }
     return p;
+  }
+  // the current device's copy (grown to `bytes`), or nullptr
+  Dev* device(size_t bytes) {
+    int d = 0;
+    if (cudaGetDevice(&d) != cudaSuccess || d < 0 || d >= kMaxDev) return nullptr;
+    Dev& x = dev[d];
+    if (!x.copy && cudaStreamCreateWithFlags(&x.copy, cudaStreamNonBlocking) != cudaSuccess) return nullptr;
+    if (!x.done && cudaEventCreateWithFlags(&x.done, cudaEventDisableTiming) != cudaSuccess) return nullptr;
+    if (bytes > x.cap) {
+      if (x.p) cudaFree(x.p);
+      x.cap = std::max(bytes, x.cap * 2);
+      if (cudaMalloc(reinterpret_cast<void**>(&x.p), x.cap) != cudaSuccess) {
+        x.p = nullptr;
+        x.cap = 0;
+        return nullptr;
+      }
+    }
+    return &x;
   }
 };
 inline PinnedStage& pinned_stage() {
@@ -934,7 +963,13 @@ struct GpuBatch {
   hseg = reinterpret_cast<DevSeg*>(sbase + o_seg);
   hsub = reinterpret_cast<int32_t*>(sbase + o_sub);
   hbytes = sbase + o_bytes;
-  parallel([&](int32_t i) {
+    timer.mark("tables + staging layout");
+    return FV_OK;
+  }
+
+  // image i's staging: its DevImg, segments, subsequence map and unstuffed
+  // bytes (worker threads; the upload of finished images runs meanwhile)
+  void stage_image(int32_t i) {
     if (!plan[i].gpu) return;
     const Stream& s = *plan[i].s;
     FvJpegInfo f;
@@ -1012,81 +1047,116 @@ struct GpuBatch {
       flush_lines(hbytes + bo, (size_t)((s.seg_len[k] + 15) / 16 * 16));
       bo += (s.seg_len[k] + 15) / 16 * 16;  // 16-byte aligned, zero padded (DBits reads whole words)
     }
-  });
-    timer.mark("unstuff + tables");
-    return FV_OK;
   }
+
 
   int run(uint8_t* planes, const int64_t* plane_off, uint8_t* const* dst, const int64_t* dst_pitch, int32_t* status,
           cudaStream_t st) {
     for (int32_t i = 0; i < n; ++i) status[i] = FV_EFALLBACK;
     if (nimg == 0) return FV_OK;
-  // 4. device buffers and passes
-  DevBuf<uint8_t> dstage;  // images, segments, subsequence map, unstuffed bytes (the pinned staging's layout)
-  DevBuf<int4> dtally, dtot0, dtot1, dcptal0, dcptal1, ddcb;
-  DevBuf<int32_t> dflags;
-  DevBuf<int16_t> dcoef;
-  DevBuf<uint64_t> dE0, dEs0, dEs1, dcp0, dcp1;
-  DevBuf<int32_t> dq0, dq1, dmark;
-  DevBuf<int64_t> dbase;
+  // 4. staging + upload: worker threads unstuff the images while this thread
+  // uploads each finished run of images (in input order) on the copy stream
+  PinnedStage::Dev* ds = pinned_stage().device(stage_bytes);
+  if (!ds) return set_error(FV_ECUDA, "fv_jpeg_decode_batch_gpu: device staging of %zu bytes", stage_bytes);
   int rc = FV_OK;
-  rc = rc ? rc : dstage.alloc(stage_bytes, st);
-  rc = rc ? rc : dtally.alloc(nsub, st);
-  rc = rc ? rc : dtot0.alloc(nsub, st);
-  rc = rc ? rc : dtot1.alloc(nsub, st);
-  rc = rc ? rc : ddcb.alloc(nsub, st);
-  rc = rc ? rc : dE0.alloc(nsub, st);
-  rc = rc ? rc : dEs0.alloc(nsub, st);
-  rc = rc ? rc : dEs1.alloc(nsub, st);
-  rc = rc ? rc : dcp0.alloc((size_t)nsub * kCp, st);
-  rc = rc ? rc : dcp1.alloc((size_t)nsub * kCp, st);
-  rc = rc ? rc : dcptal0.alloc((size_t)nsub * kCp, st);
-  rc = rc ? rc : dcptal1.alloc((size_t)nsub * kCp, st);
-  rc = rc ? rc : dq0.alloc(nsub, st);
-  rc = rc ? rc : dq1.alloc(nsub, st);
-  rc = rc ? rc : dmark.alloc(nsub, st);
-  rc = rc ? rc : dbase.alloc(nsub, st);
-  rc = rc ? rc : dcoef.alloc(ncoef, st);
-  const int nrounds = kSyncRounds * kSyncChunks;
-  rc = rc ? rc : dflags.alloc(nimg + nrounds + 2, st);
-  std::vector<int32_t> hflags(nimg + nrounds + 2, 0);
-  if (!rc) {
-    // hflags: img_bad[nimg] = 0, then the per-round queue lengths (all 0)
-    timer.gpu("start", st);
-    cudaMemcpyAsync(dstage.p, stage_base, stage_bytes, cudaMemcpyHostToDevice, st);
-    timer.gpu("h2d staging", st);
-    if (timer.on && getenv("FV_JPEG_TIMING2")) {
-      cudaMemcpyAsync(dstage.p, stage_base, stage_bytes, cudaMemcpyHostToDevice, st);
-      timer.gpu("h2d staging (again)", st);
+  {
+    std::unique_ptr<std::atomic<int32_t>[]> staged(new std::atomic<int32_t>[n]);
+    for (int32_t i = 0; i < n; ++i) staged[i].store(0, std::memory_order_relaxed);
+    WorkPool& wp = WorkPool::get();
+    WorkPool::Job job;
+    job.fn = [&](int32_t i) {
+      stage_image(i);
+      staged[i].store(1, std::memory_order_release);
+    };
+    job.n = n;
+    job.want = std::max(1, std::min(std::min<int>(nt, n), wp.size()));
+    wp.start(job);
+    size_t lo = o_bytes, hi = o_bytes;  // the pending byte run
+    auto flush = [&](bool last) {
+      if (hi > lo && (last || hi - lo >= (size_t(2) << 20))) {
+        if (cudaMemcpyAsync(ds->p + lo, stage_base + lo, hi - lo, cudaMemcpyHostToDevice, ds->copy) != cudaSuccess)
+          rc = rc ? rc : set_error(FV_ECUDA, "fv_jpeg_decode_batch_gpu: upload: %s", cudaGetErrorString(cudaGetLastError()));
+        lo = hi;
+      }
+    };
+    for (int32_t i = 0; i < n; ++i) {
+      while (!staged[i].load(std::memory_order_acquire)) std::this_thread::yield();
+      if (!plan[i].gpu) continue;
+      hi = o_bytes + (size_t)byte_off[i] + (size_t)((plan[i].bytes + 15) / 16 * 16);
+      flush(false);
     }
-    DevImg* const dimg_p = reinterpret_cast<DevImg*>(dstage.p + o_img);
-    DevSeg* const dseg_p = reinterpret_cast<DevSeg*>(dstage.p + o_seg);
-    const int32_t* const dsub_p = reinterpret_cast<const int32_t*>(dstage.p + o_sub);
-    const uint8_t* const dbytes_p = dstage.p + o_bytes;
-    cudaMemcpyAsync(dflags.p, hflags.data(), hflags.size() * sizeof(int32_t), cudaMemcpyHostToDevice, st);
+    flush(true);
+    wp.wait(job);
+    // tables, images, segments, subsequence map (written by the workers too)
+    if (cudaMemcpyAsync(ds->p, stage_base, o_bytes, cudaMemcpyHostToDevice, ds->copy) != cudaSuccess ||
+        cudaEventRecord(ds->done, ds->copy) != cudaSuccess || cudaStreamWaitEvent(st, ds->done, 0) != cudaSuccess)
+      rc = rc ? rc : set_error(FV_ECUDA, "fv_jpeg_decode_batch_gpu: upload: %s", cudaGetErrorString(cudaGetLastError()));
+  }
+  timer.mark("unstuff + upload");
+  // 5. device scratch (one stream-ordered allocation) and passes
+  size_t off = 0;
+  auto carve = [&](size_t bytes) {
+    const size_t o = off;
+    off += (bytes + 255) & ~size_t(255);
+    return o;
+  };
+  const int nrounds = kSyncRounds * kSyncChunks;
+  const size_t o_tally = carve(sizeof(int4) * nsub), o_tot0 = carve(sizeof(int4) * nsub),
+               o_tot1 = carve(sizeof(int4) * nsub), o_dcb = carve(sizeof(int4) * nsub),
+               o_cpt0 = carve(sizeof(int4) * nsub * kCp), o_cpt1 = carve(sizeof(int4) * nsub * kCp),
+               o_E0 = carve(sizeof(uint64_t) * nsub), o_Es0 = carve(sizeof(uint64_t) * nsub),
+               o_Es1 = carve(sizeof(uint64_t) * nsub), o_cp0 = carve(sizeof(uint64_t) * nsub * kCp),
+               o_cp1 = carve(sizeof(uint64_t) * nsub * kCp), o_q0 = carve(sizeof(int32_t) * nsub),
+               o_q1 = carve(sizeof(int32_t) * nsub), o_mark = carve(sizeof(int32_t) * nsub),
+               o_base = carve(sizeof(int64_t) * nsub), o_flags = carve(sizeof(int32_t) * (nimg + nrounds + 2));
+  DevBuf<uint8_t> scratch;
+  DevBuf<int16_t> dcoef;
+  rc = rc ? rc : scratch.alloc(off, st);
+  rc = rc ? rc : dcoef.alloc(ncoef, st);
+  auto at = [&](size_t o) { return scratch.p + o; };
+  int4* const tally_p = reinterpret_cast<int4*>(at(o_tally));
+  int4* const dcb_p = reinterpret_cast<int4*>(at(o_dcb));
+  uint64_t* const E0_p = reinterpret_cast<uint64_t*>(at(o_E0));
+  int32_t* const q0_p = reinterpret_cast<int32_t*>(at(o_q0));
+  int32_t* const q1_p = reinterpret_cast<int32_t*>(at(o_q1));
+  int32_t* const mark_p = reinterpret_cast<int32_t*>(at(o_mark));
+  int64_t* const base_p = reinterpret_cast<int64_t*>(at(o_base));
+  int32_t* const flags_p = reinterpret_cast<int32_t*>(at(o_flags));
+  std::vector<int32_t> hflags(nimg, 0);
+  if (!rc) {
+    timer.gpu("start (after the upload)", st);
+    DevImg* const dimg_p = reinterpret_cast<DevImg*>(ds->p + o_img);
+    DevSeg* const dseg_p = reinterpret_cast<DevSeg*>(ds->p + o_seg);
+    const int32_t* const dsub_p = reinterpret_cast<const int32_t*>(ds->p + o_sub);
+    const uint8_t* const dbytes_p = ds->p + o_bytes;
+    // img_bad[nimg] = 0, then the per-round queue lengths (all 0); the round marks
+    cudaMemsetAsync(flags_p, 0, sizeof(int32_t) * (nimg + nrounds + 2), st);
+    cudaMemsetAsync(mark_p, 0, nsub * sizeof(int32_t), st);
     // (no clearing of dcoef: the write pass stores every block whole)
-    cudaMemsetAsync(dmark.p, 0, nsub * sizeof(int32_t), st);
-    Pass P{reinterpret_cast<const DevHuff*>(dstage.p + o_huff), dimg_p, dseg_p, dsub_p, dbytes_p, nsub};
+    Pass P{reinterpret_cast<const DevHuff*>(ds->p + o_huff), dimg_p, dseg_p, dsub_p, dbytes_p, nsub};
     const unsigned grid = (unsigned)((nsub + 127) / 128);
-    int* img_bad = dflags.p;
-    int* changed = dflags.p + nimg;  // changed[r], r = 0 .. kSyncRounds
+    int* img_bad = flags_p;
+    int* changed = flags_p + nimg;  // changed[r], r = 0 .. kSyncRounds
     timer.gpu("flags + memsets", st);
-    const SpecRec R{{dcp0.p, dcp1.p}, {dcptal0.p, dcptal1.p}, {dEs0.p, dEs1.p}, {dtot0.p, dtot1.p}};
-    k_spec<<<grid, 128, 0, st>>>(P, dE0.p, dtally.p, R);
+    const SpecRec R{{reinterpret_cast<uint64_t*>(at(o_cp0)), reinterpret_cast<uint64_t*>(at(o_cp1))},
+                     {reinterpret_cast<int4*>(at(o_cpt0)), reinterpret_cast<int4*>(at(o_cpt1))},
+                     {reinterpret_cast<uint64_t*>(at(o_Es0)), reinterpret_cast<uint64_t*>(at(o_Es1))},
+                     {reinterpret_cast<int4*>(at(o_tot0)), reinterpret_cast<int4*>(at(o_tot1))}};
+    k_spec<<<grid, 128, 0, st>>>(P, E0_p, tally_p, R);
     timer.gpu("speculative pass", st);
     count_launch();
-    uint64_t* Ein = dE0.p;
+    uint64_t* Ein = E0_p;
     // rounds: the first over every subsequence, then over the queue of those
     // whose predecessor changed; after a chunk of rounds, one 4-byte readback
     // of the queue length decides whether another chunk is needed
-    int32_t* qa = dq0.p;
-    int32_t* qb = dq1.p;
+    int32_t* qa = q0_p;
+    int32_t* qb = q1_p;
     int* cnt = changed;  // cnt[r]: queue length produced by round r
     const unsigned qgrid = (unsigned)std::min<int64_t>((nsub + 127) / 128, 148 * 8);
     int r = 0;
     for (int chunk = 0; chunk < kSyncChunks && !rc; ++chunk) {
       for (int k = 0; k < kSyncRounds; ++k, ++r) {
-        k_round<<<r == 0 ? grid : qgrid, 128, 0, st>>>(P, Ein, dtally.p, qa, cnt + r, qb, cnt + r + 1, dmark.p, r + 1,
+        k_round<<<r == 0 ? grid : qgrid, 128, 0, st>>>(P, Ein, tally_p, qa, cnt + r, qb, cnt + r + 1, mark_p, r + 1,
                                                        r == 0, r == 0 ? kChain0 : kChain, R);
         if (timer.on) timer.gpu(r == 0 ? "round 0 (all)" : "round k (queue)", st);
         count_launch();
@@ -1113,8 +1183,8 @@ struct GpuBatch {
       for (int q = 1; q <= r; ++q) fprintf(stderr, " %d", ch[q]);
       fprintf(stderr, "\n");
     }
-    k_scan<<<(unsigned)nseg, 256, 0, st>>>(dseg_p, (int32_t)nseg, dtally.p, dbase.p, ddcb.p);
-    k_write<<<grid, 128, 0, st>>>(P, Ein, dbase.p, ddcb.p, dcoef.p, img_bad);
+    k_scan<<<(unsigned)nseg, 256, 0, st>>>(dseg_p, (int32_t)nseg, tally_p, base_p, dcb_p);
+    k_write<<<grid, 128, 0, st>>>(P, Ein, base_p, dcb_p, dcoef.p, img_bad);
     timer.gpu("scan + write", st);
     rc = check_launch("fv_jpeg_decode_batch_gpu passes");
     count_launch();
@@ -1123,7 +1193,7 @@ struct GpuBatch {
   timer.mark("scan + write");
   if (!rc) {
     // which images decoded cleanly (a second sync)
-    cudaMemcpyAsync(hflags.data(), dflags.p, nimg * sizeof(int32_t), cudaMemcpyDeviceToHost, st);
+    cudaMemcpyAsync(hflags.data(), flags_p, nimg * sizeof(int32_t), cudaMemcpyDeviceToHost, st);
     if (cudaStreamSynchronize(st) != cudaSuccess)
       rc = set_error(FV_ECUDA, "fv_jpeg_decode_batch_gpu: %s", cudaGetErrorString(cudaGetLastError()));
   }
