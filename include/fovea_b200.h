@@ -226,12 +226,17 @@ int fv_jpeg_decode_batch_gpu(const uint8_t* const* data, const int64_t* lens, in
 
 /* The same in two steps, so each stream is parsed once: fv_jpeg_batch_plan
  * parses the n streams (status[i] = FV_OK or the header error, infos[i] the
- * header when OK), unstuffs and stages the GPU path's inputs, and returns a
- * handle; the caller allocates the outputs from `infos`; fv_jpeg_batch_run_gpu
- * decodes (status[i] = FV_OK or FV_EFALLBACK as above; a NULL dst[i] skips
- * image i, e.g. the images from the first header error on); fv_jpeg_batch_free
- * releases the handle (it holds the library's pinned staging until then). The
- * stream bytes must stay alive until the handle is freed. */
+ * header when OK), lays out the GPU path's staging and returns a handle; the
+ * caller allocates the outputs from `infos`; fv_jpeg_batch_run_gpu unstuffs
+ * the streams on the library's worker threads while uploading each finished
+ * run of images on an internal per-device copy stream (ordered before the
+ * passes on `stream` by an event, so the upload may overlap work already
+ * queued on `stream`), then decodes (status[i] = FV_OK or FV_EFALLBACK as
+ * above; a NULL dst[i] skips image i, e.g. the images from the first header
+ * error on); it returns once the statuses are known, with the reconstruction
+ * still queued on `stream`. fv_jpeg_batch_free releases the handle (it holds
+ * the library's pinned and device staging until then: one batch at a time
+ * per process). The stream bytes must stay alive until the handle is freed. */
 int fv_jpeg_batch_plan(const uint8_t* const* data, const int64_t* lens, int32_t n, FvJpegInfo* infos, int32_t* status,
                        int32_t threads, void** handle);
 int fv_jpeg_batch_run_gpu(void* handle, uint8_t* planes, const int64_t* plane_off, uint8_t* const* dst,

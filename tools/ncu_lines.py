@@ -19,11 +19,15 @@ ei = hdr.index(col)
 agg = collections.Counter()
 text = {}
 cur = None
-for r in rows[rows.index(hdr) + 1:]:
-    if len(r) <= ei:
+fname = "?"
+for r in rows:
+    if r and r[0] == "File Path" and len(r) > 1:
+        fname = r[1].rsplit("/", 1)[-1]
+        continue
+    if len(r) <= ei or r is hdr:
         continue
     if r[0]:
-        cur = int(r[0]) if r[0].isdigit() else cur
+        cur = (fname, int(r[0])) if r[0].isdigit() else cur
         text[cur] = r[1]
     try:
         n = int(r[ei])
@@ -34,4 +38,5 @@ for r in rows[rows.index(hdr) + 1:]:
 tot = sum(agg.values())
 print("total", tot)
 for ln, n in agg.most_common(top):
-    print(f"{100 * n / tot:5.1f}% {n:>12d}  {ln}: {text.get(ln, '')[:100]}")
+    where = f"{ln[0]}:{ln[1]}" if ln else "?"
+    print(f"{100 * n / tot:5.1f}% {n:>12d}  {where}: {text.get(ln, '')[:100]}")
