@@ -1,17 +1,20 @@
 // fv_jpeg.cu -- decode -> preprocess: the reference's
 // baseline JPEG decoder (io/jpeg.py:605-806), bit-identical.
 //
-// Host (C++): marker walk, table parsing and the scan split with the
-// reference's checks and error classes, then canonical-Huffman entropy
-// decoding into quantised coefficients (natural order). This part is serial
-// per restart segment by the format; it runs on the CPU, thread-safe, one
-// image per thread in the batched Python wrapper.
+// Host (C++, fv_jpeg_host.cuh): marker walk, table parsing and the scan
+// split with the reference's checks and error classes, and the host
+// canonical-Huffman entropy decoder (natural-order coefficients) used by the
+// single-image path, the host batch path and the GPU path's fallback. The
+// GPU entropy decoder is fv_jpeg_gpu.cu.
 // Device (sm_100a): dequantisation + the 13-bit fixed-point "islow" IDCT
-// (8 threads per block, int64 like the reference's NumPy arithmetic, so any
-// stream -- including adversarial coefficient magnitudes -- gives the same
-// samples), then one kernel that upsamples the chroma planes with the
-// reference's integer triangle filters and converts YCbCr -> RGB (16-bit
-// fixed point), writing the HWC u8 image.
+// with the reference's NumPy int64 integers (int32 where no intermediate can
+// overflow, decided per warp), so any stream -- including adversarial
+// coefficient magnitudes -- gives the same samples; then one kernel that
+// upsamples the chroma planes with the reference's integer triangle filters
+// and converts YCbCr -> RGB (16-bit fixed point), writing the HWC u8 image.
+// The batch kernels (one launch each for a whole batch) serve the GPU path
+// and every dense int16 input; the per-image kernels below serve int32/int64
+// and the host batch runtime's sparse stream.
 #include <atomic>
 #include <thread>
 
