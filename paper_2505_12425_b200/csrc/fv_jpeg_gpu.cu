@@ -109,16 +109,16 @@ __device__ __forceinline__ void unpack_state(uint64_t s, int64_t& pos, int& slot
 // latency-bound).
 struct DBits {
   const uint32_t* w;  // the segment's words
-  int64_t nw;         // words holding data (the rest of the segment's padding reads as zero too)
-  int64_t cur;        // index of `nxt`
+  int nw;             // words holding data (the rest of the segment's padding reads as zero too)
+  int cur;            // index of `nxt` (segments stay below 2^27 bytes: gpu_eligible)
   uint64_t acc;
   uint32_t nxt;
   int nb;
   __device__ __forceinline__ void init(const uint8_t* seg, int64_t nbytes) {
     w = reinterpret_cast<const uint32_t*>(seg);
-    nw = (nbytes + 3) >> 2;
+    nw = (int)((nbytes + 3) >> 2);
   }
-  __device__ __forceinline__ uint32_t word(int64_t i) const {
+  __device__ __forceinline__ uint32_t word(int i) const {
     return i < nw ? __byte_perm(__ldg(w + i), 0, 0x0123) : 0u;
   }
   // after fill(): at least 33 bits buffered (a symbol takes at most 16 + 15)
@@ -130,7 +130,7 @@ struct DBits {
     }
   }
   __device__ __forceinline__ void start(int64_t bit) {
-    const int64_t c = bit >> 5;
+    const int c = (int)(bit >> 5);
     const int off = (int)(bit & 31);
     if (c + 32 < nw) asm volatile("prefetch.global.L1 [%0];" ::"l"(w + c + 32));  // the next line's words
     acc = (((uint64_t)word(c) << 32) | word(c + 1)) << off;
@@ -143,7 +143,7 @@ struct DBits {
     acc <<= k;
     nb -= k;
   }
-  __device__ __forceinline__ int64_t pos() const { return cur * 32 - nb; }
+  __device__ __forceinline__ int pos() const { return cur * 32 - nb; }
 };
 
 // one Huffman symbol; -1 = no code matches
@@ -187,7 +187,10 @@ enum { kCpNone = 0, kCpRecord = 1, kCpMatch = 2 };
 struct Tally {
   int32_t n = 0, d0 = 0, d1 = 0, d2 = 0;
   __device__ __forceinline__ int32_t add_dc(int e, int32_t diff) {
-    return e == 0 ? (d0 += diff) : (e == 1 ? (d1 += diff) : (d2 += diff));
+    d0 += e == 0 ? diff : 0;
+    d1 += e == 1 ? diff : 0;
+    d2 += e == 2 ? diff : 0;
+    return e == 0 ? d0 : (e == 1 ? d1 : d2);
   }
   __device__ __forceinline__ int4 v() const { return make_int4(n, d0, d1, d2); }
   __device__ __forceinline__ void add(int4 a, int4 b) {  // += a - b
@@ -280,17 +283,22 @@ __device__ uint64_t decode_run(const DevHuff* tabs, const DevImg& im, DBits& b, 
   const DevHuff* tac = tabs + im.ac_t[(slot_e >> (2 * slot)) & 3];  // the current block's AC table
   BlockPos bp;
   if (MODE == kModeWrite) bp.init(im, sg, z != 0 ? blk - 1 : blk, coef);
+  // sync modes: the next position at which something happens (the range's
+  // end or the next checkpoint mark) -- one compare per symbol
+  const int end32 = (int)end_bit;
+  int ev = end32;
+  if (CPM != kCpNone) ev = ck->k < kCp ? min(end32, (int)ck->mark) : end32;
   for (;;) {
-    const int64_t pos = b.pos();
+    const int pos = b.pos();
     if (MODE == kModeWrite && last_sub) {
       if (blk >= limit && z == 0) break;              // the segment's blocks are done
       if (pos > seg_bits + 64 * 16) { *bad = 1; break; }  // decoding deep into padding: corrupt
     } else if (MODE == kModeWrite) {
-      if (pos >= end_bit && z == 0) break;  // past the range and between blocks
-    } else if (pos >= end_bit) {
-      break;
+      if (pos >= end32 && z == 0) break;  // past the range and between blocks
+    } else if (pos >= ev) {
+      if (pos >= end32) break;
     }
-    if (CPM != kCpNone && pos >= ck->mark && ck->k < kCp) {
+    if (CPM != kCpNone && pos >= ev) {  // (not the end: a checkpoint mark)
       const uint64_t st = pack_state(pos, slot, z);
       if (CPM == kCpMatch) {
         const int64_t idx = ck->k * ck->nsub + ck->t;
@@ -308,6 +316,7 @@ __device__ uint64_t decode_run(const DevHuff* tabs, const DevImg& im, DBits& b, 
         ++ck->k;
         ck->mark += kCpBits;
       } while (ck->k < kCp && pos >= ck->mark);
+      ev = ck->k < kCp ? min(end32, (int)ck->mark) : end32;
     }
     b.fill();
     const int e = (slot_e >> (2 * slot)) & 3;
@@ -704,6 +713,8 @@ inline bool gpu_eligible(const Stream& s, const FvJpegInfo& f) {
     const int64_t per_seg = (int64_t)(s.dri ? s.dri : (int64_t)s.mcus_x * s.mcus_y) * c.h * c.v;
     if (per_seg * 2047 >= (1ll << 31)) return false;
   }
+  for (int64_t k = 0; k < (int64_t)s.seg_len.size(); ++k)
+    if (s.seg_len[k] >= (int64_t(1) << 27)) return false;  // the bit reader's positions are 32-bit
   int64_t per_mcu = 0;
   for (int e = 0; e < s.nscan; ++e) per_mcu += s.sof[s.scan_comp[e]].h * s.sof[s.scan_comp[e]].v;
   if (per_mcu > kMaxSlots) return false;
