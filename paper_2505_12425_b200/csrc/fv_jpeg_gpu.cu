@@ -37,6 +37,10 @@ namespace jpg {
 #define FV_JPEG_SUB_BITS 1024
 #endif
 constexpr int kSubBits = FV_JPEG_SUB_BITS;
+// Device-only fast entry: an AC table's end-of-block code (<= 10 bits) as a
+// "full" entry with this flag, so the decoder's common path covers
+// coefficients and EOBs alike (86% of the symbols of typical q90 frames).
+constexpr int32_t kEob = 1 << 14;
 constexpr int kMaxSlots = 12;
 constexpr int kSyncRounds = 6;    // rounds per chunk (one 4-byte readback per chunk)
 constexpr int kSyncChunks = 32;   // cap: images still changing after this fall back
@@ -356,16 +360,16 @@ __device__ uint64_t decode_run(const DevHuff* tabs, const DevImg& im, DBits& b, 
     } else {
       const DevHuff& t = *tac;
       const int32_t f = t.fast[b.peek(10)];
-      if (f & kFull) {
+      if (f & kFull) {  // a coefficient (run + value in one lookup) or an EOB: one branch-free path
         b.skip(f & 31);
-        z += (f >> 8) & 15;
-        if (z > 63) {
-          if (MODE == kModeWrite && dst) *bad = 1;
-          z = 64;
-        } else {
-          if (MODE == kModeWrite && dst) sb[zz[z]] = (int16_t)(f >> 16);
-          ++z;
+        const int zr = z + ((f >> 8) & 15);
+        const bool eob = (f & kEob) != 0;
+        const bool past = !eob && zr > 63;  // AC run past the block
+        if (MODE == kModeWrite && dst) {
+          if (past) *bad = 1;
+          if (!eob && !past) sb[zz[zr]] = (int16_t)(f >> 16);
         }
+        z = (eob || past) ? 64 : zr + 1;
       } else {
         const int rs = dsym(b, t, f);
         if (rs < 0) {
@@ -654,8 +658,11 @@ __global__ void __launch_bounds__(128) k_write(const __grid_constant__ Pass P, c
 // host planning
 // ---------------------------------------------------------------------------
 
-inline void to_dev_huff(const Huff& h, DevHuff& d) {
+inline void to_dev_huff(const Huff& h, DevHuff& d, bool dc) {
   memcpy(d.fast, h.fast, sizeof(d.fast));
+  if (!dc)
+    for (int x = 0; x < (1 << 10); ++x)
+      if ((d.fast[x] & kSym) && ((d.fast[x] >> 16) & 0xFF) == 0x00) d.fast[x] = kFull | kEob | (d.fast[x] & 31);
   for (int l = 0; l < 17; ++l) {
     d.maxcode[l] = h.maxcode[l];
     d.mincode[l] = h.mincode[l];
@@ -932,6 +939,7 @@ struct GpuBatch {
   struct Uniq {
     uint64_t key;
     const Huff* h;
+    bool dc;
   };
   std::vector<Uniq> uniq;
   for (int32_t i = 0; i < n; ++i) {
@@ -944,7 +952,7 @@ struct GpuBatch {
         const uint64_t key = plan[i].hkey[2 * e + cls];
         size_t u = 0;
         while (u < uniq.size() && !(uniq[u].key == key && huff_same(*uniq[u].h, h))) ++u;
-        if (u == uniq.size()) uniq.push_back({key, &h});
+        if (u == uniq.size()) uniq.push_back({key, &h, cls == 0});
         plan[i].tab[2 * e + cls] = (int32_t)u;
       }
   }
@@ -965,7 +973,7 @@ struct GpuBatch {
     std::unique_ptr<DevHuff> tmp(new DevHuff());
     for (size_t u = 0; u < uniq.size(); ++u) {  // class: the first use's (the key includes it)
       memset(tmp.get(), 0, sizeof(DevHuff));
-      to_dev_huff(*uniq[u].h, *tmp);
+      to_dev_huff(*uniq[u].h, *tmp, uniq[u].dc);
       memcpy(&hh[u], tmp.get(), sizeof(DevHuff));
     }
     flush_lines(hh, uniq.size() * sizeof(DevHuff));
