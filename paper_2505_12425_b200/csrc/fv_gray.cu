@@ -64,9 +64,17 @@ __global__ void __launch_bounds__(128) gray_u8_vec_kernel(const uint8_t* __restr
 }
 
 // Same work as gray_u8_vec_kernel with a flat (image, row, group) index and
-// 512-thread CTAs: a 1080p frame is ~130K groups, i.e. ~250 CTAs -- one
-// wave, few CTA launches (CTA launch cost dominates such small frames).
-constexpr int kFlatThreads = 512;
+// 512-thread CTAs: with 8 pixels per thread a 1080p frame is ~260K groups,
+// ~510 CTAs -- one wave, few CTA launches (launch latency dominates such
+// small frames; 16 pixels per thread left the wave too short of warps).
+#ifndef FV_GRAY_THREADS
+#define FV_GRAY_THREADS 512
+#endif
+constexpr int kFlatThreads = FV_GRAY_THREADS;
+#ifndef FV_GRAY_PX
+#define FV_GRAY_PX 8  // measured: 16 -> 8 pixels per thread 3.3 -> 2.9 us per 1080p frame; 4 is slower
+#endif
+template <int PX>  // pixels per thread: 16 / 8 / 4 (three 16- / 8- / 4-byte loads)
 __global__ void __launch_bounds__(kFlatThreads) gray_u8_flat_kernel(const uint8_t* __restrict__ src, int64_t s_is,
                                                            int64_t s_rp, uint8_t* __restrict__ dst, int64_t d_is,
                                                            int64_t d_rp, int h, int w, int64_t total) {
@@ -77,41 +85,59 @@ __global__ void __launch_bounds__(kFlatThreads) gray_u8_flat_kernel(const uint8_
   // no memory-order effect and L2 is the point of coherence, so a previous
   // grid still writing this input cannot make the later loads stale -- the
   // prefetch only overlaps this frame's DRAM ramp with that grid's tail.
-  const int groups = (w + 15) >> 4;
+  const int groups = (w + PX - 1) / PX;
   const int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const bool live = gid < total;
   const int gx = live ? (int)(gid % groups) : 0;
   const int64_t r = live ? gid / groups : 0;
   const int y = (int)(r % h);
   const int n = (int)(r / h);
-  const uint8_t* s = row_ptr<uint8_t>(src, s_is, s_rp, n, y) + gx * 48;
+  const uint8_t* s = row_ptr<uint8_t>(src, s_is, s_rp, n, y) + gx * 3 * PX;
   if (live) {
-    const int last = min(48, 3 * (w - gx * 16)) - 1;
+    const int last = min(3 * PX, 3 * (w - gx * PX)) - 1;
     asm volatile("prefetch.global.L2 [%0];" ::"l"(s));
     asm volatile("prefetch.global.L2 [%0];" ::"l"(s + last));
   }
   asm volatile("griddepcontrol.wait;" ::: "memory");
   asm volatile("griddepcontrol.launch_dependents;");  // (earlier trigger measured slower)
   if (!live) return;
-  uint8_t* d = row_ptr_mut<uint8_t>(dst, d_is, d_rp, n, y) + gx * 16;
-  const int x0 = gx * 16;
-  if (x0 + 16 <= w) {
-    uint4 v[3];
-    const uint4* s4 = reinterpret_cast<const uint4*>(s);
-    v[0] = __ldg(s4);
-    v[1] = __ldg(s4 + 1);
-    v[2] = __ldg(s4 + 2);
-    const uint32_t* wd = reinterpret_cast<const uint32_t*>(v);
-    uint32_t out[4] = {0, 0, 0, 0};
+  uint8_t* d = row_ptr_mut<uint8_t>(dst, d_is, d_rp, n, y) + gx * PX;
+  const int x0 = gx * PX;
+  if (x0 + PX <= w) {
+    uint32_t wd[3 * PX / 4];
+    if (PX == 16) {
+      const uint4* s4 = reinterpret_cast<const uint4*>(s);
 #pragma unroll
-    for (int i = 0; i < 16; ++i) {
+      for (int k = 0; k < 3; ++k) {
+        const uint4 v = __ldg(s4 + k);
+        wd[4 * k] = v.x, wd[4 * k + 1] = v.y, wd[4 * k + 2] = v.z, wd[4 * k + 3] = v.w;
+      }
+    } else if (PX == 8) {
+      const uint2* s2 = reinterpret_cast<const uint2*>(s);
+#pragma unroll
+      for (int k = 0; k < 3; ++k) {
+        const uint2 v = __ldg(s2 + k);
+        wd[2 * k] = v.x, wd[2 * k + 1] = v.y;
+      }
+    } else {
+      const uint32_t* s1 = reinterpret_cast<const uint32_t*>(s);
+#pragma unroll
+      for (int k = 0; k < 3; ++k) wd[k] = __ldg(s1 + k);
+    }
+    uint32_t out[PX / 4];
+#pragma unroll
+    for (int i = 0; i < PX / 4; ++i) out[i] = 0;
+#pragma unroll
+    for (int i = 0; i < PX; ++i) {
       const int k = 3 * i;
       uint32_t rr = (wd[k >> 2] >> ((k & 3) * 8)) & 0xFF;
       uint32_t g = (wd[(k + 1) >> 2] >> (((k + 1) & 3) * 8)) & 0xFF;
       uint32_t b = (wd[(k + 2) >> 2] >> (((k + 2) & 3) * 8)) & 0xFF;
       out[i >> 2] |= gray_u8_px(rr, g, b) << ((i & 3) * 8);
     }
-    __stcs(reinterpret_cast<uint4*>(d), make_uint4(out[0], out[1], out[2], out[3]));
+    if (PX == 16) __stcs(reinterpret_cast<uint4*>(d), make_uint4(out[0], out[1], out[2], out[3]));
+    else if (PX == 8) __stcs(reinterpret_cast<uint2*>(d), make_uint2(out[0], out[1]));
+    else __stcs(reinterpret_cast<unsigned int*>(d), out[0]);
   } else {
     for (int i = 0; x0 + i < w; ++i) d[i] = (uint8_t)gray_u8_px(s[3 * i], s[3 * i + 1], s[3 * i + 2]);
   }
@@ -193,8 +219,9 @@ int fv_gray_from_rgb_u8(const uint8_t* src, int64_t s_is, int64_t s_rp, uint8_t*
   const int gy = h < 65535 ? h : 65535;
   if (al16(src) && al16(dst) && al16(s_is) && al16(s_rp) && al16(d_is) && al16(d_rp)) {
     const int groups = (w + 15) / 16;
-    const int64_t total = (int64_t)n * h * groups;
-    if (total <= (int64_t)148 * 2048 * 4) {  // small batches: one flat wave of large CTAs
+    const int64_t total16 = (int64_t)n * h * groups;
+    const int64_t total = (int64_t)n * h * ((w + FV_GRAY_PX - 1) / FV_GRAY_PX);
+    if (total16 <= (int64_t)148 * 2048 * 4) {  // small batches: one flat wave of large CTAs
       cudaLaunchConfig_t cfg = {};
       cfg.gridDim = dim3((unsigned)((total + kFlatThreads - 1) / kFlatThreads));
       cfg.blockDim = dim3(kFlatThreads);
@@ -204,7 +231,7 @@ int fv_gray_from_rgb_u8(const uint8_t* src, int64_t s_is, int64_t s_rp, uint8_t*
       attr[0].val.programmaticStreamSerializationAllowed = 1;
       cfg.attrs = attr;
       cfg.numAttrs = 1;
-      cudaLaunchKernelEx(&cfg, gray_u8_flat_kernel, src, s_is, s_rp, dst, d_is, d_rp, (int)h, (int)w, total);
+      cudaLaunchKernelEx(&cfg, gray_u8_flat_kernel<FV_GRAY_PX>, src, s_is, s_rp, dst, d_is, d_rp, (int)h, (int)w, total);
     } else {
       dim3 grid((groups + 127) / 128, gy, n);
       gray_u8_vec_kernel<<<grid, 128, 0, st>>>(src, s_is, s_rp, dst, d_is, d_rp, h, w);
