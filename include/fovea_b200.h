@@ -130,6 +130,16 @@ int fv_warp_perspective_u8(const uint8_t* src, int64_t src_img_stride, int64_t s
                            uint8_t* dst, int64_t dst_img_stride, int64_t dst_row_pitch,
                            int32_t dst_height, int32_t dst_width, int32_t channels, int32_t n,
                            const double* hinv_host, uint8_t border, void* stream);
+/* u8 perspective within the north-star gate for u8 results of float
+ * interpolation: |out - exact| <= 1 LSB (same arguments and map). Per-thread
+ * f64 anchor + f32 projective correction (<= 5e-4 px per axis, checked per
+ * thread; the f64 per-pixel map where the bound fails), blend on the 0..255
+ * scale rounded half up. The headline cfg3 path. */
+int fv_warp_perspective_u8_fast(const uint8_t* src, int64_t src_img_stride, int64_t src_row_pitch,
+                                int32_t src_height, int32_t src_width,
+                                uint8_t* dst, int64_t dst_img_stride, int64_t dst_row_pitch,
+                                int32_t dst_height, int32_t dst_width, int32_t channels, int32_t n,
+                                const double* hinv_host, uint8_t border, void* stream);
 int fv_warp_perspective_f32(const float* src, int64_t src_img_stride, int64_t src_row_pitch,
                             int32_t src_height, int32_t src_width,
                             float* dst, int64_t dst_img_stride, int64_t dst_row_pitch,

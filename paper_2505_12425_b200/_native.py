@@ -40,6 +40,8 @@ SIGNATURES = {
                           _c.c_int),
     "fv_warp_perspective_u8": ([_P, _I64, _I64, _I32, _I32, _P, _I64, _I64, _I32, _I32, _I32, _I32, _P, _c.c_uint8,
                                 _P], _c.c_int),
+    "fv_warp_perspective_u8_fast": ([_P, _I64, _I64, _I32, _I32, _P, _I64, _I64, _I32, _I32, _I32, _I32, _P,
+                                     _c.c_uint8, _P], _c.c_int),
     "fv_warp_perspective_f32": ([_P, _I64, _I64, _I32, _I32, _P, _I64, _I64, _I32, _I32, _I32, _I32, _P, _c.c_float,
                                  _P], _c.c_int),
     "fv_resize_nearest": ([_P, _I64, _I64, _I32, _I32, _P, _I64, _I64, _I32, _I32, _I32, _I32, _I32, _P], _c.c_int),

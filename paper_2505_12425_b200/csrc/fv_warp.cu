@@ -654,6 +654,273 @@ __global__ void __launch_bounds__(256) warp_kernel_any(const __grid_constant__ W
   }
 }
 
+// ---------------------------------------------------------------------------
+// u8 perspective, <= 1 LSB (the north-star gate for u8 results of float
+// interpolation; SURVEY §7 hard part 2 asks for f32 / mixed coordinates
+// here). A warp covers 32 * PF_PX pixels of a row in groups of PF_PX:
+//   * one f64 anchor per group, computed by one lane and shared through
+//     SMEM: s_a = (X, Y)(x_a) / W(x_a); lane L then samples pixels
+//     x_w + L + 32 j (contiguous lanes: coalesced gathers and stores);
+//   * per pixel d = 0..7, exactly s(d) = s_a + k * d / W(d) with
+//     k = (m0 - s_a.x * m6, m3 - s_a.y * m6) and W(d) = W_a + m6 * d: the f32
+//     correction carries ~1e-7 RELATIVE error of a term of a few pixels, so
+//     the coordinates stay within ~1e-5 px of the f64 map (bound below);
+//   * the blend runs on the 0..255 scale (one rounding per FMA) and is
+//     rounded half up: sum_ij u_ij * w_ij + 0.5, floor.
+// Error budget against the exact recipe: |v_fast - v_exact| <= 255 * (Ex + Ey)
+// + ~3e-4 with Ex, Ey <= PF_MAX_ERR px (checked per thread, in f32, from the
+// anchor: the f64 per-pixel map takes over when the bound fails, W changes
+// sign or vanishes within the thread's pixels, or the anchor is non-finite
+// or beyond 2^22 px). Since bilinear sampling with a constant border is
+// continuous in (sx, sy) (a tap's weight reaches 0 exactly where it switches
+// between the image and the border), a shift of the integer tap across a
+// boundary changes nothing beyond the same bound, so |out - oracle| <= 1.
+// ---------------------------------------------------------------------------
+constexpr int PF_PX = 8;          // consecutive pixels per thread
+constexpr int PF_ROWS = 4;        // rows per thread (stride 8)
+constexpr float PF_MAX_ERR = 5e-4f;
+
+__device__ __forceinline__ float rcp_approx(float x) {
+  float r;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
+
+struct PfTap {
+  int x0, y0;
+  float fx, fy;
+};
+
+// Window of the two taps (x0, x0 + 1) of one source row, C bytes each, from
+// NWIN aligned 32-bit loads at byte offset `off` of a 4-byte aligned image;
+// the caller guarantees x0 <= sw - pf_safe<C>() so the window ends inside
+// the row. Returns magic words 0x4B0000uu.
+template <int C>
+constexpr int pf_nwin() { return (2 * C + 3 + 3) / 4; }
+template <int C>
+constexpr int pf_safe() { return (4 * pf_nwin<C>() + C - 1) / C; }
+template <int C>
+__device__ __forceinline__ void pf_row_taps(const uint8_t* img, uint32_t off, uint32_t (&t0)[C], uint32_t (&t1)[C]) {
+  constexpr int NW = pf_nwin<C>(), NV = (2 * C + 3) / 4;
+  const uint32_t* w = reinterpret_cast<const uint32_t*>(img + (off & ~3u));
+  uint32_t win[NW];
+#pragma unroll
+  for (int i = 0; i < NW; ++i) win[i] = __ldg(w + i);
+  const int sh = (int)(off & 3u) * 8;
+  uint32_t v[NV];
+#pragma unroll
+  for (int i = 0; i < NV; ++i) v[i] = __funnelshift_r(win[i], win[i + 1], sh);
+#pragma unroll
+  for (int c = 0; c < C; ++c) {
+    t0[c] = magic_of(v, c);
+    t1[c] = magic_of(v, C + c);
+  }
+}
+
+// One pixel of the <= 1 LSB perspective path with per-tap border handling
+// (taps at the source edge, all-outside pixels, rows near the buffer end).
+// The fast kernel calls it only from warps that hold such a pixel (a
+// warp-uniform branch), so its guarded loads never take issue slots in the
+// common path.
+template <int C>
+__device__ __forceinline__ void pf_pixel_generic(const WarpArgs& a, int n, int x0, int y0, float fx, float fy,
+                                              uint8_t* d) {
+  const uint32_t braw = (uint32_t)a.border_raw;
+  if (x0 < -1 || x0 >= a.sw || y0 < -1 || y0 >= a.sh) {
+    for (int c = 0; c < C; ++c) d[c] = (uint8_t)braw;
+    return;
+  }
+  const bool ix0 = x0 >= 0, ix1 = x0 + 1 < a.sw, iy0 = y0 >= 0, iy1 = y0 + 1 < a.sh;
+  const uint8_t* r0 = row_ptr<uint8_t>(a.src, a.s_is, a.s_rp, n, iy0 ? y0 : 0);
+  const uint8_t* r1 = row_ptr<uint8_t>(a.src, a.s_is, a.s_rp, n, iy1 ? y0 + 1 : 0);
+  const float wx0 = __fsub_rn(1.0f, fx), wy0 = __fsub_rn(1.0f, fy);
+  const float w00 = __fmul_rn(wx0, wy0), w01 = __fmul_rn(fx, wy0), w10 = __fmul_rn(wx0, fy), w11 = __fmul_rn(fx, fy);
+  const float b = (float)braw;
+  for (int c = 0; c < C; ++c) {
+    const float a00 = (iy0 && ix0) ? (float)__ldg(r0 + x0 * C + c) : b;
+    const float a01 = (iy0 && ix1) ? (float)__ldg(r0 + (x0 + 1) * C + c) : b;
+    const float a10 = (iy1 && ix0) ? (float)__ldg(r1 + x0 * C + c) : b;
+    const float a11 = (iy1 && ix1) ? (float)__ldg(r1 + (x0 + 1) * C + c) : b;
+    const float v = __fmaf_rn(a11, w11, __fmaf_rn(a10, w10, __fmaf_rn(a01, w01, __fmaf_rn(a00, w00, 0.5f))));
+    d[c] = (uint8_t)min((int)floorf(v), 255);
+  }
+}
+
+template <int C>
+__global__ void __launch_bounds__(256) warp_persp_fast_kernel(const __grid_constant__ WarpArgs a,
+                                                              const __grid_constant__ WarpMats mats) {
+  // anchors of the warp's 32 groups: {sxf, syf, kx, ky}, {W_a, ix_a, iy_a, fast}
+  __shared__ float4 anc[8][32][2];
+  const int n = blockIdx.z;
+  const int lane = threadIdx.x;
+  const int xw = blockIdx.x * (32 * PF_PX);
+  double m[9];
+#pragma unroll
+  for (int i = 0; i < 9; ++i) m[i] = mats.m[n][i];
+  const uint32_t braw = (uint32_t)a.border_raw;
+  const int y_end = min((int)blockIdx.y * 8 * PF_ROWS + 8 * PF_ROWS, a.dh);
+  const int y_first = blockIdx.y * 8 * PF_ROWS + threadIdx.y;
+  if (y_first >= y_end || xw >= a.dw) return;  // warp-uniform
+  // Whole-warp early out (as warp_kernel): the warp's region (32 * PF_PX
+  // columns x its rows) maps, W of one sign at its corners, onto the convex
+  // quadrilateral of the mapped corners; beyond one side of the source (2 px
+  // + 1e-6 relative margin) every tap is outside and every pixel is exactly
+  // the border (the weights sum to within 2^-21 of 1).
+  {
+    const int y_last = y_first + 8 * ((y_end - 1 - y_first) / 8);
+    int bits = 0;
+    if (lane < 4) {
+      const double cx = (double)((lane & 1) ? min(xw + 32 * PF_PX - 1, a.dw - 1) : xw);
+      const double cy = (double)((lane & 2) ? y_last : y_first);
+      const double X = m[0] * cx + m[1] * cy + m[2], Y = m[3] * cx + m[4] * cy + m[5];
+      const double W = m[6] * cx + m[7] * cy + m[8];
+      const double sx = X / W, sy = Y / W;
+      const double mx = 2.0 + 1e-6 * fabs(sx), my = 2.0 + 1e-6 * fabs(sy);
+      if (isfinite(sx) && isfinite(sy)) {
+        bits |= (sx < -1.0 - mx) ? 1 : 0;
+        bits |= (sx > (double)a.sw + mx) ? 2 : 0;
+        bits |= (sy < -1.0 - my) ? 4 : 0;
+        bits |= (sy > (double)a.sh + my) ? 8 : 0;
+      }
+      bits |= W > 0.0 ? 16 : (W < 0.0 ? 32 : 0);
+    }
+    const int all = __shfl_sync(0xffffffffu, bits, 0) & __shfl_sync(0xffffffffu, bits, 1) &
+                    __shfl_sync(0xffffffffu, bits, 2) & __shfl_sync(0xffffffffu, bits, 3);
+    if ((all & 48) && (all & 15)) {
+#pragma unroll 1
+      for (int y = y_first; y < y_end; y += 8) {
+        uint8_t* d = row_ptr_mut<uint8_t>(a.dst, a.d_is, a.d_rp, n, y);
+#pragma unroll
+        for (int j = 0; j < PF_PX; ++j) {
+          const int x = xw + lane + 32 * j;
+          if (x < a.dw) {
+#pragma unroll
+            for (int c = 0; c < C; ++c) d[x * C + c] = (uint8_t)braw;
+          }
+        }
+      }
+      return;
+    }
+  }
+  const float m6f = (float)m[6];
+  const float dlt = (float)(lane & (PF_PX - 1));
+  const uint8_t* simg = reinterpret_cast<const uint8_t*>(a.src) + (int64_t)n * a.s_is;
+  const uint32_t rp32 = (uint32_t)a.s_rp;
+  const unsigned xlim = (unsigned)(a.sw - pf_safe<C>()), ylim = (unsigned)(a.sh - 1);
+  const f2_t HALF = f2(0.5f, 0.5f), MAG = f2(8388608.0f, 8388608.0f), NMAG = f2(-8388608.0f, -8388608.0f);
+  float4(&A)[32][2] = anc[threadIdx.y];
+#pragma unroll 1
+  for (int y = y_first; y < y_end; y += 8) {
+    const double yd = (double)y;
+    const double rx = m[1] * yd + m[2], ry = m[4] * yd + m[5], rw = m[7] * yd + m[8];
+    {
+      // this lane's anchor: group `lane`, pixels xg .. xg + PF_PX - 1
+      const double xd = (double)(xw + PF_PX * lane);
+      const double Wa = m[6] * xd + rw;
+      const double We = Wa + m[6] * (double)(PF_PX - 1);
+      const double sa_x = (m[0] * xd + rx) / Wa, sa_y = (m[3] * xd + ry) / Wa;
+      bool fast = ((Wa > 0.0 && We > 0.0) || (Wa < 0.0 && We < 0.0)) && fabs(sa_x) < 4194304.0 &&
+                  fabs(sa_y) < 4194304.0;  // false for NaN too
+      const float kx = (float)(m[0] - sa_x * m[6]), ky = (float)(m[3] - sa_y * m[6]);
+      const float waf = (float)Wa;
+      if (fast) {
+        // per-axis bound (block comment): Cmax * 2^-23 * ((|Wa| + 7|m6|) / Wmin + 3) + 2^-22
+        const float iw = 1.0f / (float)fmin(fabs(Wa), fabs(We));
+        const float rho = (fabsf(waf) + (float)(PF_PX - 1) * fabsf(m6f)) * iw + 3.0f;
+        const float cx = fabsf(kx) * (float)(PF_PX - 1) * iw, cy = fabsf(ky) * (float)(PF_PX - 1) * iw;
+        const float ex = cx * rho * 1.1920929e-7f + 2.3841858e-7f, ey = cy * rho * 1.1920929e-7f + 2.3841858e-7f;
+        fast = ex <= PF_MAX_ERR && ey <= PF_MAX_ERR;  // false for inf / NaN
+      }
+      const double fxa = floor(sa_x), fya = floor(sa_y);
+      A[lane][0] = make_float4((float)(sa_x - fxa), (float)(sa_y - fya), kx, ky);
+      A[lane][1] = make_float4(waf, __int_as_float(fast ? (int)fxa : 0), __int_as_float(fast ? (int)fya : 0),
+                               __int_as_float(fast ? 1 : 0));
+    }
+    __syncwarp();
+    uint8_t* drow = row_ptr_mut<uint8_t>(a.dst, a.d_is, a.d_rp, n, y);
+#pragma unroll 1
+    for (int j = 0; j < PF_PX; j += 2) {
+      // pixels x_k = xw + lane + 32 * (j + k): lanes stay contiguous for the
+      // gathers; group (x_k - xw) / PF_PX holds the anchor, offset lane % 8
+      int tx0[2], ty0[2];
+      float tfx[2], tfy[2];
+#pragma unroll
+      for (int k = 0; k < 2; ++k) {
+        const int g = 4 * (j + k) + (lane >> 3);
+        const float4 q1 = A[g][1];
+        if (__float_as_int(q1.w)) {
+          const float4 q0 = A[g][0];
+          const float Wd = __fmaf_rn(m6f, dlt, q1.x);
+          const float r0 = rcp_approx(Wd);
+          const float r = __fmaf_rn(r0, __fmaf_rn(-Wd, r0, 1.0f), r0);  // one Newton step
+          const float tx = __fadd_rn(q0.x, __fmul_rn(__fmul_rn(q0.z, dlt), r));
+          const float ty = __fadd_rn(q0.y, __fmul_rn(__fmul_rn(q0.w, dlt), r));
+          const float flx = floorf(tx), fly = floorf(ty);
+          tfx[k] = __fsub_rn(tx, flx);
+          tfy[k] = __fsub_rn(ty, fly);
+          tx0[k] = __float_as_int(q1.y) + (int)flx;  // |.| < 2^23: no clamp needed
+          ty0[k] = __float_as_int(q1.z) + (int)fly;
+        } else {
+          // the f64 per-pixel map (warp_tap); non-finite -> every tap outside
+          const WarpTap w = warp_tap<true>(m, rx, ry, rw, min(xw + lane + 32 * (j + k), a.dw - 1), a.sw, a.sh);
+          tfx[k] = w.wx1;
+          tfy[k] = w.wy1;
+          tx0[k] = w.finite ? w.x0 : -2;
+          ty0[k] = w.finite ? w.y0 : -2;
+        }
+      }
+      const int xa = xw + lane + 32 * j, xb = xa + 32;
+      const bool va = xa < a.dw, vb = xb < a.dw;
+      // interior: all four taps inside and the load window inside the row
+      const bool easy = (!va || ((unsigned)tx0[0] <= xlim && (unsigned)ty0[0] < ylim)) &&
+                        (!vb || ((unsigned)tx0[1] <= xlim && (unsigned)ty0[1] < ylim));
+      if (!__all_sync(0xffffffffu, easy)) {
+        const bool ina = va && (unsigned)(tx0[0] + 1) <= (unsigned)a.sw && (unsigned)(ty0[0] + 1) <= (unsigned)a.sh;
+        const bool inb = vb && (unsigned)(tx0[1] + 1) <= (unsigned)a.sw && (unsigned)(ty0[1] + 1) <= (unsigned)a.sh;
+        if (!__any_sync(0xffffffffu, ina || inb)) {  // the warp's 64 pixels are all border
+#pragma unroll
+          for (int c = 0; c < C; ++c) {
+            if (va) drow[xa * C + c] = (uint8_t)braw;
+            if (vb) drow[xb * C + c] = (uint8_t)braw;
+          }
+        } else {
+          if (va) pf_pixel_generic<C>(a, n, tx0[0], ty0[0], tfx[0], tfy[0], drow + xa * C);
+          if (vb) pf_pixel_generic<C>(a, n, tx0[1], ty0[1], tfx[1], tfy[1], drow + xb * C);
+        }
+        continue;
+      }
+      uint32_t v00[2][C], v01[2][C], v10[2][C], v11[2][C];
+      {
+        // 32-bit offsets inside the image (host-checked: < 2^31), 4-byte
+        // aligned rows (host-checked): lanes past the edge load row 0
+        const uint32_t oa = va ? (uint32_t)ty0[0] * rp32 + (uint32_t)(tx0[0] * C) : 0u;
+        const uint32_t ob = vb ? (uint32_t)ty0[1] * rp32 + (uint32_t)(tx0[1] * C) : 0u;
+        pf_row_taps<C>(simg, oa, v00[0], v01[0]);
+        pf_row_taps<C>(simg, oa + rp32, v10[0], v11[0]);
+        pf_row_taps<C>(simg, ob, v00[1], v01[1]);
+        pf_row_taps<C>(simg, ob + rp32, v10[1], v11[1]);
+      }
+      const f2_t WX1 = f2(tfx[0], tfx[1]), WY1 = f2(tfy[0], tfy[1]);
+      const f2_t WX0 = fadd2(f2(1.0f, 1.0f), fmul2(WX1, f2(-1.0f, -1.0f)));
+      const f2_t WY0 = fadd2(f2(1.0f, 1.0f), fmul2(WY1, f2(-1.0f, -1.0f)));
+      const f2_t W00 = fmul2(WX0, WY0), W01 = fmul2(WX1, WY0), W10 = fmul2(WX0, WY1), W11 = fmul2(WX1, WY1);
+      uint8_t* pa = drow + xa * C;
+      uint8_t* pb = drow + xb * C;
+#pragma unroll
+      for (int c = 0; c < C; ++c) {
+        const f2_t A00 = fadd2(f2u(v00[0][c], v00[1][c]), NMAG), A01 = fadd2(f2u(v01[0][c], v01[1][c]), NMAG);
+        const f2_t A10 = fadd2(f2u(v10[0][c], v10[1][c]), NMAG), A11 = fadd2(f2u(v11[0][c], v11[1][c]), NMAG);
+        const f2_t v = ffma2(A11, W11, ffma2(A10, W10, ffma2(A01, W01, ffma2(A00, W00, HALF))));
+        uint32_t lo, hi;
+        f2split(fadd2_rd(v, MAG), lo, hi);  // floor(v) in the low byte (0 <= v < 256)
+        if (va) pa[c] = (uint8_t)(lo & 0xFF);
+        if (vb) pb[c] = (uint8_t)(hi & 0xFF);
+      }
+    }
+    __syncwarp();
+  }
+}
+
 static int g_warp_path = 0;  // 0 auto, 1 direct gathers only, 2 bulk-copy tiles (fv_set_warp_path)
 static int g_warp_tma = 1;   // TMA-tensor tiles when available (path 0)
 
@@ -705,6 +972,64 @@ static int launch_tma(int dw, int dh, int nb, cudaStream_t st, const WarpArgs& a
   if (ensure_smem_attr(kern, smem, attr_mask) != FV_OK) return check_launch("warp_affine_tma_kernel (smem attribute)");
   dim3 grid((dw + AT - 1) / AT, (dh + 15) / 16, nb);
   kern<<<grid, dim3(32, 4), smem, st>>>(tm, a, mats);  // the tensor map first: 64-byte aligned at offset 0
+  return FV_OK;
+}
+
+template <typename InT, bool PERSP>
+static int launch_warp(const InT* src, int64_t s_is, int64_t s_rp, int sh, int sw, InT* dst, int64_t d_is,
+                       int64_t d_rp, int dh, int dw, int c, int n, const double* mats_host, int mat_len,
+                       float border_f, float border_raw, cudaStream_t st, const char* fn);
+
+// u8 perspective, <= 1 LSB path (warp_persp_fast_kernel); C outside {1, 3, 4}
+// takes the exact kernel (which meets the same gate trivially)
+static int launch_persp_fast(const uint8_t* src, int64_t s_is, int64_t s_rp, int sh, int sw, uint8_t* dst,
+                             int64_t d_is, int64_t d_rp, int dh, int dw, int c, int n, const double* mats_host,
+                             uint8_t border, cudaStream_t st, const char* fn) {
+  const float bf = (float)border / 255.0f;
+  // the fast kernel's 32-bit window loads want 4-byte aligned rows, offsets
+  // inside an image below 2^31 and rows at least one load window wide
+  const bool fits = (c == 1 || c == 3 || c == 4) && ((reinterpret_cast<uintptr_t>(src) | (uintptr_t)s_rp) & 3) == 0 &&
+                    (n <= 1 || (s_is & 3) == 0) && s_rp > 0 && (int64_t)sh * s_rp < ((int64_t)1 << 31) &&
+                    sw > 4 * 3 + 1;
+  if (!fits)
+    return launch_warp<uint8_t, true>(src, s_is, s_rp, sh, sw, dst, d_is, d_rp, dh, dw, c, n, mats_host, 9, bf,
+                                      (float)border, st, fn);
+  if (n < 0 || sh < 1 || sw < 1 || dh < 1 || dw < 1)
+    return set_error(FV_EINVAL, "%s: bad shape n=%d src=%dx%d dst=%dx%d c=%d", fn, n, sh, sw, dh, dw, c);
+  if ((int64_t)(dh + 8 * PF_ROWS - 1) / (8 * PF_ROWS) > 65535)
+    return set_error(FV_EINVAL, "%s: destination height %d too large", fn, dh);
+  if (n == 0) return FV_OK;
+  if (!src || !dst || !mats_host) return set_error(FV_EINVAL, "%s: null pointer", fn);
+  WarpArgs a{};
+  a.s_is = s_is;
+  a.s_rp = s_rp;
+  a.sh = sh;
+  a.sw = sw;
+  a.d_is = d_is;
+  a.d_rp = d_rp;
+  a.dh = dh;
+  a.dw = dw;
+  a.c = c;
+  a.border_f = bf;
+  a.border_raw = (float)border;
+  a.one2 = kOne2Bits;
+  a.zero_border = border == 0;
+  WarpMats mats;
+  for (int b = 0; b < n; b += MAXW) {
+    const int nb = (n - b) < MAXW ? (n - b) : MAXW;
+    for (int i = 0; i < nb; ++i)
+      for (int j = 0; j < 9; ++j) mats.m[i][j] = mats_host[(int64_t)(b + i) * 9 + j];
+    a.src = reinterpret_cast<const char*>(src) + (int64_t)b * s_is;
+    a.dst = reinterpret_cast<char*>(dst) + (int64_t)b * d_is;
+    dim3 grid((dw + 32 * PF_PX - 1) / (32 * PF_PX), (dh + 8 * PF_ROWS - 1) / (8 * PF_ROWS), nb);
+    switch (c) {
+      case 1: warp_persp_fast_kernel<1><<<grid, dim3(32, 8), 0, st>>>(a, mats); break;
+      case 3: warp_persp_fast_kernel<3><<<grid, dim3(32, 8), 0, st>>>(a, mats); break;
+      default: warp_persp_fast_kernel<4><<<grid, dim3(32, 8), 0, st>>>(a, mats); break;
+    }
+    const int rc = check_launch(fn);
+    if (rc) return rc;
+  }
   return FV_OK;
 }
 
@@ -812,6 +1137,13 @@ int fv_warp_perspective_u8(const uint8_t* src, int64_t s_is, int64_t s_rp, int32
   const float bf = (float)border / 255.0f;
   return launch_warp<uint8_t, true>(src, s_is, s_rp, sh, sw, dst, d_is, d_rp, dh, dw, c, n, hinv_host, 9, bf,
                                     (float)border, static_cast<cudaStream_t>(stream), "fv_warp_perspective_u8");
+}
+
+int fv_warp_perspective_u8_fast(const uint8_t* src, int64_t s_is, int64_t s_rp, int32_t sh, int32_t sw,
+                                uint8_t* dst, int64_t d_is, int64_t d_rp, int32_t dh, int32_t dw, int32_t c,
+                                int32_t n, const double* hinv_host, uint8_t border, void* stream) {
+  return launch_persp_fast(src, s_is, s_rp, sh, sw, dst, d_is, d_rp, dh, dw, c, n, hinv_host, border,
+                           static_cast<cudaStream_t>(stream), "fv_warp_perspective_u8_fast");
 }
 
 int fv_warp_perspective_f32(const float* src, int64_t s_is, int64_t s_rp, int32_t sh, int32_t sw, float* dst,

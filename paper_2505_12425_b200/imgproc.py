@@ -170,7 +170,7 @@ def _matrices(m, n: int, rows: int, inverse: bool) -> np.ndarray:
     return np.ascontiguousarray(inv[:, :rows])
 
 
-def _warp(src, dst, m, border, inverse, perspective):
+def _warp(src, dst, m, border, inverse, perspective, exact=True):
     s, d = as_image(src, "src"), as_image(dst, "dst")
     if s.dtype != d.dtype:
         raise UnsupportedDtype(f"source {s.dtype} and destination {d.dtype} must match")
@@ -187,7 +187,7 @@ def _warp(src, dst, m, border, inverse, perspective):
         b = int(border)
         if not 0 <= b <= 255:
             raise UnsupportedDtype(f"u8 border must be in [0, 255], got {border}")
-        fn, bval = f"fv_warp_{kind}_u8", b
+        fn, bval = f"fv_warp_{kind}_u8" + ("" if exact else "_fast"), b
     else:
         fn, bval = f"fv_warp_{kind}_f32", float(border)
     with torch.cuda.device(src.device):
@@ -203,11 +203,17 @@ def warp_affine(src: torch.Tensor, dst: torch.Tensor, m, border=0, inverse: bool
     _warp(src, dst, m, border, inverse, perspective=False)
 
 
-def warp_perspective(src: torch.Tensor, dst: torch.Tensor, h, border=0, inverse: bool = False) -> None:
+def warp_perspective(src: torch.Tensor, dst: torch.Tensor, h, border=0, inverse: bool = False,
+                     exact: bool = False) -> None:
     """Bilinear perspective warp into `dst` (absent from the reference). `h` is
     the forward 3x3 homography (or N of them), inverted once in f64 on the
-    host. Pixels whose inverse-mapped W is 0 get the raw border value."""
-    _warp(src, dst, h, border, inverse, perspective=True)
+    host. Pixels whose inverse-mapped W is 0 get the raw border value.
+
+    u8 images: by default within 1 LSB of the builder oracle (the north-star
+    gate for u8 results of float interpolation; f64 anchor + f32 projective
+    correction per 8 pixels, `fv_warp_perspective_u8_fast`); `exact=True`
+    runs the bit-exact f64-per-pixel kernel. f32 images are always exact."""
+    _warp(src, dst, h, border, inverse, perspective=True, exact=exact)
 
 
 # ---------------------------------------------------------------------------

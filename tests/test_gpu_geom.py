@@ -119,6 +119,8 @@ def test_no_writes_outside_destination(rng, path):
             ("gray", (n, 37, 53, 1), torch.uint8, lambda d: fv.gray_from_rgb(src, d)),
             ("affine", (n, 40, 50, c), torch.float32, lambda d: fv.warp_affine(srcf, d, synth.affine_forward(3, 53, 37))),
             ("persp", (n, 40, 50, c), torch.uint8, lambda d: fv.warp_perspective(src, d, synth.perspective_forward(4))),
+            ("persp_exact", (n, 40, 50, c), torch.uint8,
+             lambda d: fv.warp_perspective(src, d, synth.perspective_forward(4), exact=True)),
             ("nearest", (n, 19, 90, c), torch.uint8, lambda d: fv.resize_nearest(src, d)),
             ("flip", (n, 37, 53, c), torch.uint8, lambda d: fv.flip_horizontal(src, d)),
         ]
