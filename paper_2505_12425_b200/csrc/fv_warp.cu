@@ -668,28 +668,32 @@ __global__ void __launch_bounds__(256) warp_kernel_any(const __grid_constant__ W
 //   * the blend runs on the 0..255 scale (one rounding per FMA) and is
 //     rounded half up: sum_ij u_ij * w_ij + 0.5, floor.
 // Error budget against the exact recipe: |v_fast - v_exact| <= 255 * (Ex + Ey)
-// + ~3e-4 with Ex, Ey <= PF_MAX_ERR px (checked per thread, in f32, from the
-// anchor: the f64 per-pixel map takes over when the bound fails, W changes
-// sign or vanishes within the thread's pixels, or the anchor is non-finite
-// or beyond 2^22 px). Since bilinear sampling with a constant border is
-// continuous in (sx, sy) (a tap's weight reaches 0 exactly where it switches
-// between the image and the border), a shift of the integer tap across a
-// boundary changes nothing beyond the same bound, so |out - oracle| <= 1.
+// + ~3e-4 with Ex, Ey <= PF_MAX_ERR px, checked per group in f32 from the
+// anchor. With u = 2^-24, Cmax = |k| * 7 / Wmin (the largest correction)
+// and rho = (|W_a| + 7 |m6|) / Wmin: W(d) carries <= u * (rho + 1) relative
+// error (the f32 roundings of W_a and m6 and the FMA), rcp.approx <= 2u, k
+// and the two products u each, so the correction is off by <= Cmax * u *
+// (rho + 6) <= Cmax * 2^-23 * (rho + 4); the sum s_frac + c adds <= u * (1 +
+// Cmax) and s_frac's own rounding 2^-25, both inside the 2^-22 term. The
+// f64 per-pixel map (warp_tap) takes over when the bound fails, W changes
+// sign or vanishes within the group, or the anchor is non-finite or beyond
+// 2^22 px. Bilinear sampling with a constant border is continuous in
+// (sx, sy) (a tap's weight reaches 0 exactly where it switches between the
+// image and the border), so a shift of the integer tap across a boundary
+// changes nothing beyond the same bound: |out - oracle| <= 1 LSB.
 // ---------------------------------------------------------------------------
 constexpr int PF_PX = 8;          // consecutive pixels per thread
 constexpr int PF_ROWS = 4;        // rows per thread (stride 8)
 constexpr float PF_MAX_ERR = 5e-4f;
+#ifndef PF_MINB
+#define PF_MINB 4  // resident CTAs per SM the register budget is sized for
+#endif
 
 __device__ __forceinline__ float rcp_approx(float x) {
   float r;
   asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
   return r;
 }
-
-struct PfTap {
-  int x0, y0;
-  float fx, fy;
-};
 
 // Window of the two taps (x0, x0 + 1) of one source row, C bytes each, from
 // NWIN aligned 32-bit loads at byte offset `off` of a 4-byte aligned image;
@@ -747,7 +751,7 @@ __device__ __forceinline__ void pf_pixel_generic(const WarpArgs& a, int n, int x
 }
 
 template <int C>
-__global__ void __launch_bounds__(256) warp_persp_fast_kernel(const __grid_constant__ WarpArgs a,
+__global__ void __launch_bounds__(256, PF_MINB) warp_persp_fast_kernel(const __grid_constant__ WarpArgs a,
                                                               const __grid_constant__ WarpMats mats) {
   // anchors of the warp's 32 groups: {sxf, syf, kx, ky}, {W_a, ix_a, iy_a, fast}
   __shared__ float4 anc[8][32][2];
@@ -818,15 +822,16 @@ __global__ void __launch_bounds__(256) warp_persp_fast_kernel(const __grid_const
       const double xd = (double)(xw + PF_PX * lane);
       const double Wa = m[6] * xd + rw;
       const double We = Wa + m[6] * (double)(PF_PX - 1);
-      const double sa_x = (m[0] * xd + rx) / Wa, sa_y = (m[3] * xd + ry) / Wa;
+      const double ra = 1.0 / Wa;  // s_a only needs ~1e-10 px: one reciprocal for both axes
+      const double sa_x = (m[0] * xd + rx) * ra, sa_y = (m[3] * xd + ry) * ra;
       bool fast = ((Wa > 0.0 && We > 0.0) || (Wa < 0.0 && We < 0.0)) && fabs(sa_x) < 4194304.0 &&
                   fabs(sa_y) < 4194304.0;  // false for NaN too
       const float kx = (float)(m[0] - sa_x * m[6]), ky = (float)(m[3] - sa_y * m[6]);
       const float waf = (float)Wa;
       if (fast) {
-        // per-axis bound (block comment): Cmax * 2^-23 * ((|Wa| + 7|m6|) / Wmin + 3) + 2^-22
+        // per-axis bound (block comment): Cmax * 2^-23 * ((|Wa| + 7|m6|) / Wmin + 4) + 2^-22
         const float iw = 1.0f / (float)fmin(fabs(Wa), fabs(We));
-        const float rho = (fabsf(waf) + (float)(PF_PX - 1) * fabsf(m6f)) * iw + 3.0f;
+        const float rho = (fabsf(waf) + (float)(PF_PX - 1) * fabsf(m6f)) * iw + 4.0f;
         const float cx = fabsf(kx) * (float)(PF_PX - 1) * iw, cy = fabsf(ky) * (float)(PF_PX - 1) * iw;
         const float ex = cx * rho * 1.1920929e-7f + 2.3841858e-7f, ey = cy * rho * 1.1920929e-7f + 2.3841858e-7f;
         fast = ex <= PF_MAX_ERR && ey <= PF_MAX_ERR;  // false for inf / NaN
@@ -850,9 +855,7 @@ __global__ void __launch_bounds__(256) warp_persp_fast_kernel(const __grid_const
         const float4 q1 = A[g][1];
         if (__float_as_int(q1.w)) {
           const float4 q0 = A[g][0];
-          const float Wd = __fmaf_rn(m6f, dlt, q1.x);
-          const float r0 = rcp_approx(Wd);
-          const float r = __fmaf_rn(r0, __fmaf_rn(-Wd, r0, 1.0f), r0);  // one Newton step
+          const float r = rcp_approx(__fmaf_rn(m6f, dlt, q1.x));  // <= 1 ulp (bound term 2^-23)
           const float tx = __fadd_rn(q0.x, __fmul_rn(__fmul_rn(q0.z, dlt), r));
           const float ty = __fadd_rn(q0.y, __fmul_rn(__fmul_rn(q0.w, dlt), r));
           const float flx = floorf(tx), fly = floorf(ty);
