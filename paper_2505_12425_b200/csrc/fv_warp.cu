@@ -511,73 +511,62 @@ constexpr int tma_win_elems() {
   return sizeof(InT) == 4 ? 48 * C : (C == 3 ? 192 : (C == 4 ? 256 : 64));
 }
 
+// Thread 0's part of a staged tile: the source box spanned by the mapped
+// corners (every in-image tap of the tile lies in [floor(lo) - 2,
+// floor(hi) + 3]) and, when it fits the window, ONE 3-D tensor copy of the
+// window into `stage`, completing on `bar`. Returns {ex0, by0, staged}.
 template <typename InT, int C>
-#ifndef FV_AFFINE_MINB
-#define FV_AFFINE_MINB 9  // 9 x 23 KB windows per SM (measured: +0.7% over 8)
-#endif
-__global__ void __launch_bounds__(128, FV_AFFINE_MINB) warp_affine_tma_kernel(const __grid_constant__ CUtensorMap tmap,
-                                                                 const __grid_constant__ WarpArgs a,
-                                                                 const __grid_constant__ WarpMats mats) {
+__device__ __forceinline__ int3 affine_tma_issue(const CUtensorMap* tmap, const WarpArgs& a, const double (&m)[9], int n,
+                                                 int tx0, int ty0, uint8_t* stage, uint64_t* bar) {
+  constexpr int ES = (int)sizeof(InT);
+  constexpr int TH = 16;
+  constexpr int TBE = tma_win_elems<InT, C>();
+  constexpr int AL = 16 / ES;
+  double xlo = 0, xhi = 0, ylo = 0, yhi = 0;
+  bool fin = true;
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const double cx = (double)((k & 1) ? min(tx0 + AT, a.dw) - 1 : tx0);
+    const double cy = (double)((k & 2) ? min(ty0 + TH, a.dh) - 1 : ty0);
+    const double sx = __dadd_rn(__dmul_rn(m[0], cx), __dadd_rn(__dmul_rn(m[1], cy), m[2]));
+    const double sy = __dadd_rn(__dmul_rn(m[3], cx), __dadd_rn(__dmul_rn(m[4], cy), m[5]));
+    fin = fin && isfinite(sx) && isfinite(sy);
+    xlo = k ? fmin(xlo, sx) : sx;
+    xhi = k ? fmax(xhi, sx) : sx;
+    ylo = k ? fmin(ylo, sy) : sy;
+    yhi = k ? fmax(yhi, sy) : sy;
+  }
+  fin = fin && xlo > -1e9 && xhi < 1e9 && ylo > -1e9 && yhi < 1e9;
+  const int bx0 = fin ? (int)floor(xlo) - 2 : 0, by0 = fin ? (int)floor(ylo) - 2 : 0;
+  const int e0 = bx0 * C;
+  const int ex0 = (e0 >= 0 ? e0 : e0 - (AL - 1)) / AL * AL;  // floor to the alignment
+  const bool staged = fin && ((int)floor(xhi) + 4) * C - ex0 <= TBE && (int)floor(yhi) + 3 - by0 < TBH;
+  if (staged) {
+    mbar_expect_tx(bar, (uint32_t)(TBE * TBH * ES));
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], "
+        "[%5];" ::"r"(smem_u32(stage)),
+        "l"(reinterpret_cast<uint64_t>(tmap)), "r"(ex0), "r"(by0), "r"(n), "r"(smem_u32(bar))
+        : "memory");
+  }
+  return make_int3(ex0, by0, staged ? 1 : 0);
+}
+
+// The threads' part of one 32 x 16 tile: 4 pixels each (rows ly, ly + 4,
+// ly + 8, ly + 12), taps from the window at `stage` (window element (ex0,
+// by0) first) when staged, else direct gathers; blend and store.
+template <typename InT, int C>
+__device__ __forceinline__ void affine_tma_tile(const WarpArgs& a, const double (&m)[9], int n, int tx0, int ty0, int ex0,
+                                                int by0, bool staged, const uint8_t* stage, int lx, int ly) {
   constexpr int PB = C * (int)sizeof(InT);
   constexpr int ES = (int)sizeof(InT);
   constexpr int TH = 16, RS = TH / 4;
-  constexpr int TBE = tma_win_elems<InT, C>();  // window row, elements
-  constexpr int AL = 16 / ES;                   // start alignment, elements
-  extern __shared__ __align__(128) uint8_t smem[];
-  uint64_t* bar = reinterpret_cast<uint64_t*>(smem);
-  int* box = reinterpret_cast<int*>(smem + 16);  // ex0 (window's first element), by0, staged
-  uint8_t* stage = smem + 128;
-  const int n = blockIdx.z;
-  const int lx = threadIdx.x, ly = threadIdx.y;
-  const int tx0 = blockIdx.x * AT, ty0 = blockIdx.y * TH;
-  double m[9];
-#pragma unroll
-  for (int i = 0; i < 6; ++i) m[i] = mats.m[n][i];
-  m[6] = m[7] = m[8] = 0.0;
-  if (lx == 0 && ly == 0) {
-    double xlo = 0, xhi = 0, ylo = 0, yhi = 0;
-    bool fin = true;
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      const double cx = (double)((k & 1) ? min(tx0 + AT, a.dw) - 1 : tx0);
-      const double cy = (double)((k & 2) ? min(ty0 + TH, a.dh) - 1 : ty0);
-      const double sx = __dadd_rn(__dmul_rn(m[0], cx), __dadd_rn(__dmul_rn(m[1], cy), m[2]));
-      const double sy = __dadd_rn(__dmul_rn(m[3], cx), __dadd_rn(__dmul_rn(m[4], cy), m[5]));
-      fin = fin && isfinite(sx) && isfinite(sy);
-      xlo = k ? fmin(xlo, sx) : sx;
-      xhi = k ? fmax(xhi, sx) : sx;
-      ylo = k ? fmin(ylo, sy) : sy;
-      yhi = k ? fmax(yhi, sy) : sy;
-    }
-    // every in-image tap of the tile lies in [floor(lo) - 2, floor(hi) + 3]
-    fin = fin && xlo > -1e9 && xhi < 1e9 && ylo > -1e9 && yhi < 1e9;
-    const int bx0 = fin ? (int)floor(xlo) - 2 : 0, by0 = fin ? (int)floor(ylo) - 2 : 0;
-    const int e0 = bx0 * C;
-    const int ex0 = (e0 >= 0 ? e0 : e0 - (AL - 1)) / AL * AL;  // floor to the alignment
-    const bool staged = fin && ((int)floor(xhi) + 4) * C - ex0 <= TBE && (int)floor(yhi) + 3 - by0 < TBH;
-    box[0] = ex0;
-    box[1] = by0;
-    box[2] = staged;
-    if (staged) {
-      mbar_init(bar, 1);
-      fence_mbar_init();
-      mbar_expect_tx(bar, (uint32_t)(TBE * TBH * ES));
-      asm volatile(
-          "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], "
-          "[%5];" ::"r"(smem_u32(stage)),
-          "l"(reinterpret_cast<uint64_t>(&tmap)), "r"(ex0), "r"(by0), "r"(n), "r"(smem_u32(bar))
-          : "memory");
-    }
-  }
-  __syncthreads();
-  const int ex0 = box[0], by0 = box[1];
-  const bool staged = box[2] != 0;
+  constexpr int TBE = tma_win_elems<InT, C>();
   const int x = tx0 + lx;
+  if (x >= a.dw) return;
   const uint32_t bord = sizeof(InT) == 1 ? (0x4B000000u | (uint32_t)a.border_raw) : __float_as_uint(a.border_f);
   // element e of row y at sb + (y * TBE + e) * ES
   const uint32_t sb = smem_u32(stage) - (uint32_t)((by0 * TBE + ex0) * ES);
-  if (staged) mbar_wait_block(bar, 0);
-  if (x >= a.dw) return;
 #pragma unroll 1
   for (int half = 0; half < 2; ++half) {
     const int ya = ty0 + ly + 2 * RS * half, yb = ya + RS;
@@ -616,6 +605,37 @@ __global__ void __launch_bounds__(128, FV_AFFINE_MINB) warp_affine_tma_kernel(co
     InT* db = row_ptr_mut<InT>(a.dst, a.d_is, a.d_rp, n, okb ? yb : ya) + x * C;
     blend_store<InT, C>(a, t, v00, v01, v10, v11, da, db, okb);
   }
+}
+
+template <typename InT, int C>
+#ifndef FV_AFFINE_MINB
+#define FV_AFFINE_MINB 9  // 9 x 23 KB windows per SM (measured: +0.7% over 8)
+#endif
+__global__ void __launch_bounds__(128, FV_AFFINE_MINB) warp_affine_tma_kernel(const __grid_constant__ CUtensorMap tmap,
+                                                                 const __grid_constant__ WarpArgs a,
+                                                                 const __grid_constant__ WarpMats mats) {
+  extern __shared__ __align__(128) uint8_t smem[];
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem);
+  int* box = reinterpret_cast<int*>(smem + 16);  // ex0 (window's first element), by0, staged
+  uint8_t* stage = smem + 128;
+  const int n = blockIdx.z;
+  const int tx0 = blockIdx.x * AT, ty0 = blockIdx.y * 16;
+  double m[9];
+#pragma unroll
+  for (int i = 0; i < 6; ++i) m[i] = mats.m[n][i];
+  m[6] = m[7] = m[8] = 0.0;
+  if (threadIdx.x == 0 && threadIdx.y == 0) {
+    mbar_init(bar, 1);
+    fence_mbar_init();
+    const int3 b = affine_tma_issue<InT, C>(&tmap, a, m, n, tx0, ty0, stage, bar);
+    box[0] = b.x;
+    box[1] = b.y;
+    box[2] = b.z;
+  }
+  __syncthreads();
+  const bool staged = box[2] != 0;
+  if (staged) mbar_wait_block(bar, 0);
+  affine_tma_tile<InT, C>(a, m, n, tx0, ty0, box[0], box[1], staged, stage, threadIdx.x, threadIdx.y);
 }
 
 // Any channel count: same sampler, channel loop at run time.
@@ -969,11 +989,12 @@ static int launch_tma(int dw, int dh, int nb, cudaStream_t st, const WarpArgs& a
           const_cast<void*>(a.src), dims, strides, boxd, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
           CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
     return 1;
+  const int tiles_x = (dw + AT - 1) / AT, tiles_y = (dh + 15) / 16;
   auto kern = warp_affine_tma_kernel<InT, C>;
   const int smem = 128 + tma_win_elems<InT, C>() * TBH * (int)sizeof(InT);
   static unsigned long long attr_mask[2] = {0, 0};  // per instantiation
   if (ensure_smem_attr(kern, smem, attr_mask) != FV_OK) return check_launch("warp_affine_tma_kernel (smem attribute)");
-  dim3 grid((dw + AT - 1) / AT, (dh + 15) / 16, nb);
+  dim3 grid(tiles_x, tiles_y, nb);
   kern<<<grid, dim3(32, 4), smem, st>>>(tm, a, mats);  // the tensor map first: 64-byte aligned at offset 0
   return FV_OK;
 }

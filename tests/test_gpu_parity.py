@@ -286,6 +286,32 @@ class TestWarp:
         print(f"cfg3 fast path: {diff_px} of {out.size} u8 values differ by 1 LSB ({frac:.2e})")
         assert frac < 1e-3
 
+    @pytest.mark.parametrize("c", [1, 3, 4])
+    def test_perspective_fast_path_cases(self, rng, c):
+        """The <= 1 LSB u8 perspective kernel beyond cfg3: strong homographies
+        whose W changes sign inside the frame (the f64 per-pixel fallback),
+        zoom-in / zoom-out, non-zero borders, ragged widths (tail groups),
+        a batch with per-image matrices, and a crop view (offset rows)."""
+        h, w = 150, 301
+        a = rng.integers(0, 256, (3, h, w + 8, c), dtype=np.uint8)
+        mats = [
+            np.array([[1.0, 0.0, 0.0], [0.0, 1.0, 0.0], [0.004, 0.003, 1.0]]),     # W crosses 0 in the frame
+            np.array([[0.45, 0.02, 10.0], [-0.03, 0.5, 5.0], [1e-4, -2e-4, 1.0]]),  # zoom in
+            np.array([[2.6, 0.3, -40.0], [-0.2, 2.4, -20.0], [2e-3, 1e-3, 1.0]]),   # zoom out, strong tilt
+            np.array([[1.0, 0.1, 3.0], [-0.1, 1.0, 2.0], [-3e-3, 2e-3, 1.0]]),
+        ]
+        for hinv in mats:
+            for oh, ow, border, crop in [(h, w, 0, False), (97, 255, 17, False), (h, w, 255, True)]:
+                view = a[:, :, 5:w + 5] if crop else np.ascontiguousarray(a[:, :, :w])
+                src = cu(a)[:, :, 5:w + 5] if crop else cu(view)
+                dst = torch.zeros((3, oh, ow, c), dtype=torch.uint8, device=DEV)
+                fv.warp_perspective(src, dst, np.stack([hinv, hinv @ np.diag([1.0, 1.0, 1.0]), hinv]), border=border,
+                                    inverse=True)
+                got = host(dst)
+                for i in range(3):
+                    ref = O.warp_perspective(np.ascontiguousarray(view[i]), hinv, oh, ow, border=border)
+                    assert_within_gate(got[i], ref)
+
     @pytest.mark.parametrize("dtype", [np.uint8, np.float32])
     def test_small_shapes_with_border(self, rng, dtype, warp_path):
         for (h, w, oh, ow, c) in [(14, 17, 12, 19, 3), (5, 5, 9, 9, 1), (33, 20, 20, 33, 4)]:
