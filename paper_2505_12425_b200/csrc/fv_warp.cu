@@ -705,6 +705,10 @@ __global__ void __launch_bounds__(256) warp_kernel_any(const __grid_constant__ W
 constexpr int PF_PX = 8;          // consecutive pixels per thread
 constexpr int PF_ROWS = 4;        // rows per thread (stride 8)
 constexpr float PF_MAX_ERR = 5e-4f;
+#ifndef PF_JUNROLL
+#define PF_JUNROLL 1
+#endif
+constexpr int kPfJUnroll = PF_JUNROLL;  // pixel pairs per sampling-loop iteration
 #ifndef PF_MINB
 #define PF_MINB 4  // resident CTAs per SM the register budget is sized for
 #endif
@@ -863,7 +867,7 @@ __global__ void __launch_bounds__(256, PF_MINB) warp_persp_fast_kernel(const __g
     }
     __syncwarp();
     uint8_t* drow = row_ptr_mut<uint8_t>(a.dst, a.d_is, a.d_rp, n, y);
-#pragma unroll 1
+#pragma unroll kPfJUnroll
     for (int j = 0; j < PF_PX; j += 2) {
       // pixels x_k = xw + lane + 32 * (j + k): lanes stay contiguous for the
       // gathers; group (x_k - xw) / PF_PX holds the anchor, offset lane % 8
