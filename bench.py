@@ -621,7 +621,11 @@ def main():
 
     summary = {}
     for name, r in results.items():
-        summary[name] = {"dst_mps": job_mps(name), "ms_per_step": r["ms_per_step"], **r["op"].get("extra", {}),
+        # src_mps: the reference harness's convention (MP/s over SOURCE
+        # pixels, bench.py:151 of the reference); dst_mps is the primary basis
+        src_mps = job_mps(name) * r["op"]["src_px"] / r["op"]["dst_px"]
+        summary[name] = {"dst_mps": job_mps(name), "src_mps": src_mps, "ms_per_step": r["ms_per_step"],
+                         **r["op"].get("extra", {}),
                          "kernels": [{k: (round(v, 4) if isinstance(v, float) else v) for k, v in kk.items()}
                                      for kk in r["kernels"]],
                          "l2": r["op"]["l2"]}
