@@ -553,22 +553,18 @@ __device__ __forceinline__ int3 affine_tma_issue(const CUtensorMap* tmap, const 
 }
 
 // The threads' part of one 32 x 16 tile: 4 pixels each (rows ly, ly + 4,
-// ly + 8, ly + 12). The f64 maps of all four pixels are computed BEFORE
-// waiting for the window (`bar`, when staged), so that work overlaps the
-// tensor copy (0.398 -> 0.358 ms for cfg2; also precomputing the window
+// ly + 8, ly + 12). The f64 maps of all four pixels (affine_tile_maps) are
+// computed BEFORE waiting for the window (`bar`, when staged) -- and before
+// the CTA barrier that publishes the box -- so that work overlaps the box
+// and the tensor copy (0.398 -> 0.358 ms for cfg2; also precomputing the window
 // offsets, or mapping the box corners on four lanes, measured slower); then
 // taps come from the window at `stage` (window element (ex0, by0) first)
 // when staged, else from direct gathers; blend and store.
 template <typename InT, int C>
-__device__ __forceinline__ void affine_tma_tile(const WarpArgs& a, const double (&m)[9], int n, int tx0, int ty0,
-                                                int ex0, int by0, bool staged, const uint8_t* stage, uint64_t* bar,
-                                                int lx, int ly) {
-  constexpr int PB = C * (int)sizeof(InT);
-  constexpr int ES = (int)sizeof(InT);
-  constexpr int TH = 16, RS = TH / 4;
-  constexpr int TBE = tma_win_elems<InT, C>();
+__device__ __forceinline__ void affine_tile_maps(const WarpArgs& a, const double (&m)[9], int tx0, int ty0, int lx,
+                                                 int ly, WarpTap (&t)[2][2]) {
+  constexpr int RS = 4;
   const int x = tx0 + lx;
-  WarpTap t[2][2];
 #pragma unroll
   for (int half = 0; half < 2; ++half) {
     const int ya = ty0 + ly + 2 * RS * half, yb = ya + RS;
@@ -580,6 +576,17 @@ __device__ __forceinline__ void affine_tma_tile(const WarpArgs& a, const double 
       t[half][k] = warp_tap<false>(m, rx, ry, 0.0, x, a.sw, a.sh);
     }
   }
+}
+
+template <typename InT, int C>
+__device__ __forceinline__ void affine_tma_tile(const WarpArgs& a, const WarpTap (&t)[2][2], int n, int tx0, int ty0,
+                                                int ex0, int by0, bool staged, const uint8_t* stage, uint64_t* bar,
+                                                int lx, int ly) {
+  constexpr int PB = C * (int)sizeof(InT);
+  constexpr int ES = (int)sizeof(InT);
+  constexpr int TH = 16, RS = TH / 4;
+  constexpr int TBE = tma_win_elems<InT, C>();
+  const int x = tx0 + lx;
   if (staged) mbar_wait_block(bar, 0);
   if (x >= a.dw) return;
   const uint32_t bord = sizeof(InT) == 1 ? (0x4B000000u | (uint32_t)a.border_raw) : __float_as_uint(a.border_f);
@@ -642,8 +649,10 @@ __global__ void __launch_bounds__(128, FV_AFFINE_MINB) warp_affine_tma_kernel(co
     box[1] = b.y;
     box[2] = b.z;
   }
+  WarpTap t[2][2];
+  affine_tile_maps<InT, C>(a, m, tx0, ty0, threadIdx.x, threadIdx.y, t);
   __syncthreads();
-  affine_tma_tile<InT, C>(a, m, n, tx0, ty0, box[0], box[1], box[2] != 0, stage, bar, threadIdx.x, threadIdx.y);
+  affine_tma_tile<InT, C>(a, t, n, tx0, ty0, box[0], box[1], box[2] != 0, stage, bar, threadIdx.x, threadIdx.y);
 }
 
 // Any channel count: same sampler, channel loop at run time.
