@@ -104,13 +104,19 @@ __device__ __forceinline__ bool tap_outside(const WarpTap& t, int sw, int sh) {
 // u8 -> magic words 0x4B0000uu (converted later, two at a time), f32 -> bits.
 // u8, C = 3: three aligned 32-bit loads + two funnel shifts instead of six
 // byte loads.
+// SAFE: the caller guarantees x0 <= sw - kPairSafe<InT, C> (the wide window
+// ends inside the row), so the in-row test and its per-element fallback --
+// which ptxas if-converts into every gather -- are left out.
 template <typename InT, int C>
+constexpr int kPairSafe = (C == 3) ? (sizeof(InT) == 1 ? 4 : 3) : 2;  // generic: x0 + 1 < sw
+
+template <typename InT, int C, bool SAFE = false>
 __device__ __forceinline__ void load_pair_raw(const InT* row, int x0, int row_elems, uint32_t (&t0)[C],
                                               uint32_t (&t1)[C]) {
   if constexpr (sizeof(InT) == 1 && C == 3) {
     const uintptr_t p = reinterpret_cast<uintptr_t>(row) + 3 * x0;
     const uintptr_t al = p & ~(uintptr_t)3;
-    if (al + 12 <= reinterpret_cast<uintptr_t>(row) + row_elems) {
+    if (SAFE || al + 12 <= reinterpret_cast<uintptr_t>(row) + row_elems) {
       const uint32_t* w = reinterpret_cast<const uint32_t*>(al);
       const uint32_t w0 = __ldg(w), w1 = __ldg(w + 1), w2 = __ldg(w + 2);
       const int sh = (int)(p & 3) * 8;
@@ -130,7 +136,7 @@ __device__ __forceinline__ void load_pair_raw(const InT* row, int x0, int row_el
     // them for either 8-byte phase (4 LSU requests instead of 6)
     const uintptr_t p = reinterpret_cast<uintptr_t>(row) + 12 * x0;
     const uintptr_t al = p & ~(uintptr_t)7;
-    if (al + 32 <= reinterpret_cast<uintptr_t>(row) + 4 * row_elems) {
+    if (SAFE || al + 32 <= reinterpret_cast<uintptr_t>(row) + 4 * row_elems) {
       const uint2* w = reinterpret_cast<const uint2*>(al);
       const uint2 q0 = __ldg(w), q1 = __ldg(w + 1), q2 = __ldg(w + 2), q3 = __ldg(w + 3);
       const uint32_t v[8] = {q0.x, q0.y, q1.x, q1.y, q2.x, q2.y, q3.x, q3.y};
@@ -313,8 +319,25 @@ __global__ void __launch_bounds__(256, 4) warp_kernel(const __grid_constant__ Wa
       continue;
     }
     uint32_t v00[2][C], v01[2][C], v10[2][C], v11[2][C];
+    // warp-uniform fast path: every lane's taps interior with the wide load
+    // window inside the row (no per-thread fallback code in the common case)
+    bool easy = true;
 #pragma unroll
-    for (int k = 0; k < 2; ++k) gather_raw<InT, C>(a, n, t[k], bord, v00[k], v01[k], v10[k], v11[k]);
+    for (int k = 0; k < 2; ++k)
+      easy &= t[k].finite && t[k].x0 >= 0 && t[k].x0 <= a.sw - kPairSafe<InT, C> && t[k].y0 >= 0 &&
+              t[k].y0 + 1 < a.sh;
+    if (__all_sync(__activemask(), easy)) {
+#pragma unroll
+      for (int k = 0; k < 2; ++k) {
+        const InT* r0 = row_ptr<InT>(a.src, a.s_is, a.s_rp, n, t[k].y0);
+        const InT* r1 = row_ptr<InT>(a.src, a.s_is, a.s_rp, n, t[k].y0 + 1);
+        load_pair_raw<InT, C, true>(r0, t[k].x0, a.sw * C, v00[k], v01[k]);
+        load_pair_raw<InT, C, true>(r1, t[k].x0, a.sw * C, v10[k], v11[k]);
+      }
+    } else {
+#pragma unroll
+      for (int k = 0; k < 2; ++k) gather_raw<InT, C>(a, n, t[k], bord, v00[k], v01[k], v10[k], v11[k]);
+    }
 
     blend_store<InT, C>(a, t, v00, v01, v10, v11, d, d + 32 * C, two);
   }
