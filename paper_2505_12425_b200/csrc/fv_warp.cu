@@ -743,7 +743,10 @@ __global__ void __launch_bounds__(256) warp_kernel_any(const __grid_constant__ W
 // changes nothing beyond the same bound: |out - oracle| <= 1 LSB.
 // ---------------------------------------------------------------------------
 constexpr int PF_PX = 8;          // consecutive pixels per thread
-constexpr int PF_ROWS = 4;        // rows per thread (stride 8)
+#ifndef FV_PF_ROWS
+#define FV_PF_ROWS 8  // measured: 2 -> 0.586, 4 -> 0.560, 8 -> 0.552, 16 -> 0.571 ms (cfg3)
+#endif
+constexpr int PF_ROWS = FV_PF_ROWS;  // rows per thread (stride 8)
 constexpr float PF_MAX_ERR = 5e-4f;
 #ifndef PF_JUNROLL
 #define PF_JUNROLL 1
