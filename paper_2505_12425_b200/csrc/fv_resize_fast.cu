@@ -195,6 +195,9 @@ __device__ __forceinline__ void up2_emit_copy(uint8_t* drow, const f2_t (&h)[4 *
 // their 4-byte aligned windows with LDS (lane stride 12 B: conflict-free) and
 // release the slot on its "empty" mbarrier.
 constexpr int UP2_NCW = 3, UP2_GROUPS = UP2_NCW * 32, UP2_RING = 8;
+#ifndef UP2_BAND
+#define UP2_BAND 32  // source rows per CTA (one halo row re-read per band); 16 / 64 / 128 measured slower
+#endif
 
 template <int C>
 __device__ __forceinline__ void up2_lds(const uint8_t* seg_row_base, int t, uint32_t (&w)[Up2<C>::NW]) {
@@ -423,7 +426,7 @@ static int launch_fast_c(const FastArgs& a0, bool down, cudaStream_t st) {
     resize_down2_kernel<C><<<(unsigned)((total + 127) / 128), 128, 0, st>>>(a);
   } else {
     a.groups = a.sw / 4;
-    a.band = 32;
+    a.band = UP2_BAND;
     a.bands = (a.sh + a.band - 1) / a.band;
     // ring slot: the tile's source bytes (+ halo, + alignment), 16-byte padded
     // on both sides for the unused halo words of the edge groups
