@@ -821,7 +821,11 @@ template <int C>
 __global__ void __launch_bounds__(256, PF_MINB) warp_persp_fast_kernel(const __grid_constant__ WarpArgs a,
                                                               const __grid_constant__ WarpMats mats) {
   // anchors of the warp's 32 groups: {sxf, syf, kx, ky}, {W_a, ix_a, iy_a, fast}
-  __shared__ float4 anc[8][32][2];
+  // anchors of the warp's 32 groups, stored by group PAIR (g, g + 4) --
+  // the two groups a lane samples in one iteration -- so one LDS.128 yields
+  // a field of both as f32x2 operands: {sxf, syf}, {kx, ky}, {W_a, ix_a},
+  // {iy_a, fast}, each as (group g, group g + 4)
+  __shared__ float4 anc[8][16][4];
   const int n = blockIdx.z;
   const int lane = threadIdx.x;
   const int xw = blockIdx.x * (32 * PF_PX);
@@ -879,7 +883,7 @@ __global__ void __launch_bounds__(256, PF_MINB) warp_persp_fast_kernel(const __g
   const uint32_t rp32 = (uint32_t)a.s_rp;
   const unsigned xlim = (unsigned)(a.sw - pf_safe<C>()), ylim = (unsigned)(a.sh - 1);
   const f2_t HALF = f2(0.5f, 0.5f), MAG = f2(8388608.0f, 8388608.0f), NMAG = f2(-8388608.0f, -8388608.0f);
-  float4(&A)[32][2] = anc[threadIdx.y];
+  float4(&A)[16][4] = anc[threadIdx.y];
 #pragma unroll 1
   for (int y = y_first; y < y_end; y += 8) {
     const double yd = (double)y;
@@ -904,9 +908,15 @@ __global__ void __launch_bounds__(256, PF_MINB) warp_persp_fast_kernel(const __g
         fast = ex <= PF_MAX_ERR && ey <= PF_MAX_ERR;  // false for inf / NaN
       }
       const double fxa = floor(sa_x), fya = floor(sa_y);
-      A[lane][0] = make_float4((float)(sa_x - fxa), (float)(sa_y - fya), kx, ky);
-      A[lane][1] = make_float4(waf, __int_as_float(fast ? (int)fxa : 0), __int_as_float(fast ? (int)fya : 0),
-                               __int_as_float(fast ? 1 : 0));
+      float* q = reinterpret_cast<float*>(&A[(lane >> 3) * 4 + (lane & 3)][0]) + ((lane >> 2) & 1);
+      q[0] = (float)(sa_x - fxa);
+      q[2] = (float)(sa_y - fya);
+      q[4] = kx;
+      q[6] = ky;
+      q[8] = waf;
+      q[10] = __int_as_float(fast ? (int)fxa : 0);
+      q[12] = __int_as_float(fast ? (int)fya : 0);
+      q[14] = __int_as_float(fast ? 1 : 0);
     }
     __syncwarp();
     uint8_t* drow = row_ptr_mut<uint8_t>(a.dst, a.d_is, a.d_rp, n, y);
@@ -916,27 +926,53 @@ __global__ void __launch_bounds__(256, PF_MINB) warp_persp_fast_kernel(const __g
       // gathers; group (x_k - xw) / PF_PX holds the anchor, offset lane % 8
       int tx0[2], ty0[2];
       float tfx[2], tfy[2];
+      const int pp = (j >> 1) * 4 + (lane >> 3);  // groups 4j + lane/8 and 4j + 4 + lane/8
+      const float4 F0 = A[pp][0], F1 = A[pp][1], F2 = A[pp][2], F3 = A[pp][3];
+      if (__float_as_int(F3.z) & __float_as_int(F3.w)) {
+        // both pixels on the f32 correction: the two maps as f32x2 pairs
+        const f2_t D = f2(dlt, dlt);
+        const f2_t W = ffma2(f2(m6f, m6f), D, f2(F2.x, F2.y));
+        uint32_t wl, wh;
+        f2split(W, wl, wh);
+        const f2_t R = f2(rcp_approx(__uint_as_float(wl)), rcp_approx(__uint_as_float(wh)));
+        const f2_t TX = fadd2(f2(F0.x, F0.y), fmul2(fmul2(f2(F1.x, F1.y), D), R));
+        const f2_t TY = fadd2(f2(F0.z, F0.w), fmul2(fmul2(f2(F1.z, F1.w), D), R));
+        // floor: RD(t + 1.5 * 2^23) holds floor(t) in its low bits for |t| < 2^22
+        const f2_t MG = f2(12582912.0f, 12582912.0f), NMG = f2(-12582912.0f, -12582912.0f);
+        const f2_t FX = fadd2_rd(TX, MG), FY = fadd2_rd(TY, MG);
+        uint32_t fxl, fxh, fyl, fyh, rxl, rxh, ryl, ryh;
+        f2split(FX, fxl, fxh);
+        f2split(FY, fyl, fyh);
+        f2split(fadd2(TX, fadd2(NMG, FX) ^ 0x8000000080000000ull), rxl, rxh);  // t - floor(t)
+        f2split(fadd2(TY, fadd2(NMG, FY) ^ 0x8000000080000000ull), ryl, ryh);
+        tfx[0] = __uint_as_float(rxl);
+        tfx[1] = __uint_as_float(rxh);
+        tfy[0] = __uint_as_float(ryl);
+        tfy[1] = __uint_as_float(ryh);
+        tx0[0] = (int)(fxl - 0x4B400000u) + __float_as_int(F2.z);
+        tx0[1] = (int)(fxh - 0x4B400000u) + __float_as_int(F2.w);
+        ty0[0] = (int)(fyl - 0x4B400000u) + __float_as_int(F3.x);
+        ty0[1] = (int)(fyh - 0x4B400000u) + __float_as_int(F3.y);
+      } else {
 #pragma unroll
-      for (int k = 0; k < 2; ++k) {
-        const int g = 4 * (j + k) + (lane >> 3);
-        const float4 q1 = A[g][1];
-        if (__float_as_int(q1.w)) {
-          const float4 q0 = A[g][0];
-          const float r = rcp_approx(__fmaf_rn(m6f, dlt, q1.x));  // <= 1 ulp (bound term 2^-23)
-          const float tx = __fadd_rn(q0.x, __fmul_rn(__fmul_rn(q0.z, dlt), r));
-          const float ty = __fadd_rn(q0.y, __fmul_rn(__fmul_rn(q0.w, dlt), r));
-          const float flx = floorf(tx), fly = floorf(ty);
-          tfx[k] = __fsub_rn(tx, flx);
-          tfy[k] = __fsub_rn(ty, fly);
-          tx0[k] = __float_as_int(q1.y) + (int)flx;  // |.| < 2^23: no clamp needed
-          ty0[k] = __float_as_int(q1.z) + (int)fly;
-        } else {
-          // the f64 per-pixel map (warp_tap); non-finite -> every tap outside
-          const WarpTap w = warp_tap<true>(m, rx, ry, rw, min(xw + lane + 32 * (j + k), a.dw - 1), a.sw, a.sh);
-          tfx[k] = w.wx1;
-          tfy[k] = w.wy1;
-          tx0[k] = w.finite ? w.x0 : -2;
-          ty0[k] = w.finite ? w.y0 : -2;
+        for (int k = 0; k < 2; ++k) {
+          if (__float_as_int(k ? F3.w : F3.z)) {
+            const float r = rcp_approx(__fmaf_rn(m6f, dlt, k ? F2.y : F2.x));  // <= 1 ulp (bound term 2^-23)
+            const float tx = __fadd_rn(k ? F0.y : F0.x, __fmul_rn(__fmul_rn(k ? F1.y : F1.x, dlt), r));
+            const float ty = __fadd_rn(k ? F0.w : F0.z, __fmul_rn(__fmul_rn(k ? F1.w : F1.z, dlt), r));
+            const float flx = floorf(tx), fly = floorf(ty);
+            tfx[k] = __fsub_rn(tx, flx);
+            tfy[k] = __fsub_rn(ty, fly);
+            tx0[k] = __float_as_int(k ? F2.w : F2.z) + (int)flx;  // |.| < 2^23: no clamp needed
+            ty0[k] = __float_as_int(k ? F3.y : F3.x) + (int)fly;
+          } else {
+            // the f64 per-pixel map (warp_tap); non-finite -> every tap outside
+            const WarpTap w = warp_tap<true>(m, rx, ry, rw, min(xw + lane + 32 * (j + k), a.dw - 1), a.sw, a.sh);
+            tfx[k] = w.wx1;
+            tfy[k] = w.wy1;
+            tx0[k] = w.finite ? w.x0 : -2;
+            ty0[k] = w.finite ? w.y0 : -2;
+          }
         }
       }
       const int xa = xw + lane + 32 * j, xb = xa + 32;
