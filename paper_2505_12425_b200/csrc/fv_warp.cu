@@ -771,13 +771,13 @@ constexpr int pf_nwin() { return (2 * C + 3 + 3) / 4; }
 template <int C>
 constexpr int pf_safe() { return (4 * pf_nwin<C>() + C - 1) / C; }
 template <int C>
-__device__ __forceinline__ void pf_row_taps(const uint8_t* img, uint32_t off, uint32_t (&t0)[C], uint32_t (&t1)[C]) {
+__device__ __forceinline__ void pf_row_taps(const uint8_t* img, uint32_t al, int sh, uint32_t (&t0)[C],
+                                            uint32_t (&t1)[C]) {
   constexpr int NW = pf_nwin<C>(), NV = (2 * C + 3) / 4;
-  const uint32_t* w = reinterpret_cast<const uint32_t*>(img + (off & ~3u));
+  const uint32_t* w = reinterpret_cast<const uint32_t*>(img + al);
   uint32_t win[NW];
 #pragma unroll
   for (int i = 0; i < NW; ++i) win[i] = __ldg(w + i);
-  const int sh = (int)(off & 3u) * 8;
   uint32_t v[NV];
 #pragma unroll
   for (int i = 0; i < NV; ++i) v[i] = __funnelshift_r(win[i], win[i + 1], sh);
@@ -1001,22 +1001,29 @@ __global__ void __launch_bounds__(256, PF_MINB) warp_persp_fast_kernel(const __g
         // aligned rows (host-checked): lanes past the edge load row 0
         const uint32_t oa = va ? (uint32_t)ty0[0] * rp32 + (uint32_t)(tx0[0] * C) : 0u;
         const uint32_t ob = vb ? (uint32_t)ty0[1] * rp32 + (uint32_t)(tx0[1] * C) : 0u;
-        pf_row_taps<C>(simg, oa, v00[0], v01[0]);
-        pf_row_taps<C>(simg, oa + rp32, v10[0], v11[0]);
-        pf_row_taps<C>(simg, ob, v00[1], v01[1]);
-        pf_row_taps<C>(simg, ob + rp32, v10[1], v11[1]);
+        // rows are 4-byte aligned: both tap rows share the byte shift
+        const int sha = (int)(oa & 3u) * 8, shb = (int)(ob & 3u) * 8;
+        pf_row_taps<C>(simg, oa & ~3u, sha, v00[0], v01[0]);
+        pf_row_taps<C>(simg, (oa & ~3u) + rp32, sha, v10[0], v11[0]);
+        pf_row_taps<C>(simg, ob & ~3u, shb, v00[1], v01[1]);
+        pf_row_taps<C>(simg, (ob & ~3u) + rp32, shb, v10[1], v11[1]);
       }
       const f2_t WX1 = f2(tfx[0], tfx[1]), WY1 = f2(tfy[0], tfy[1]);
       const f2_t WX0 = fadd2(f2(1.0f, 1.0f), fmul2(WX1, f2(-1.0f, -1.0f)));
       const f2_t WY0 = fadd2(f2(1.0f, 1.0f), fmul2(WY1, f2(-1.0f, -1.0f)));
       const f2_t W00 = fmul2(WX0, WY0), W01 = fmul2(WX1, WY0), W10 = fmul2(WX0, WY1), W11 = fmul2(WX1, WY1);
+      // first tap straight from its magic word M = 2^23 + u: C00 = 0.5 -
+      // 2^23 * W00 is exact for W00 >= 2^-24 (at most 24 significant bits
+      // from 2^-1 down to W00's last bit times 2^23; below, off by <= 2^-25),
+      // so fma(M, W00, C00) = RN(u * W00 + 0.5)
+      const f2_t C00 = ffma2(W00, NMAG, HALF);
       uint8_t* pa = drow + xa * C;
       uint8_t* pb = drow + xb * C;
 #pragma unroll
       for (int c = 0; c < C; ++c) {
-        const f2_t A00 = fadd2(f2u(v00[0][c], v00[1][c]), NMAG), A01 = fadd2(f2u(v01[0][c], v01[1][c]), NMAG);
+        const f2_t A01 = fadd2(f2u(v01[0][c], v01[1][c]), NMAG);
         const f2_t A10 = fadd2(f2u(v10[0][c], v10[1][c]), NMAG), A11 = fadd2(f2u(v11[0][c], v11[1][c]), NMAG);
-        const f2_t v = ffma2(A11, W11, ffma2(A10, W10, ffma2(A01, W01, ffma2(A00, W00, HALF))));
+        const f2_t v = ffma2(A11, W11, ffma2(A10, W10, ffma2(A01, W01, ffma2(f2u(v00[0][c], v00[1][c]), W00, C00))));
         uint32_t lo, hi;
         f2split(fadd2_rd(v, MAG), lo, hi);  // floor(v) in the low byte (0 <= v < 256)
         if (va) pa[c] = (uint8_t)(lo & 0xFF);
