@@ -22,6 +22,9 @@ namespace fv {
 
 constexpr int MAXW = 256;  // images per launch (matrices live in the param block)
 constexpr int WARP_ROWS = 4;  // rows per thread in warp_kernel
+#ifndef WK_MINB
+#define WK_MINB 4  // warp_kernel: resident CTAs per SM the register budget is sized for
+#endif
 
 struct WarpArgs {
   const void* src;
@@ -239,7 +242,7 @@ __device__ __forceinline__ void blend_store(const WarpArgs& a, const WarpTap (&t
 // f32x2 pairs. Interior pixels take unguarded loads, pixels whose four taps
 // are all outside skip the loads.
 template <typename InT, bool PERSP, int C>
-__global__ void __launch_bounds__(256, 4) warp_kernel(const __grid_constant__ WarpArgs a,
+__global__ void __launch_bounds__(256, WK_MINB) warp_kernel(const __grid_constant__ WarpArgs a,
                                                    const __grid_constant__ WarpMats mats) {
   const int n = blockIdx.z;
   const int x = blockIdx.x * 64 + threadIdx.x;
