@@ -16,33 +16,14 @@
 #include <cudaTypedefs.h>
 #include <mutex>
 
-#include "fv_common.cuh"
+#include "fv_warp.cuh"
 
 namespace fv {
 
-constexpr int MAXW = 256;  // images per launch (matrices live in the param block)
 constexpr int WARP_ROWS = 4;  // rows per thread in warp_kernel
 #ifndef WK_MINB
 #define WK_MINB 4  // warp_kernel: resident CTAs per SM the register budget is sized for
 #endif
-
-struct WarpArgs {
-  const void* src;
-  int64_t s_is, s_rp;
-  int sh, sw;
-  void* dst;
-  int64_t d_is, d_rp;
-  int dh, dw;
-  int c;
-  float border_f;     // border as a blend operand (u8: RN(b/255))
-  float border_raw;   // border as stored for non-finite coordinates
-  f2_t one2;          // runtime {1.0f, 1.0f} (f32x2 contraction guard)
-  int zero_border;    // border is +0: fully-outside pixels are exactly 0
-};
-
-struct WarpMats {
-  double m[MAXW][9];
-};
 
 template <typename T>
 __device__ __forceinline__ T to_out(float v);
@@ -53,48 +34,6 @@ __device__ __forceinline__ float to_out<float>(float v) {
 template <>
 __device__ __forceinline__ uint8_t to_out<uint8_t>(float v) {
   return (uint8_t)unit_to_u8(v);
-}
-
-// Inverse map of destination pixel (x, y) and its bilinear taps.
-struct WarpTap {
-  int x0, y0;
-  float wx0, wx1, wy0, wy1;
-  bool finite;
-};
-
-template <bool PERSP>
-__device__ __forceinline__ WarpTap warp_tap(const double (&m)[9], double rx, double ry, double rw, int x, int sw,
-                                            int sh) {
-  WarpTap t;
-  const double xd = (double)x;
-  double sx = __dadd_rn(__dmul_rn(m[0], xd), rx);
-  double sy = __dadd_rn(__dmul_rn(m[3], xd), ry);
-  t.finite = true;
-  if (PERSP) {
-    const double w = __dadd_rn(__dmul_rn(m[6], xd), rw);
-    if (w == 0.0) {
-      t.finite = false;
-    } else {
-      const double r = __drcp_rn(w);
-      sx = __dmul_rn(sx, r);
-      sy = __dmul_rn(sy, r);
-    }
-  }
-  t.finite = t.finite && isfinite(sx) && isfinite(sy);
-  if (!t.finite) {
-    sx = 0.0;
-    sy = 0.0;
-  }
-  const double fx = floor(sx), fy = floor(sy);
-  t.wx1 = __double2float_rn(__dadd_rn(sx, -fx));
-  t.wy1 = __double2float_rn(__dadd_rn(sy, -fy));
-  t.wx0 = __fsub_rn(1.0f, t.wx1);
-  t.wy0 = __fsub_rn(1.0f, t.wy1);
-  // cvt.rmi saturates out-of-range values; clamping keeps every out-of-range
-  // tap out of range (the oracle clips the float the same way)
-  t.x0 = min(max(__double2int_rd(sx), -2), sw + 1);
-  t.y0 = min(max(__double2int_rd(sy), -2), sh + 1);
-  return t;
 }
 
 // every tap of the pixel outside the source, or a non-finite map: the
@@ -759,11 +698,6 @@ constexpr int kPfJUnroll = PF_JUNROLL;  // pixel pairs per sampling-loop iterati
 #define PF_MINB 4  // resident CTAs per SM the register budget is sized for
 #endif
 
-__device__ __forceinline__ float rcp_approx(float x) {
-  float r;
-  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
-  return r;
-}
 
 // Window of the two taps (x0, x0 + 1) of one source row, C bytes each, from
 // NWIN aligned 32-bit loads at byte offset `off` of a 4-byte aligned image;
@@ -1107,7 +1041,7 @@ static int launch_persp_fast(const uint8_t* src, int64_t s_is, int64_t s_rp, int
   // inside an image below 2^31 and rows at least one load window wide
   const bool fits = (c == 1 || c == 3 || c == 4) && ((reinterpret_cast<uintptr_t>(src) | (uintptr_t)s_rp) & 3) == 0 &&
                     (n <= 1 || (s_is & 3) == 0) && s_rp > 0 && (int64_t)sh * s_rp < ((int64_t)1 << 31) &&
-                    sw > 4 * 3 + 1;
+                    sw > 4 * 3 + 1 && sh >= 2;
   if (!fits)
     return launch_warp<uint8_t, true>(src, s_is, s_rp, sh, sw, dst, d_is, d_rp, dh, dw, c, n, mats_host, 9, bf,
                                       (float)border, st, fn);
@@ -1139,12 +1073,16 @@ static int launch_persp_fast(const uint8_t* src, int64_t s_is, int64_t s_rp, int
     a.src = reinterpret_cast<const char*>(src) + (int64_t)b * s_is;
     a.dst = reinterpret_cast<char*>(dst) + (int64_t)b * d_is;
     dim3 grid((dw + 32 * PF_PX - 1) / (32 * PF_PX), (dh + 8 * PF_ROWS - 1) / (8 * PF_ROWS), nb);
-    switch (c) {
-      case 1: warp_persp_fast_kernel<1><<<grid, dim3(32, 8), 0, st>>>(a, mats); break;
-      case 3: warp_persp_fast_kernel<3><<<grid, dim3(32, 8), 0, st>>>(a, mats); break;
-      default: warp_persp_fast_kernel<4><<<grid, dim3(32, 8), 0, st>>>(a, mats); break;
+    int rc = g_warp_path == 3 ? 1 : launch_persp_tile(a, mats, nb, st);
+    if (rc > 1 || rc < 0) return rc;
+    if (rc == 1) {
+      switch (c) {
+        case 1: warp_persp_fast_kernel<1><<<grid, dim3(32, 8), 0, st>>>(a, mats); break;
+        case 3: warp_persp_fast_kernel<3><<<grid, dim3(32, 8), 0, st>>>(a, mats); break;
+        default: warp_persp_fast_kernel<4><<<grid, dim3(32, 8), 0, st>>>(a, mats); break;
+      }
     }
-    const int rc = check_launch(fn);
+    rc = check_launch(fn);
     if (rc) return rc;
   }
   return FV_OK;
@@ -1229,7 +1167,7 @@ using namespace fv;
 extern "C" {
 
 void fv_set_warp_path(int32_t mode) {
-  g_warp_path = mode == 2 ? 0 : mode;
+  g_warp_path = mode == 2 ? 0 : mode;  // 3: the round-1 perspective kernel (A/B)
   g_warp_tma = mode == 2 ? 0 : 1;
 }
 

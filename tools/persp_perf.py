@@ -24,9 +24,16 @@ def main():
     n = 16
     src = synth.device_u8_batch(n, 2160, 3840, 3, synth.SEED_PERSP, dev)
     hs = np.stack([synth.perspective_forward(synth.SEED_PERSP_PARAMS + i) for i in range(n)])
-    d_ex, d_fa = torch.zeros_like(src), torch.zeros_like(src)
+    d_ex, d_fa, d_old = torch.zeros_like(src), torch.zeros_like(src), torch.zeros_like(src)
+    from paper_2505_12425_b200 import _native
+
+    def old():
+        _native.lib().fv_set_warp_path(3)
+        fv.warp_perspective(src, d_old, hs)
+        _native.lib().fv_set_warp_path(0)
+
     runs = {"exact": lambda: fv.warp_perspective(src, d_ex, hs, exact=True),
-            "fast": lambda: fv.warp_perspective(src, d_fa, hs)}
+            "fast": lambda: fv.warp_perspective(src, d_fa, hs), "fast_r01": old}
     for f in runs.values():
         for _ in range(3):
             f()
@@ -40,8 +47,9 @@ def main():
         torch.cuda.synchronize()
         ms = e0.elapsed_time(e1) / a.reps
         print(f"{name}: {ms:.4f} ms / 16 images, {n * 3840 * 2160 / ms / 1e3:.0f} dst MP/s")
-    diff = (d_ex.to(torch.int16) - d_fa.to(torch.int16)).abs()
-    print(f"fast vs exact: max |diff| {int(diff.max())}, {int((diff > 0).sum())} of {diff.numel()} values differ")
+    for name, d in (("fast", d_fa), ("fast_r01", d_old)):
+        diff = (d_ex.to(torch.int16) - d.to(torch.int16)).abs()
+        print(f"{name} vs exact: max |diff| {int(diff.max())}, {int((diff > 0).sum())} of {diff.numel()} values differ")
 
 
 if __name__ == "__main__":
