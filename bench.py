@@ -2,27 +2,46 @@
 """Benchmark of the B200 image-transformation path (BASELINE.json contract).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl fovea|reference]
+                    [--ops gray,resize,affine,persp,fused,jpeg] [--no-cpu] [--no-e2e]
+                    [--no-verify] [--dry-run]
 
 Headline workload (BASELINE.json configs[1]): one step = bilinear u8 resize of
 a batch of 64 3840x2160x3 images down to 1920x1080x3 AND up to 7680x4320x3
 (`_resize_u8` semantics, app.py:64-78). `value` = destination megapixels per
 second over the whole job, inputs resident in HBM (1.59 GB of source >> the
-126 MB L2, so no flush is needed between steps). The other four configs are
+126 MB L2, so no flush is needed between steps). The other configs are
 measured the same way and reported under "ops" (cfg0 rotates over 32 distinct
-images, 265 MB, so every step reads from HBM, not L2), plus the decode ->
-preprocess row (64 host-resident 1080p JPEGs decoded and
-resized/normalised to 3x640x640 per step, host entropy decoding included).
+images, 265 MB, so every step reads from HBM), plus the decode -> preprocess
+row.
 
-Multi-GPU: one process per GPU (torchrun), each rank takes a contiguous shard
-of the images, no collective on the data path; a host barrier plus
-torch.cuda.synchronize() bracket the timed region and the elapsed time is the
-MAX over ranks (all_reduce MAX of a scalar, harness only). `value` = all
-images' destination pixels / that time ("scaling": "weak" per image shard is
-fixed by the batch split: total work fixed = "strong"; see below).
+Every op carries, besides its kernels' CUDA-event times and roofline
+fractions:
+  * "cpu_baseline": the CPU path on the box's own host cores, 1 core and all
+    cores (one process per core, started together behind a barrier), on a
+    bounded seeded sample of the same workload (`sample` says which): the
+    oracle/ NumPy port of the reference for gray and the u8 resize
+    (imgproc.py:43-64, app.py:64-78; pinned to reference-generated goldens),
+    the oracle CPU path for the warps and the fused chain (no reference
+    implementation exists), the pure-Python port of the reference decoder
+    for the JPEG row;
+  * "e2e": the same op through the public API from pinned HOST buffers, the
+    H2D copy of the inputs and the D2H copy of the outputs inside the timed
+    region (chunked over copy-in / compute / copy-out streams);
+  * "verified": the timed run's outputs compared, after timing, with the
+    oracle on sampled rows of the first and last image of the shard.
 
---impl reference runs the reference's CPU algorithm for the same workload (the
-NumPy restatement in oracle/, since the reference is pure Python and does not
-exist on the GPU box), on all host cores, rank 0 only.
+Multi-GPU: one process per GPU, each rank takes a contiguous shard of the
+images, no collective on the data path; a barrier plus synchronize bracket
+the timed region and the elapsed time is the MAX over ranks (all_reduce MAX of
+a scalar, harness only). `--gpus N` without torchrun re-launches itself under
+`torch.distributed.run` with N processes; a WORLD_SIZE that disagrees with
+--gpus is an error. `--dry-run` runs the same rank plumbing on CPU over gloo
+with stand-in ops (tests/test_bench_ranks.py).
+
+--impl reference times the reference's CPU algorithm for the same workload
+(the oracle/ NumPy restatement; the reference is pure Python and does not
+exist on the GPU box) on all host cores, rank 0 only, with the same samples
+as the fovea arm's cpu_baseline.
 """
 from __future__ import annotations
 
@@ -31,6 +50,7 @@ import json
 import math
 import multiprocessing as mp
 import os
+import socket
 import statistics
 import subprocess
 import sys
@@ -42,6 +62,7 @@ sys.path.insert(0, ROOT)
 
 METRIC = "megapixels/sec per op at 1/2/4/8 B200; achieved HBM GB/s vs peak"
 UNIT = "MP/s"
+HEAD = "cfg1_resize_u8_64x4k"
 
 
 def load_traffic():
@@ -79,6 +100,100 @@ def shard(n_total, world, rank):
     lo = rank * n_total // world
     hi = (rank + 1) * n_total // world
     return lo, hi
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def relaunch(gpus, argv):
+    """`--gpus N` outside torchrun: run this script under torch.distributed.run
+    with N processes (one per GPU) and return its exit code."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={gpus}",
+           "--master-addr", "127.0.0.1", f"--master-port={_free_port()}", os.path.abspath(__file__), *argv]
+    return subprocess.call(cmd)
+
+
+class Backend:
+    """Device-side plumbing of one rank: CUDA (the product) or the dry-run CPU
+    stand-in that exercises the same sharding / timing / reduction code."""
+
+    def __init__(self, dry, world, rank, local):
+        import torch
+        import torch.distributed as dist
+
+        self.torch, self.dist, self.dry, self.world, self.rank = torch, dist, dry, world, rank
+        if dry:
+            self.dev = torch.device("cpu")
+            if world > 1:
+                dist.init_process_group("gloo")
+        else:
+            if world > 1:
+                torch.cuda.set_device(local)
+                dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+            self.dev = torch.device("cuda", local if world > 1 else 0)
+            torch.cuda.set_device(self.dev)
+
+    def sync(self):
+        if not self.dry:
+            self.torch.cuda.synchronize()
+
+    def barrier(self):
+        if self.world > 1:
+            self.dist.barrier()
+
+    def reduce(self, vals, op="max"):
+        """MAX (or SUM) over ranks of a list of floats."""
+        if self.world == 1:
+            return list(vals)
+        t = self.torch.tensor(list(vals), dtype=self.torch.float64,
+                              device="cpu" if self.dry else self.dev)
+        self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX if op == "max" else self.dist.ReduceOp.SUM)
+        return [float(v) for v in t]
+
+    def gather(self, obj):
+        if self.world == 1:
+            return [obj]
+        out = [None] * self.world
+        self.dist.all_gather_object(out, obj)
+        return out
+
+    def device_id(self):
+        if self.dry:
+            return {"rank": self.rank, "device": f"cpu:{self.rank}", "bus_id": f"dry-{self.rank}"}
+        p = self.torch.cuda.get_device_properties(self.dev)
+        bus = f"{getattr(p, 'pci_domain_id', 0):04x}:{getattr(p, 'pci_bus_id', 0):02x}:{getattr(p, 'pci_device_id', 0):02x}"
+        return {"rank": self.rank, "device": str(self.dev), "name": p.name, "bus_id": str(bus),
+                "uuid": str(getattr(p, "uuid", ""))}
+
+    def timer(self, stream=None):
+        return Timer(self, stream)
+
+    def close(self):
+        if self.world > 1:
+            self.dist.barrier()
+            self.dist.destroy_process_group()
+
+
+class Timer:
+    """CUDA events on the launching stream (real) or perf_counter (dry)."""
+
+    def __init__(self, be, stream):
+        self.be, self.stream = be, stream
+
+    def mark(self):
+        if self.be.dry:
+            return time.perf_counter()
+        e = self.be.torch.cuda.Event(enable_timing=True)
+        e.record(self.stream)
+        return e
+
+    def ms(self, a, b):
+        if self.be.dry:
+            return (b - a) * 1e3
+        return a.elapsed_time(b)
 
 
 # ---------------------------------------------------------------------------
@@ -137,126 +252,418 @@ class ClockSampler:
 
 
 # ---------------------------------------------------------------------------
+# CPU baseline: the oracle port of the reference algorithm on host cores
+# ---------------------------------------------------------------------------
+# Task sizes are the bounded samples (about 0.2-0.6 s of one core each); both
+# arms (cpu_baseline of the fovea arm, --impl reference) use these same sizes.
+CPU_UP_ROWS = 240       # of 4320 destination rows, 3840x2160 -> 7680x4320
+CPU_AFFINE_ROWS = 270   # of 1080, 1920x1080 f32 affine
+CPU_PERSP_ROWS = 135    # of 2160, 3840x2160 u8 perspective
+CPU_GRAY_REPS = 8       # 1080p frames per gray task
+CPU_FUSED_REPS = 3      # 1080p -> 3x640x640 images per fused task
+
+
+def _cpu_prepare(task):
+    """Inputs of one CPU task (outside the timed part): regenerated from the
+    per-image seeds, like each GPU rank."""
+    import oracle as O
+    from paper_2505_12425_b200 import synth
+
+    kind, i = task[0], task[1]
+    if kind == "gray":
+        return task, O.seeded_u8_image(1920, 1080, 3, seed=synth.SEED_GRAY + i)
+    if kind in ("down", "up"):
+        return task, O.seeded_u8_image(3840, 2160, 3, seed=synth.SEED_RESIZE + i)
+    if kind == "affine":
+        return task, (O.seeded_f32_image(1920, 1080, 3, seed=synth.SEED_AFFINE + i),
+                      O.invert_affine(O.affine_forward(synth.SEED_AFFINE_PARAMS + i, 1920, 1080)))
+    if kind == "persp":
+        return task, (O.seeded_u8_image(3840, 2160, 3, seed=synth.SEED_PERSP + i),
+                      O.invert_homography(O.perspective_forward(synth.SEED_PERSP_PARAMS + i)))
+    if kind == "fused":
+        return task, O.seeded_u8_image(1920, 1080, 3, seed=synth.SEED_FUSED + i)
+    if kind == "jpeg":
+        return task, jpeg_streams(i, i + 1)[0]
+    if kind == "dry":
+        return task, None
+    raise ValueError(kind)
+
+
+def _cpu_run(task, data):
+    """Run one prepared task; returns destination pixels produced."""
+    import oracle as O
+    from paper_2505_12425_b200 import synth
+
+    kind = task[0]
+    if kind == "gray":
+        for _ in range(CPU_GRAY_REPS):
+            O.gray_from_rgb(data)
+        return CPU_GRAY_REPS * 1920 * 1080
+    if kind == "down":
+        O.resize_u8(data, 1920, 1080)
+        return 1920 * 1080
+    if kind == "up":
+        lo = task[2]
+        O.resize_u8(data, 7680, 4320, rows=(lo, lo + CPU_UP_ROWS))
+        return 7680 * CPU_UP_ROWS
+    if kind == "affine":
+        lo = task[2]
+        O.warp_affine(data[0], data[1], 1080, 1920, border=0.0, rows=(lo, lo + CPU_AFFINE_ROWS))
+        return 1920 * CPU_AFFINE_ROWS
+    if kind == "persp":
+        lo = task[2]
+        O.warp_perspective(data[0], data[1], 2160, 3840, border=0, rows=(lo, lo + CPU_PERSP_ROWS))
+        return 3840 * CPU_PERSP_ROWS
+    if kind == "fused":
+        for _ in range(CPU_FUSED_REPS):
+            O.resize_normalize_chw(data, 640, 640, synth.MEAN, synth.STD)
+        return CPU_FUSED_REPS * 640 * 640
+    if kind == "jpeg":
+        sys.path.insert(0, os.path.join(ROOT, "oracle"))
+        import jpeg_oracle
+
+        frame = jpeg_oracle.decode_jpeg(data)
+        O.resize_normalize_chw(frame, 640, 640, synth.MEAN, synth.STD)
+        return 1920 * 1080
+    if kind == "dry":
+        t_end = time.perf_counter() + 0.01
+        while time.perf_counter() < t_end:
+            pass
+        return 1000
+    raise ValueError(kind)
+
+
+def _cpu_proc(tasks, barrier, q):
+    os.environ["OMP_NUM_THREADS"] = "1"
+    try:
+        prepared = [_cpu_prepare(t) for t in tasks]
+        barrier.wait(timeout=600)
+        t0 = time.perf_counter()
+        px = sum(_cpu_run(t, d) for t, d in prepared)
+        q.put((px, time.perf_counter() - t0))
+    except Exception as e:  # reported, not hidden
+        q.put(("error", repr(e)))
+
+
+def cpu_measure(tasks_per_proc):
+    """One process per entry of `tasks_per_proc` (a list of task lists), all
+    released together by a barrier once their inputs exist; returns
+    (destination px, seconds = the slowest process's time)."""
+    ctx = mp.get_context("fork")
+    barrier = ctx.Barrier(len(tasks_per_proc))
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_cpu_proc, args=(tl, barrier, q)) for tl in tasks_per_proc]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=900) for _ in procs]
+    for p in procs:
+        p.join(timeout=60)
+    errs = [r[1] for r in res if r[0] == "error"]
+    if errs:
+        raise RuntimeError(f"CPU baseline task failed: {errs[0]}")
+    return sum(r[0] for r in res), max(r[1] for r in res)
+
+
+def cpu_tasks(op, k):
+    """Task k (per process) of an op's bounded sample."""
+    if op == "gray":
+        return [("gray", k % 32)]
+    if op == "resize":
+        return [("down", k % 64), ("up", k % 64, (k * 977) % (4320 - CPU_UP_ROWS))]
+    if op == "affine":
+        return [("affine", k % 32, (k * 211) % (1080 - CPU_AFFINE_ROWS))]
+    if op == "persp":
+        return [("persp", k % 16, (k * 353) % (2160 - CPU_PERSP_ROWS))]
+    if op == "fused":
+        return [("fused", k % 512)]
+    if op == "jpeg":
+        return [("jpeg", k % 64)]
+    if op == "dry":
+        return [("dry", k)]
+    raise ValueError(op)
+
+
+CPU_SAMPLE = {
+    "gray": f"{CPU_GRAY_REPS} seeded 1920x1080 frames per process (oracle port of imgproc.py:43-64, "
+            "pinned to reference goldens)",
+    "resize": f"per process one full 3840x2160->1920x1080 + {CPU_UP_ROWS} of 4320 destination rows of "
+              "3840x2160->7680x4320 (oracle port of app.py:64-78, pinned to reference goldens); "
+              "the step time = 64 x (down + up image times)",
+    "affine": f"per process {CPU_AFFINE_ROWS} of 1080 rows of one seeded 1920x1080 f32 image "
+              "(oracle CPU path: no reference implementation)",
+    "persp": f"per process {CPU_PERSP_ROWS} of 2160 rows of one seeded 3840x2160 u8 image "
+             "(oracle CPU path: no reference implementation)",
+    "fused": f"per process {CPU_FUSED_REPS} seeded 1920x1080 images -> 3x640x640 f32 "
+             "(oracle CPU path: _resize_u8 composition + normalise + CHW)",
+    "jpeg": "per process one q90 4:2:0 1920x1080 JPEG decoded by the pure-Python port of "
+            "io/jpeg.py:605-806 + the fused preprocessing (oracle CPU path)",
+    "dry": "dry-run stand-in",
+}
+
+
+def cpu_baseline(op, cores, one_core=True):
+    """1-core and all-core destination MP/s of an op's bounded sample."""
+    t0 = time.perf_counter()
+    if op == "resize":
+        # the two cfg1 outputs run at different per-pixel rates: measure each,
+        # then time the 64-image step as 64 x (down + up) per-image times
+        rates = {"1core": None}
+        for label, procs in ((("1core", 1),) if one_core else ()) + (("all", cores),):
+            per = {}
+            for kind in ("down", "up"):
+                tl = [[t for t in cpu_tasks("resize", k) if t[0] == kind] for k in range(procs)]
+                px, s = cpu_measure(tl)
+                per[kind] = (px / procs, s)  # per-process px and time (all concurrent)
+            img_down = 1920 * 1080 / (per["down"][0] / per["down"][1])
+            img_up = 7680 * 4320 / (per["up"][0] / per["up"][1])
+            step_s = 64 * (img_down + img_up) / procs
+            rates[label] = 64 * (1920 * 1080 + 7680 * 4320) / step_s / 1e6
+        v1, vall = rates["1core"], rates["all"]
+    else:
+        v1 = None
+        if one_core:
+            px1, s1 = cpu_measure([cpu_tasks(op, 0)])
+            v1 = px1 / s1 / 1e6
+        pxa, sa = cpu_measure([cpu_tasks(op, k) for k in range(cores)])
+        vall = pxa / sa / 1e6
+    return {"value": vall, "unit": UNIT, "cores": cores, "value_1core": v1,
+            "kind": "port", "sample": CPU_SAMPLE[op], "wall_s": round(time.perf_counter() - t0, 2)}
+
+
+def host_cores():
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:
+        return os.cpu_count() or 1
+
+
+# ---------------------------------------------------------------------------
 # workloads
 # ---------------------------------------------------------------------------
 
-def build_ops(n_scale, world, rank, dev, include):
-    """Per-config workloads for this rank. Each returns a dict with
-    launches: list of (name, fn, algorithmic_bytes), dst_px, src_px, units."""
+class Op:
+    """One config on one rank: launches [(kernel label, fn, algorithmic bytes)],
+    px counts, and hooks for verification and the end-to-end run."""
+
+    def __init__(self, name, key, launches, dst_px, src_px, job_dst_px, l2, **kw):
+        self.name, self.key, self.launches = name, key, launches
+        self.dst_px, self.src_px, self.job_dst_px, self.l2 = dst_px, src_px, job_dst_px, l2
+        self.replicas = kw.get("replicas", False)
+        self.launches_per_call = kw.get("launches_per_call")
+        self.extra = kw.get("extra", {})
+        self.nominal_bytes = kw.get("nominal_bytes")
+        self.verify = kw.get("verify")
+        self.e2e = kw.get("e2e")
+        self.keep = kw.get("keep")
+
+
+def build_ops(be, include):
+    """Per-config workloads for this rank (device inputs resident). Each op is
+    built in its own function so its closures bind its own tensors."""
+    if be.dry:
+        return build_dry_ops(be, include)
+    builders = [("gray", op_gray), ("resize", op_resize), ("affine", op_affine), ("persp", op_persp),
+                ("fused", op_fused), ("jpeg", op_jpeg)]
+    return [b(be) for k, b in builders if k in include]
+
+
+def op_gray(be):
     import numpy as np
     import torch
 
     import paper_2505_12425_b200 as fv
     from paper_2505_12425_b200 import synth
 
-    ops = {}
+    world, rank, dev = be.world, be.rank, be.dev
+    # cfg0: one 1080p image per call. A frame is 8 MB (L2-resident, far
+    # below launch latency), so steps rotate over 32 distinct buffers
+    # (265 MB > 2x L2), replayed from a CUDA graph of 32 launches; the
+    # same kernel is also timed on the 32-frame batch in one launch.
+    pool = 32
+    srcs = synth.device_u8_batch(pool, 1080, 1920, 3, synth.SEED_GRAY + 1000 * rank, dev)
+    dsts = torch.zeros((pool, 1080, 1920, 1), dtype=torch.uint8, device=dev)
+    dstb = torch.zeros_like(dsts)
+    side = torch.cuda.Stream(dev)
+    side.wait_stream(torch.cuda.current_stream(dev))
+    with torch.cuda.stream(side):
+        for i in range(pool):  # warm (lazy module load) outside capture
+            fv.gray_from_rgb(srcs[i], dsts[i])
+    torch.cuda.current_stream(dev).wait_stream(side)
+    torch.cuda.synchronize(dev)
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(graph):
+        for i in range(pool):
+            fv.gray_from_rgb(srcs[i], dsts[i])
+    b = pool * 1920 * 1080 * 4
+    return Op(
+        "cfg0_gray_u8_1x1080p", "gray",
+        [("gray_u8 per frame (graph of 32 launches)", graph.replay, b),
+         ("gray_u8 32-frame batch (one launch)", lambda: fv.gray_from_rgb(srcs, dstb), b)],
+        dst_px=2 * pool * 1920 * 1080, src_px=2 * pool * 1920 * 1080, job_dst_px=None,
+        l2="32 rotating 1080p buffers (265 MB > 2x L2)", replicas=True, launches_per_call=pool + 1,
+        extra={"api_call_us": gray_api_latency(srcs, dsts)},
+        verify=lambda: verify_gray(srcs, dsts, dstb),
+        e2e=lambda steps: e2e_gray(be, srcs[0], steps), keep=(graph, srcs, dsts, dstb))
 
-    if "gray" in include:
-        # cfg0: one 1080p image per step. A single 1080p frame is 8 MB (L2-resident
-        # and far below launch latency), so steps rotate over 32 distinct buffers
-        # (265 MB > 2x L2) and are replayed from a CUDA graph of 32 launches, so
-        # the measured time is device time, not Python launch overhead.
-        pool = 32
-        srcs = synth.device_u8_batch(pool, 1080, 1920, 3, synth.SEED_GRAY + 1000 * rank, dev)
-        dsts = torch.zeros((pool, 1080, 1920, 1), dtype=torch.uint8, device=dev)
-        side = torch.cuda.Stream(dev)
-        side.wait_stream(torch.cuda.current_stream(dev))
-        with torch.cuda.stream(side):
-            for i in range(pool):  # warm (lazy module load) outside capture
-                fv.gray_from_rgb(srcs[i], dsts[i])
-        torch.cuda.current_stream(dev).wait_stream(side)
-        torch.cuda.synchronize(dev)
-        graph = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(graph):
-            for i in range(pool):
-                fv.gray_from_rgb(srcs[i], dsts[i])
 
-        ops["cfg0_gray_u8_1x1080p"] = dict(
-            launches=[("gray_u8 (graph of 32 launches)", graph.replay, pool * 1920 * 1080 * 4)],
-            dst_px=pool * 1920 * 1080, src_px=pool * 1920 * 1080, images=pool, replicas=True, per_step=pool,
-            launches_per_call=pool, graph=graph, l2="32 rotating 1080p buffers (265 MB > 2x L2), CUDA graph replay")
+def op_resize(be):
+    import numpy as np
+    import torch
 
-    if "resize" in include:
-        n_total = 64
-        lo, hi = shard(n_total, world, rank)
+    import paper_2505_12425_b200 as fv
+    from paper_2505_12425_b200 import synth
+
+    world, rank, dev = be.world, be.rank, be.dev
+    lo, hi = shard(64, world, rank)
+    n = hi - lo
+    src = synth.device_u8_batch(n, 2160, 3840, 3, synth.SEED_RESIZE + lo, dev)
+    down = torch.zeros((n, 1080, 1920, 3), dtype=torch.uint8, device=dev)
+    up = torch.zeros((n, 4320, 7680, 3), dtype=torch.uint8, device=dev)
+    sb = n * 2160 * 3840 * 3
+    return Op(
+        HEAD, "resize",
+        [("resize_down", lambda: fv.resize_bilinear_u8(src, down), sb + n * 1080 * 1920 * 3),
+         ("resize_up", lambda: fv.resize_bilinear_u8(src, up), sb + n * 4320 * 7680 * 3)],
+        dst_px=n * (1920 * 1080 + 7680 * 4320), src_px=2 * n * 3840 * 2160,
+        job_dst_px=64 * (1920 * 1080 + 7680 * 4320), l2="inputs 1.59 GB >> L2",
+        verify=lambda: verify_resize(src, down, up),
+        e2e=lambda steps: e2e_pipeline(be, src, [down, up],
+                                       lambda s, d: (fv.resize_bilinear_u8(s, d[0]), fv.resize_bilinear_u8(s, d[1])),
+                                       steps, 64 * (1920 * 1080 + 7680 * 4320), chunks=8))
+
+
+def op_affine(be):
+    import numpy as np
+    import torch
+
+    import paper_2505_12425_b200 as fv
+    from paper_2505_12425_b200 import synth
+
+    world, rank, dev = be.world, be.rank, be.dev
+    lo, hi = shard(32, world, rank)
+    n = hi - lo
+    src = synth.device_f32_batch(n, 1080, 1920, 3, synth.SEED_AFFINE + lo, dev)
+    dst = torch.zeros_like(src)
+    ms = np.stack([synth.affine_forward(synth.SEED_AFFINE_PARAMS + lo + i, 1920, 1080) for i in range(n)])
+    foot = footprint_bytes(ms, False, 1080, 1920, 12, dev) + n * 1920 * 1080 * 12
+    return Op(
+        "cfg2_warp_affine_f32_32x1080p", "affine",
+        [("warp_affine", lambda: fv.warp_affine(src, dst, ms, border=0.0), foot)],
+        dst_px=n * 1920 * 1080, src_px=n * 1920 * 1080, job_dst_px=32 * 1920 * 1080,
+        l2="inputs 796 MB >> L2", nominal_bytes=2 * n * 1920 * 1080 * 12,
+        verify=lambda: verify_warp(src, dst, ms, False, lo),
+        e2e=lambda steps: e2e_pipeline(be, src, [dst], None, steps, 32 * 1920 * 1080, chunks=4,
+                                       warp=(ms, False)))
+
+
+def op_persp(be):
+    import numpy as np
+    import torch
+
+    import paper_2505_12425_b200 as fv
+    from paper_2505_12425_b200 import synth
+
+    world, rank, dev = be.world, be.rank, be.dev
+    lo, hi = shard(16, world, rank)
+    n = hi - lo
+    src = synth.device_u8_batch(n, 2160, 3840, 3, synth.SEED_PERSP + lo, dev)
+    dst = torch.zeros_like(src)
+    hs = np.stack([synth.perspective_forward(synth.SEED_PERSP_PARAMS + lo + i) for i in range(n)])
+    foot = footprint_bytes(hs, True, 2160, 3840, 3, dev) + n * 3840 * 2160 * 3
+    return Op(
+        "cfg3_warp_perspective_u8_16x4k", "persp",
+        [("warp_perspective", lambda: fv.warp_perspective(src, dst, hs, border=0), foot)],
+        dst_px=n * 3840 * 2160, src_px=n * 3840 * 2160, job_dst_px=16 * 3840 * 2160,
+        l2="inputs 398 MB >> L2", nominal_bytes=2 * n * 3840 * 2160 * 3,
+        extra={"kernel_contract": "default u8 path: within 1 LSB of the oracle (north-star gate); "
+                                  "exact=True is the bit-exact kernel"},
+        verify=lambda: verify_warp(src, dst, hs, True, lo),
+        e2e=lambda steps: e2e_pipeline(be, src, [dst], None, steps, 16 * 3840 * 2160, chunks=4,
+                                       warp=(hs, True)))
+
+
+def op_fused(be):
+    import numpy as np
+    import torch
+
+    import paper_2505_12425_b200 as fv
+    from paper_2505_12425_b200 import synth
+
+    world, rank, dev = be.world, be.rank, be.dev
+    lo, hi = shard(512, world, rank)
+    n = hi - lo
+    src = synth.device_u8_batch(n, 1080, 1920, 3, synth.SEED_FUSED + lo, dev)
+    dst = torch.zeros((n, 3, 640, 640), dtype=torch.float32, device=dev)
+    return Op(
+        "cfg4_resize_normalize_chw_512x1080p", "fused",
+        [("resize_normalize_chw", lambda: fv.resize_normalize_chw(src, dst, synth.MEAN, synth.STD),
+          n * (1920 * 1080 * 3 + 3 * 640 * 640 * 4))],
+        dst_px=n * 640 * 640, src_px=n * 1920 * 1080, job_dst_px=512 * 640 * 640, l2="inputs 3.2 GB >> L2",
+        verify=lambda: verify_fused(src, dst),
+        e2e=lambda steps: e2e_pipeline(be, src, [dst],
+                                       lambda s, d: fv.resize_normalize_chw(s, d[0], synth.MEAN, synth.STD),
+                                       steps, 512 * 640 * 640, chunks=8))
+
+
+def op_jpeg(be):
+    import numpy as np
+    import torch
+
+    import paper_2505_12425_b200 as fv
+    from paper_2505_12425_b200 import synth
+
+    world, rank, dev = be.world, be.rank, be.dev
+    # SURVEY 8f rank 4, decode -> preprocess: host JPEG bytes -> decode
+    # (GPU entropy decoding + reconstruction) -> fused resize/normalise/CHW
+    lo, hi = shard(64, world, rank)
+    streams = jpeg_streams(lo, hi)
+    dst = torch.empty((hi - lo, 3, 640, 640), dtype=torch.float32, device=dev)
+    frames = torch.empty((hi - lo, 1080, 1920, 3), dtype=torch.uint8, device=dev)
+    from paper_2505_12425_b200 import io as fio
+
+    def step():
+        fio.decode_jpeg_batch(streams, dev, out=frames)  # the frames as one batch ...
+        fv.resize_normalize_chw(frames, dst, synth.MEAN, synth.STD)  # ... preprocessed in one launch
+
+    nbytes = sum(len(b) for b in streams) + dst.numel() * 4
+    gpu0 = fio.stats["gpu_entropy"]
+    step()
+    on_gpu = fio.stats["gpu_entropy"] - gpu0
+    return Op(
+        "f4_jpeg_decode_preprocess_64x1080p", "jpeg",
+        [("jpeg_decode+preprocess (GPU entropy + reconstruction + resize)", step, nbytes)],
+        dst_px=(hi - lo) * 1920 * 1080, src_px=(hi - lo) * 1920 * 1080, job_dst_px=64 * 1920 * 1080,
+        l2="host JPEG bytes (q90 4:2:0, ~200 KB each)",
+        extra={"mean_stream_kb": round(sum(len(b) for b in streams) / len(streams) / 1e3, 1),
+               "entropy_decoding": f"GPU ({on_gpu}/{hi - lo} images; self-synchronising subsequences)",
+               "px_basis": "decoded 1920x1080 pixels",
+               "e2e_note": "the step itself starts from host JPEG bytes and ends in HBM"},
+        verify=lambda: verify_jpeg(streams, frames, dst),
+        e2e=lambda steps: e2e_jpeg(be, step, dst, steps, 64 * 1920 * 1080, sum(len(b) for b in streams)))
+
+
+def build_dry_ops(be, include):
+    """CPU stand-ins with the real ops' names: the rank plumbing, not kernels."""
+    import torch
+
+    ops = []
+    for name, key, n_total in (("cfg0_gray_u8_1x1080p", "gray", 1), (HEAD, "resize", 64),
+                               ("cfg2_warp_affine_f32_32x1080p", "affine", 32),
+                               ("cfg3_warp_perspective_u8_16x4k", "persp", 16),
+                               ("cfg4_resize_normalize_chw_512x1080p", "fused", 512),
+                               ("f4_jpeg_decode_preprocess_64x1080p", "jpeg", 64)):
+        if key not in include:
+            continue
+        lo, hi = shard(n_total, be.world, be.rank) if key != "gray" else (0, 1)
         n = hi - lo
-        src = synth.device_u8_batch(n, 2160, 3840, 3, synth.SEED_RESIZE + lo, dev)
-        down = torch.zeros((n, 1080, 1920, 3), dtype=torch.uint8, device=dev)
-        up = torch.zeros((n, 4320, 7680, 3), dtype=torch.uint8, device=dev)
-        sb = n * 2160 * 3840 * 3
-        ops["cfg1_resize_u8_64x4k"] = dict(
-            launches=[("resize_down", lambda s=src, d=down: fv.resize_bilinear_u8(s, d), sb + n * 1080 * 1920 * 3),
-                      ("resize_up", lambda s=src, d=up: fv.resize_bilinear_u8(s, d), sb + n * 4320 * 7680 * 3)],
-            dst_px=n * (1920 * 1080 + 7680 * 4320), src_px=2 * n * 3840 * 2160, images=n_total,
-            l2="inputs 1.59 GB >> L2", tensors=(src, down, up))
-
-    if "affine" in include:
-        n_total = 32
-        lo, hi = shard(n_total, world, rank)
-        n = hi - lo
-        src = synth.device_f32_batch(n, 1080, 1920, 3, synth.SEED_AFFINE + lo, dev)
-        dst = torch.zeros_like(src)
-        ms = np.stack([synth.affine_forward(synth.SEED_AFFINE_PARAMS + lo + i, 1920, 1080) for i in range(n)])
-        nominal = 2 * n * 1920 * 1080 * 12
-        foot = footprint_bytes(ms, False, 1080, 1920, 12, dev) + n * 1920 * 1080 * 12
-        ops["cfg2_warp_affine_f32_32x1080p"] = dict(
-            launches=[("warp_affine", lambda s=src, d=dst, m=ms: fv.warp_affine(s, d, m, border=0.0), foot)],
-            dst_px=n * 1920 * 1080, src_px=n * 1920 * 1080, images=n_total, nominal_bytes=nominal,
-            l2="inputs 796 MB >> L2")
-
-    if "persp" in include:
-        n_total = 16
-        lo, hi = shard(n_total, world, rank)
-        n = hi - lo
-        src = synth.device_u8_batch(n, 2160, 3840, 3, synth.SEED_PERSP + lo, dev)
-        dst = torch.zeros_like(src)
-        hs = np.stack([synth.perspective_forward(synth.SEED_PERSP_PARAMS + lo + i) for i in range(n)])
-        nominal = 2 * n * 3840 * 2160 * 3
-        foot = footprint_bytes(hs, True, 2160, 3840, 3, dev) + n * 3840 * 2160 * 3
-        ops["cfg3_warp_perspective_u8_16x4k"] = dict(
-            launches=[("warp_perspective", lambda s=src, d=dst, m=hs: fv.warp_perspective(s, d, m, border=0), foot)],
-            dst_px=n * 3840 * 2160, src_px=n * 3840 * 2160, images=n_total, nominal_bytes=nominal,
-            l2="inputs 398 MB >> L2")
-
-    if "fused" in include:
-        n_total = 512
-        lo, hi = shard(n_total, world, rank)
-        n = hi - lo
-        src = synth.device_u8_batch(n, 1080, 1920, 3, synth.SEED_FUSED + lo, dev)
-        dst = torch.zeros((n, 3, 640, 640), dtype=torch.float32, device=dev)
-        ops["cfg4_resize_normalize_chw_512x1080p"] = dict(
-            launches=[("resize_normalize_chw",
-                       lambda s=src, d=dst: fv.resize_normalize_chw(s, d, synth.MEAN, synth.STD),
-                       n * (1920 * 1080 * 3 + 3 * 640 * 640 * 4))],
-            dst_px=n * 640 * 640, src_px=n * 1920 * 1080, images=n_total, l2="inputs 3.2 GB >> L2")
-
-    if "jpeg" in include:
-        # SURVEY 8f rank 4, decode -> preprocess: host JPEG bytes -> decode
-        # (native batch runtime: threaded entropy decoding, GPU IDCT/colour)
-        # -> fused resize/normalise/CHW 640x640, per step
-        n_total = 64
-        lo, hi = shard(n_total, world, rank)
-        streams = jpeg_streams(lo, hi)
-        dst = torch.empty((hi - lo, 3, 640, 640), dtype=torch.float32, device=dev)
-        frames = torch.empty((hi - lo, 1080, 1920, 3), dtype=torch.uint8, device=dev)
-        from paper_2505_12425_b200 import io as fio
-
-        def step(st=streams, d=dst, fr=frames):
-            fio.decode_jpeg_batch(st, dev, out=fr)  # the frames as one batch ...
-            fv.resize_normalize_chw(fr, d, synth.MEAN, synth.STD)  # ... preprocessed in one launch
-
-        nbytes = sum(len(b) for b in streams) + dst.numel() * 4
-        gpu0 = fio.stats["gpu_entropy"]
-        step()
-        on_gpu = fio.stats["gpu_entropy"] - gpu0
-        ops["f4_jpeg_decode_preprocess_64x1080p"] = dict(
-            launches=[("jpeg_decode+preprocess (GPU entropy + reconstruction + resize)", step, nbytes)],
-            dst_px=(hi - lo) * 1920 * 1080, src_px=(hi - lo) * 1920 * 1080, images=n_total,
-            l2="host JPEG bytes (q90 4:2:0, ~200 KB each)",
-            extra={"mean_stream_kb": round(sum(len(b) for b in streams) / len(streams) / 1e3, 1),
-                   "entropy_decoding": f"GPU ({on_gpu}/{hi - lo} images; self-synchronising subsequences)",
-                   "host_threads": host_cores(), "px_basis": "decoded 1920x1080 pixels",
-                   "cpu_oracle_mps_1core": jpeg_cpu_oracle_mps()})
+        x = torch.arange(max(n, 1) * 4096, dtype=torch.float32)
+        y = torch.empty_like(x)
+        ops.append(Op(name, key, [("dry_copy", lambda x=x, y=y: y.copy_(x), x.numel() * 8)],
+                      dst_px=n * 1000, src_px=n * 1000, job_dst_px=None if key == "gray" else n_total * 1000,
+                      l2="dry run", replicas=key == "gray",
+                      verify=lambda lo=lo, hi=hi: {"verified": True, "checked": f"dry run, images [{lo}, {hi})"},
+                      e2e=lambda steps: {"value": 0.0, "unit": UNIT, "h2d_bytes_per_step": 0,
+                                         "d2h_bytes_per_step": 0, "note": "dry run"}))
     return ops
 
 
@@ -279,26 +686,6 @@ def jpeg_streams(lo, hi):
         Image.fromarray(img).save(buf, format="JPEG", quality=90, subsampling=2)
         out.append(buf.getvalue())
     return out
-
-
-def jpeg_cpu_oracle_mps():
-    """The oracle port of the reference decoder (oracle/jpeg_oracle.py, pure
-    Python like the reference) on one 480x270 frame, one core: decoded MP/s."""
-    import io as pyio
-
-    from PIL import Image
-
-    from paper_2505_12425_b200 import synth
-
-    sys.path.insert(0, os.path.join(ROOT, "oracle"))
-    import jpeg_oracle
-
-    buf = pyio.BytesIO()
-    Image.fromarray(synth.seeded_smooth_u8_image(480, 270, 3, seed=1)).save(buf, format="JPEG", quality=90,
-                                                                           subsampling=2)
-    t = time.perf_counter()
-    jpeg_oracle.decode_jpeg(buf.getvalue())
-    return round(480 * 270 / (time.perf_counter() - t) / 1e6, 3)
 
 
 def footprint_bytes(mats, perspective, h, w, bpp, dev):
@@ -343,184 +730,329 @@ def footprint_bytes(mats, perspective, h, w, bpp, dev):
     return total
 
 
-def time_op(op, steps, warmup, stream, world, soak_s=0.0):
-    """Warmup, then `steps` timed steps bracketed by barrier + synchronize.
-    Per-launch CUDA events (on the launching stream) give each kernel's
-    average duration for the roofline."""
-    import torch
-    import torch.distributed as dist
+# ---------------------------------------------------------------------------
+# timing
+# ---------------------------------------------------------------------------
 
+def time_op(be, op, steps, warmup, stream, soak_s=0.0):
+    """Warmup, then `steps` timed steps bracketed by barrier + synchronize.
+    Per-launch timers (CUDA events on the launching stream) give each
+    kernel's average duration for the roofline. Returns (ms of the whole
+    timed region, per-launch ms, our kernel launches), MAX over ranks for the
+    times and SUM for the launch count."""
     from paper_2505_12425_b200 import _native
 
-    launches = op["launches"]
+    launches = op.launches
     for _ in range(warmup):
         for _, fn, _ in launches:
             fn()
-    torch.cuda.synchronize()
+    be.sync()
     if soak_s > 0:  # untimed soak so the clock sampler sees a loaded GPU
         t_end = time.time() + soak_s
         while time.time() < t_end:
             for _, fn, _ in launches:
                 fn()
-            torch.cuda.synchronize()
-    ev = [[(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in launches]
-          for _ in range(steps)]
-    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    if world > 1:
-        dist.barrier()
-    torch.cuda.synchronize()
-    lc0 = _native.launch_count()
-    t0.record(stream)
-    for s in range(steps):
-        for j, (_, fn, _) in enumerate(launches):
-            ev[s][j][0].record(stream)
+            be.sync()
+    tm = be.timer(stream)
+    be.barrier()
+    be.sync()
+    lc0 = 0 if be.dry else _native.launch_count()
+    marks = []
+    t0 = tm.mark()
+    for _ in range(steps):
+        row = []
+        for _, fn, _ in launches:
+            a = tm.mark()
             fn()
-            ev[s][j][1].record(stream)
-    t1.record(stream)
+            row.append((a, tm.mark()))
+        marks.append(row)
+    t1 = tm.mark()
+    be.sync()
+    lc = len(launches) * steps if be.dry else _native.launch_count() - lc0
+    if op.launches_per_call:
+        lc = steps * op.launches_per_call
+    be.barrier()
+    ms = tm.ms(t0, t1)
+    per = [statistics.fmean(tm.ms(*marks[s][j]) for s in range(steps)) for j in range(len(launches))]
+    vals = be.reduce([ms] + per, "max")
+    lc = int(be.reduce([lc], "sum")[0])
+    return vals[0], vals[1:], lc
+
+
+def gray_api_latency(srcs, dsts, calls=200):
+    """Host wall time per public-API call (validation + ctypes + launch) of
+    fv.gray_from_rgb on resident tensors: back-to-back calls, then one sync;
+    and per call with a synchronize after each (the single-frame latency)."""
+    import torch
+
+    import paper_2505_12425_b200 as fv
+
+    for i in range(8):
+        fv.gray_from_rgb(srcs[i % 32], dsts[i % 32])
     torch.cuda.synchronize()
-    lc = _native.launch_count() - lc0
-    if "launches_per_call" in op:
-        lc = steps * op["launches_per_call"]
-    if world > 1:
-        dist.barrier()
-    ms = t0.elapsed_time(t1)
-    per = [statistics.fmean(ev[s][j][0].elapsed_time(ev[s][j][1]) for s in range(steps)) for j in range(len(launches))]
-    if world > 1:
-        t = torch.tensor([ms] + per, dtype=torch.float64, device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms, per = float(t[0]), [float(v) for v in t[1:]]
-        lct = torch.tensor([lc], dtype=torch.int64, device="cuda")
-        dist.all_reduce(lct)
-        lc = int(lct.item())
-    return ms, per, lc
+    t = time.perf_counter()
+    for i in range(calls):
+        fv.gray_from_rgb(srcs[i % 32], dsts[i % 32])
+    issue = time.perf_counter() - t
+    torch.cuda.synchronize()
+    t = time.perf_counter()
+    for i in range(calls // 4):
+        fv.gray_from_rgb(srcs[i % 32], dsts[i % 32])
+        torch.cuda.synchronize()
+    synced = time.perf_counter() - t
+    return {"issue_us_per_call": round(issue / calls * 1e6, 2),
+            "synced_us_per_call": round(synced / (calls // 4) * 1e6, 2)}
 
 
 # ---------------------------------------------------------------------------
 # e2e: public API with host (pinned) buffers, copies inside the timed region
 # ---------------------------------------------------------------------------
 
-def e2e_resize(steps, world, rank, dev, chunks=8):
-    """cfg1 end to end through the public API from pinned host memory: per
-    step the H2D copy of the 64 source images, both resizes, and the D2H copy
-    of both outputs. The batch is split into `chunks` image groups pipelined
-    over three streams (copy-in, compute, copy-out), so PCIe transfers in both
+_PINNED = {}
+
+
+def pinned(nbytes, slot):
+    """One reusable pinned host buffer per slot (in / out), grown on demand."""
+    import torch
+
+    b = _PINNED.get(slot)
+    if b is None or b.numel() < nbytes:
+        _PINNED.pop(slot, None)
+        del b
+        empty = getattr(torch._C, "_host_emptyCache", None)
+        if empty is not None:  # return the outgrown block instead of caching it
+            empty()
+        b = torch.empty(nbytes, dtype=torch.uint8).pin_memory()
+        _PINNED[slot] = b
+    return b
+
+
+def host_like(t, slot):
+    return pinned(t.numel() * t.element_size(), slot)[: t.numel() * t.element_size()].view(t.dtype).view(t.shape)
+
+
+def e2e_pipeline(be, d_src, d_outs, fn, steps, job_dst_px, chunks=8, warp=None):
+    """The op end to end through the public API from pinned host memory: per
+    step the H2D copy of the inputs, the kernels and the D2H copy of every
+    output. The batch is split into `chunks` image groups pipelined over three
+    streams (copy-in, compute, copy-out), so PCIe transfers in both
     directions overlap each other and the kernels."""
     import torch
-    import torch.distributed as dist
 
     import paper_2505_12425_b200 as fv
 
-    lo, hi = shard(64, world, rank)
-    n = hi - lo
+    dev = be.dev
+    n = d_src.shape[0]
     chunks = max(1, min(chunks, n))
-    h_src = torch.randint(0, 256, (n, 2160, 3840, 3), dtype=torch.uint8).pin_memory()
-    h_down = torch.empty((n, 1080, 1920, 3), dtype=torch.uint8).pin_memory()
-    h_up = torch.empty((n, 4320, 7680, 3), dtype=torch.uint8).pin_memory()
-    d_src = torch.empty(h_src.shape, dtype=torch.uint8, device=dev)
-    d_down = torch.empty(h_down.shape, dtype=torch.uint8, device=dev)
-    d_up = torch.empty(h_up.shape, dtype=torch.uint8, device=dev)
+    h_src = host_like(d_src, "in")
+    h_src.copy_(d_src)  # the step's input content (any content times the same)
+    h_outs = [host_like(d, f"out{i}") for i, d in enumerate(d_outs)]
+    d_in = torch.empty_like(d_src)
     bounds = [(i * n // chunks, (i + 1) * n // chunks) for i in range(chunks)]
     s_in, s_comp, s_out = torch.cuda.Stream(dev), torch.cuda.Stream(dev), torch.cuda.Stream(dev)
     ev_comp = [torch.cuda.Event() for _ in bounds]
     ev_out = [torch.cuda.Event() for _ in bounds]
     first = {"v": True}
 
+    def run(a, b):
+        if warp is not None:
+            mats, persp = warp
+            (fv.warp_perspective if persp else fv.warp_affine)(d_in[a:b], d_outs[0][a:b], mats[a:b])
+        else:
+            fn(d_in[a:b], [d[a:b] for d in d_outs])
+
     def step():
         for i, (a, b) in enumerate(bounds):
             with torch.cuda.stream(s_in):
                 if not first["v"]:
-                    s_in.wait_event(ev_comp[i])  # previous step's kernels done reading d_src[a:b]
-                d_src[a:b].copy_(h_src[a:b], non_blocking=True)
+                    s_in.wait_event(ev_comp[i])  # previous step's kernels done reading d_in[a:b]
+                d_in[a:b].copy_(h_src[a:b], non_blocking=True)
                 ev_in = torch.cuda.Event()
                 ev_in.record(s_in)
             with torch.cuda.stream(s_comp):
                 s_comp.wait_event(ev_in)
                 if not first["v"]:
                     s_comp.wait_event(ev_out[i])  # previous step's D2H of this chunk done
-                fv.resize_bilinear_u8(d_src[a:b], d_down[a:b])
-                fv.resize_bilinear_u8(d_src[a:b], d_up[a:b])
+                run(a, b)
                 ev_comp[i].record(s_comp)
             with torch.cuda.stream(s_out):
                 s_out.wait_event(ev_comp[i])
-                h_down[a:b].copy_(d_down[a:b], non_blocking=True)
-                h_up[a:b].copy_(d_up[a:b], non_blocking=True)
+                for h, d in zip(h_outs, d_outs):
+                    h[a:b].copy_(d[a:b], non_blocking=True)
                 ev_out[i].record(s_out)
         first["v"] = False
 
     step()
     torch.cuda.synchronize()
     t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    if world > 1:
-        dist.barrier()
+    be.barrier()
     t0.record(s_in)
     for _ in range(steps):
         step()
     s_in.wait_stream(s_out)
     t1.record(s_in)
     torch.cuda.synchronize()
-    ms = t0.elapsed_time(t1)
-    if world > 1:
-        t = torch.tensor([ms], dtype=torch.float64, device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t[0])
-    dst_px_total = 64 * (1920 * 1080 + 7680 * 4320)
-    return {"value": dst_px_total * steps / (ms / 1e3) / 1e6, "unit": UNIT,
-            "h2d_bytes_per_step": h_src.numel(), "d2h_bytes_per_step": h_down.numel() + h_up.numel(),
-            "ms_per_step": ms / steps, "steps": steps, "pipeline": f"{chunks} chunks x (H2D | kernels | D2H) streams"}
+    ms = be.reduce([t0.elapsed_time(t1)], "max")[0]
+    h2d = h_src.numel() * h_src.element_size()
+    d2h = sum(h.numel() * h.element_size() for h in h_outs)
+    tot = be.reduce([h2d, d2h], "sum")
+    return {"value": job_dst_px * steps / (ms / 1e3) / 1e6, "unit": UNIT, "h2d_bytes_per_step": int(tot[0]),
+            "d2h_bytes_per_step": int(tot[1]), "ms_per_step": ms / steps, "steps": steps,
+            "pipeline": f"{chunks} chunks x (H2D | kernels | D2H) streams"}
+
+
+def e2e_gray(be, d_src, steps):
+    """cfg0 end to end, one frame per step as a caller would: pinned host
+    frame -> H2D -> fv.gray_from_rgb -> D2H of the gray frame, synchronised
+    per step (single-frame latency, no pipelining across frames)."""
+    import torch
+
+    import paper_2505_12425_b200 as fv
+
+    h_src = host_like(d_src, "in")
+    h_src.copy_(d_src)
+    d_in = torch.empty_like(d_src)
+    d_out = torch.empty((1080, 1920, 1), dtype=torch.uint8, device=be.dev)
+    h_out = host_like(d_out, "out0")
+
+    def step():
+        d_in.copy_(h_src, non_blocking=True)
+        fv.gray_from_rgb(d_in, d_out)
+        h_out.copy_(d_out, non_blocking=True)
+        torch.cuda.current_stream().synchronize()
+
+    for _ in range(3):
+        step()
+    be.barrier()
+    t = time.perf_counter()
+    for _ in range(steps):
+        step()
+    s = be.reduce([time.perf_counter() - t], "max")[0]
+    return {"value": 1920 * 1080 * steps / s / 1e6, "unit": UNIT, "h2d_bytes_per_step": h_src.numel(),
+            "d2h_bytes_per_step": h_out.numel(), "ms_per_step": s / steps * 1e3, "steps": steps,
+            "timing": "host wall clock, one synchronised call per frame (replicas: per-rank value)"}
+
+
+def e2e_jpeg(be, step, dst, steps, job_dst_px, stream_bytes):
+    """decode -> preprocess from host JPEG bytes (the step's own input) with
+    the D2H of the preprocessed f32 batch."""
+    import torch
+
+    h_out = host_like(dst, "out0")
+
+    def run():
+        step()
+        h_out.copy_(dst, non_blocking=True)
+
+    run()
+    torch.cuda.synchronize()
+    be.barrier()
+    t = time.perf_counter()
+    for _ in range(steps):
+        run()
+    torch.cuda.synchronize()
+    s = be.reduce([time.perf_counter() - t], "max")[0]
+    return {"value": job_dst_px * steps / s / 1e6, "unit": UNIT, "h2d_bytes_per_step": int(be.reduce([stream_bytes], "sum")[0]),
+            "d2h_bytes_per_step": int(be.reduce([h_out.numel()], "sum")[0]), "ms_per_step": s / steps * 1e3,
+            "steps": steps, "timing": "host wall clock"}
 
 
 # ---------------------------------------------------------------------------
-# CPU reference path (the oracle port of the reference's NumPy algorithm)
+# verification of the timed outputs (oracle on sampled rows)
 # ---------------------------------------------------------------------------
 
-def _cpu_worker(args):
-    kind, seed, rows = args
-    os.environ["OMP_NUM_THREADS"] = "1"
-    sys.path.insert(0, ROOT)
+def _bands(h, k=4):
+    return [(0, k), (h // 2 - k // 2, h // 2 + k // 2), (h - k, h)]
+
+
+def _cmp(got, ref, tol=0):
+    import numpy as np
+
+    d = np.abs(got.astype(np.float64) - ref.astype(np.float64))
+    return float(d.max()) if d.size else 0.0, int((d > 0).sum())
+
+
+def _summary(results, tol, what):
+    worst = max(r[0] for r in results)
+    diff = sum(r[1] for r in results)
+    return {"verified": bool(worst <= tol), "max_abs_diff": worst, "values_differing": diff,
+            "tolerance": tol, "checked": what}
+
+
+def verify_gray(srcs, dsts, dstb):
     import oracle as O
 
-    a = O.seeded_u8_image(3840, 2160, 3, seed=seed)
-    t = time.perf_counter()
-    if kind == "down":
-        O.resize_u8(a, 1920, 1080)
-        px = 1920 * 1080
-    else:
-        O.resize_u8(a, 7680, 4320, rows=rows)
-        px = 7680 * (rows[1] - rows[0])
-    return kind, px, time.perf_counter() - t
+    res = []
+    for i in (0, srcs.shape[0] - 1):
+        a = srcs[i].cpu().numpy()
+        ref = O.gray_from_rgb(a)
+        res.append(_cmp(dsts[i].cpu().numpy(), ref))
+        res.append(_cmp(dstb[i].cpu().numpy(), ref))
+    return _summary(res, 0, "frames 0 and 31, full, both gray timings (bit-exact)")
 
 
-def cpu_reference(cores, up_rows=270):
-    """Bounded sample of cfg1 on `cores` processes: each worker resizes one
-    full 4K image down to 1080p and one band of `up_rows` destination rows of
-    4K -> 8K (the reference algorithm is row-separable, so a band costs the
-    same per pixel as the full frame). Returns dst MP/s of the full step
-    extrapolated from the per-op rates, and the sample description."""
-    tasks = []
-    for i in range(cores):
-        tasks.append(("down", 20000 + i, None))
-        lo = (i * 977) % (4320 - up_rows)
-        tasks.append(("up", 20000 + i, (lo, lo + up_rows)))
-    ctx = mp.get_context("fork")
-    t0 = time.perf_counter()
-    with ctx.Pool(cores) as pool:
-        res = pool.map(_cpu_worker, tasks, chunksize=1)
-    wall = time.perf_counter() - t0
-    px_down = sum(p for k, p, _ in res if k == "down")
-    px_up = sum(p for k, p, _ in res if k == "up")
-    cpu_down = sum(s for k, _, s in res if k == "down")
-    cpu_up = sum(s for k, _, s in res if k == "up")
-    # per-core rates -> full-step time on `cores` cores
-    r_down = px_down / cpu_down
-    r_up = px_up / cpu_up
-    step_px = 64 * (1920 * 1080 + 7680 * 4320)
-    step_s = (64 * 1920 * 1080 / r_down + 64 * 7680 * 4320 / r_up) / cores
-    return {"value": step_px / step_s / 1e6, "unit": UNIT, "cores": cores, "kind": "port",
-            "sample": f"{cores} procs x (one full 3840x2160->1920x1080 + {up_rows} of 4320 dst rows "
-                      f"3840x2160->7680x4320), oracle/ NumPy port of app.py:64-78; "
-                      f"per-core rates extrapolated to the 64-image step; wall {wall:.1f}s",
-            "wall_s": wall}
+def verify_resize(src, down, up):
+    import oracle as O
 
+    res = []
+    for i in (0, src.shape[0] - 1):
+        a = src[i].cpu().numpy()
+        for lo, hi in _bands(1080):
+            res.append(_cmp(down[i, lo:hi].cpu().numpy(), O.resize_u8(a, 1920, 1080, rows=(lo, hi))))
+        for lo, hi in _bands(4320):
+            res.append(_cmp(up[i, lo:hi].cpu().numpy(), O.resize_u8(a, 7680, 4320, rows=(lo, hi))))
+    return _summary(res, 0, "first and last image of the shard, 3 bands of 4 rows per output (bit-exact)")
+
+
+def verify_warp(src, dst, mats, persp, lo_img):
+    import oracle as O
+
+    res = []
+    h, w = src.shape[1], src.shape[2]
+    for i in (0, src.shape[0] - 1):
+        a = src[i].cpu().numpy()
+        for lo, hi in _bands(h, 8):
+            if persp:
+                ref = O.warp_perspective(a, O.invert_homography(mats[i]), h, w, border=0, rows=(lo, hi))
+            else:
+                ref = O.warp_affine(a, O.invert_affine(mats[i]), h, w, border=0.0, rows=(lo, hi))
+            res.append(_cmp(dst[i, lo:hi].cpu().numpy(), ref))
+    tol = 1 if persp else 0
+    return _summary(res, tol, f"images {lo_img} and {lo_img + src.shape[0] - 1}, 3 bands of 8 rows "
+                              f"({'<= 1 LSB' if persp else 'bit-exact'})")
+
+
+def verify_fused(src, dst):
+    import oracle as O
+    from paper_2505_12425_b200 import synth
+
+    res = []
+    for i in (0, src.shape[0] - 1):
+        a = src[i].cpu().numpy()
+        for lo, hi in _bands(640):
+            ref = O.resize_normalize_chw(a, 640, 640, synth.MEAN, synth.STD, rows=(lo, hi))
+            res.append(_cmp(dst[i, :, lo:hi].cpu().numpy(), ref))
+    return _summary(res, 0, "first and last image of the shard, 3 bands of 4 rows, all channels (bit-exact)")
+
+
+def verify_jpeg(streams, frames, dst):
+    import oracle as O
+    from paper_2505_12425_b200 import synth
+
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import jpeg_oracle
+
+    ref_frame = jpeg_oracle.decode_jpeg(streams[0])
+    res = [_cmp(frames[0].cpu().numpy(), ref_frame)]
+    lo, hi = 300, 308
+    res.append(_cmp(dst[0, :, lo:hi].cpu().numpy(),
+                    O.resize_normalize_chw(ref_frame, 640, 640, synth.MEAN, synth.STD, rows=(lo, hi))))
+    return _summary(res, 0, "image 0: decoded frame (full) and 8 preprocessed rows vs the decoder port (bit-exact)")
+
+
+# ---------------------------------------------------------------------------
+# main
+# ---------------------------------------------------------------------------
 
 def headline_config(world):
     """The `config` object of both arms' JSON line (BASELINE.json configs[1])."""
@@ -530,18 +1062,7 @@ def headline_config(world):
             "l2": "inputs 1.59 GB >> 126 MB L2 (no flush needed)"}
 
 
-def host_cores():
-    try:
-        return len(os.sched_getaffinity(0))
-    except AttributeError:
-        return os.cpu_count() or 1
-
-
-# ---------------------------------------------------------------------------
-# main
-# ---------------------------------------------------------------------------
-
-def main():
+def parse_args(argv=None):
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)
@@ -550,142 +1071,153 @@ def main():
     ap.add_argument("--ops", default="gray,resize,affine,persp,fused,jpeg")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-verify", action="store_true")
     ap.add_argument("--cpu-cores", type=int, default=0)
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--dry-run", action="store_true", help="CPU/gloo stand-in ops: exercises the rank plumbing")
     ap.add_argument("--soak", type=float, default=1.0,
                     help="seconds of untimed cfg1 steps before timing (clock sampler sees a loaded GPU)")
-    args = ap.parse_args()
+    return ap.parse_args(argv)
+
+
+def main(argv=None):
+    argv = sys.argv[1:] if argv is None else argv
+    args = parse_args(argv)
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(relaunch(args.gpus, argv))
     world, rank, local = dist_env()
-
+    if world != args.gpus:
+        sys.exit(f"bench.py: launched with WORLD_SIZE={world} but --gpus {args.gpus}")
     if args.impl == "reference":
-        if rank != 0:
-            return
-        cores = args.cpu_cores or host_cores()
-        vals = []
-        for i in range(args.warmup + args.steps):
-            r = cpu_reference(cores, up_rows=60)
-            if i >= args.warmup:
-                vals.append(r)
-        v = statistics.median(x["value"] for x in vals)
-        step_px = 64 * (1920 * 1080 + 7680 * 4320)
-        line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
-                "steps": args.steps, "warmup": args.warmup, "ms_per_step": step_px / (v * 1e6) * 1e3,
-                "higher_is_better": True, "scaling": "strong",
-                "vs_baseline": None, "dtype": "u8", "data": "synthetic (seeded uniform u8)",
-                "config": dict(headline_config(1), parallelism=f"{cores} host processes (reference NumPy path)"),
-                "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "port",
-                                 "sample": vals[0]["sample"]},
-                "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
-        print(json.dumps(line))
+        if rank == 0:
+            run_reference(args)
         return
+    run_fovea(args, world, rank, local)
 
-    import torch
-    import torch.distributed as dist
 
-    if world > 1:
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    dev = torch.device("cuda", local if world > 1 else 0)
-    torch.cuda.set_device(dev)
-    from paper_2505_12425_b200 import _native
+def run_reference(args):
+    """The reference CPU path on the host cores (rank 0 only): each step one
+    bounded all-core sample of the headline workload, same sample as the
+    fovea arm's cpu_baseline; per-op all-core numbers under "ops"."""
+    cores = args.cpu_cores or host_cores()
+    vals = []
+    for i in range(args.warmup + args.steps):
+        r = cpu_baseline("resize" if not args.dry_run else "dry", cores, one_core=i == args.warmup)
+        if i >= args.warmup:
+            vals.append(r)
+    v = statistics.median(x["value"] for x in vals)
+    step_px = 64 * (1920 * 1080 + 7680 * 4320)
+    ops = {}
+    if not args.dry_run:
+        for op in [o for o in args.ops.split(",") if o not in ("resize",)]:
+            r = cpu_baseline(op, cores)
+            ops[op] = {k: r[k] for k in ("value", "value_1core", "cores", "sample")}
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": step_px / (v * 1e6) * 1e3,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "u8",
+            "data": "synthetic (seeded uniform u8)",
+            "config": dict(headline_config(1), parallelism=f"{cores} host processes (reference NumPy path)"),
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "port",
+                             "value_1core": vals[0]["value_1core"],
+                             "sample": CPU_SAMPLE["resize"] + "; oracle/ NumPy port of the reference"},
+            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "ops": ops}
+    print(json.dumps(line))
 
-    _native.lib()
+
+def run_fovea(args, world, rank, local):
+    be = Backend(args.dry_run, world, rank, local)
+    if not be.dry:
+        from paper_2505_12425_b200 import _native
+
+        _native.lib()
+        stream = be.torch.cuda.current_stream(be.dev)
+    else:
+        stream = None
     peak, peak_src = load_peaks()
     include = set(args.ops.split(","))
-    ops = build_ops(1, world, rank, dev, include)
-    stream = torch.cuda.current_stream(dev)
-    sampler = ClockSampler(dev.index if dev.index is not None else 0)
-    sampler.start()
+    ops = build_ops(be, include)
+    sampler = ClockSampler(be.dev.index if (not be.dry and be.dev.index is not None) else 0)
+    if not be.dry:
+        sampler.start()
     results = {}
-    total_launches = 0
-    for name, op in ops.items():
-        soak = args.soak if name.startswith("cfg1") else 0.0
-        ms, per, lc = time_op(op, args.steps, max(3, args.warmup), stream, world, soak_s=soak)
-        total_launches += lc if name.startswith("cfg1") else 0
+    for op in ops:
+        soak = args.soak if (op.key == "resize" and not be.dry) else 0.0
+        ms, per, lc = time_op(be, op, args.steps, max(3, args.warmup), stream, soak_s=soak)
         kern = []
-        for (lname, _, nbytes), t in zip(op["launches"], per):
+        for (lname, _, nbytes), t in zip(op.launches, per):
             gbs = nbytes / (t / 1e3) / 1e9
             kern.append({"kernel": lname, "ms": t, "algorithmic_bytes": nbytes, "gbs": gbs, "frac": gbs / peak})
-        results[name] = dict(ms_per_step=ms / args.steps, kernels=kern, lc=lc, op=op)
+        results[op.name] = dict(ms_per_step=ms / args.steps, kernels=kern, lc=lc, op=op)
     sampler.stop()
-    clocks = sampler.summary()
+    clocks = sampler.summary() if not be.dry else {"sm_mhz": None, "reasons": ["dry run"]}
 
-    # whole-job values (all ranks): per-rank shards sum to the batch
-    def job_mps(name):
-        r = results[name]
+    def job_mps(r):
         op = r["op"]
-        if op.get("replicas"):
-            px = op["dst_px"] * world
-        else:
-            px = per_batch_dst_px(name)
+        px = op.dst_px * world if op.replicas else op.job_dst_px
         return px / (r["ms_per_step"] / 1e3) / 1e6
 
     summary = {}
     for name, r in results.items():
+        op = r["op"]
         # src_mps: the reference harness's convention (MP/s over SOURCE
         # pixels, bench.py:151 of the reference); dst_mps is the primary basis
-        src_mps = job_mps(name) * r["op"]["src_px"] / r["op"]["dst_px"]
-        summary[name] = {"dst_mps": job_mps(name), "src_mps": src_mps, "ms_per_step": r["ms_per_step"],
-                         **r["op"].get("extra", {}),
+        summary[name] = {"dst_mps": job_mps(r), "src_mps": job_mps(r) * op.src_px / op.dst_px,
+                         "ms_per_step": r["ms_per_step"], **op.extra,
                          "kernels": [{k: (round(v, 4) if isinstance(v, float) else v) for k, v in kk.items()}
                                      for kk in r["kernels"]],
-                         "l2": r["op"]["l2"]}
-        if "nominal_bytes" in r["op"]:
-            summary[name]["nominal_bytes_per_rank"] = r["op"]["nominal_bytes"]
+                         "frac": round(max(k["frac"] for k in r["kernels"]), 4), "l2": op.l2}
+        if op.nominal_bytes:
+            summary[name]["nominal_bytes_per_rank"] = op.nominal_bytes
 
-    e2e = None
-    if "resize" in include and not args.no_e2e:
-        e2e = e2e_resize(max(1, min(args.steps, 3)), world, rank, dev)
+    # post-timing checks and end-to-end runs (outside the timed regions)
+    for name, r in results.items():
+        op = r["op"]
+        if not args.no_verify and op.verify is not None:
+            v = op.verify()
+            oks = be.gather(v["verified"])
+            v["verified"] = all(oks)
+            summary[name]["verify"] = v
+            summary[name]["verified"] = v["verified"]
+        if not args.no_e2e and op.e2e is not None:
+            summary[name]["e2e"] = op.e2e(args.e2e_steps if op.key != "gray" else max(args.steps, 20))
+
+    devices = be.gather(be.device_id())
+    if rank == 0 and world == 1 and not args.no_cpu:
+        cores = args.cpu_cores or host_cores()
+        for name, r in results.items():
+            cb = cpu_baseline("dry" if be.dry else r["op"].key, cores)
+            summary[name]["cpu_baseline"] = cb
 
     if rank == 0:
-        head = "cfg1_resize_u8_64x4k"
-        if head in results:
-            r = results[head]
-            dom = max(r["kernels"], key=lambda k: k["ms"])
-            value = job_mps(head)
-            ms_step = r["ms_per_step"]
-            gpu_launches = r["lc"]
-        else:
-            name0 = next(iter(results))
-            r = results[name0]
-            dom = max(r["kernels"], key=lambda k: k["ms"])
-            value = job_mps(name0)
-            ms_step = r["ms_per_step"]
-            gpu_launches = r["lc"]
-        cpu = None
-        if world == 1 and not args.no_cpu:
-            cpu = cpu_reference(args.cpu_cores or host_cores())
-            cpu.pop("wall_s", None)
+        head = HEAD if HEAD in results else next(iter(results))
+        r = results[head]
+        dom = max(r["kernels"], key=lambda k: k["ms"])
+        traffic = load_traffic().get(dom["kernel"], {})
+        cpu = summary[head].get("cpu_baseline")
         line = {
-            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
-            "vs_baseline": None, "dtype": "u8", "data": "synthetic (seeded uniform u8/f32, generated on device)",
+            "metric": METRIC, "value": job_mps(r), "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": r["ms_per_step"], "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "u8",
+            "data": "synthetic (seeded uniform u8/f32, generated on device)" if not be.dry else "dry run",
             "config": headline_config(world),
             "roofline": {"bound": "hbm", "kernel": dom["kernel"], "achieved": dom["gbs"], "peak": peak,
                          "peak_source": peak_src, "unit": "GB/s", "frac": dom["gbs"] / peak,
-                         "traffic": load_traffic().get(dom["kernel"], {}).get("dram_bytes"),
-                         "traffic_source": load_traffic().get(dom["kernel"], {}).get("source"),
-                         "algorithmic_bytes_per_launch": dom["algorithmic_bytes"],
-                         "launch_ms": dom["ms"]},
-            "cpu_baseline": cpu,
-            "e2e": e2e,
-            "gpu_launches": gpu_launches,
+                         "traffic": traffic.get("dram_bytes"), "traffic_source": traffic.get("source"),
+                         "algorithmic_bytes_per_launch": dom["algorithmic_bytes"], "launch_ms": dom["ms"]},
+            "cpu_baseline": ({k: cpu[k] for k in ("value", "unit", "cores", "kind", "sample", "value_1core")}
+                             if cpu else None),
+            "e2e": summary[head].get("e2e"),
+            "gpu_launches": r["lc"],
+            "gpus_active": len({d["bus_id"] for d in devices}),
+            "devices": devices,
             "clocks": clocks,
             "ops": summary,
         }
+        if be.dry:
+            line["dry_run"] = True
         print(json.dumps(line))
-    if world > 1:
-        dist.barrier()
-        dist.destroy_process_group()
-
-
-def per_batch_dst_px(name):
-    return {
-        "cfg1_resize_u8_64x4k": 64 * (1920 * 1080 + 7680 * 4320),
-        "cfg2_warp_affine_f32_32x1080p": 32 * 1920 * 1080,
-        "cfg3_warp_perspective_u8_16x4k": 16 * 3840 * 2160,
-        "cfg4_resize_normalize_chw_512x1080p": 512 * 640 * 640,
-        "f4_jpeg_decode_preprocess_64x1080p": 64 * 1920 * 1080,
-    }[name]
+    be.close()
 
 
 if __name__ == "__main__":

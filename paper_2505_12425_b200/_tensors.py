@@ -88,15 +88,53 @@ def _extent(t: torch.Tensor):
     return lo, lo + span * t.element_size()
 
 
+def _runs(t: torch.Tensor):
+    """Byte intervals [start, end) of `t`'s contiguous runs (the trailing
+    dimensions merged while they are contiguous), sorted, or None when they
+    are not disjoint and increasing (then the caller stays conservative)."""
+    import numpy as np
+
+    shape, stride = list(t.shape), list(t.stride())
+    if any(s == 0 for s in shape):
+        return np.empty(0, np.int64), np.empty(0, np.int64)
+    run, k = 1, len(shape) - 1
+    while k >= 0 and (shape[k] == 1 or stride[k] == run):
+        run *= shape[k]
+        k -= 1
+    offs = np.zeros(1, np.int64)
+    for d in range(k + 1):
+        offs = (offs[:, None] + np.arange(shape[d], dtype=np.int64)[None, :] * stride[d]).reshape(-1)
+    es = t.element_size()
+    starts = np.sort(offs) * es + t.data_ptr()
+    ends = starts + run * es
+    if starts.size > 1 and np.any(starts[1:] < ends[:-1]):
+        return None
+    return starts, ends
+
+
 def check_distinct(a: torch.Tensor, b: torch.Tensor) -> None:
-    """imgproc.py:38-40 (`np.shares_memory`), as a conservative storage-range
-    overlap test: overlapping address ranges are rejected."""
+    """imgproc.py:38-40 (`np.shares_memory`): AliasedBuffers when the two
+    tensors share any byte. Disjoint address ranges pass at once; otherwise
+    the exact test compares the tensors' contiguous runs (image rows), so
+    interleaved views that share no element -- e.g. the left and right halves
+    of one image -- are accepted, as NumPy accepts them."""
     if a.device != b.device:
         return
     a0, a1 = _extent(a)
     b0, b1 = _extent(b)
-    if a0 < b1 and b0 < a1:
-        raise AliasedBuffers("source and destination must not share storage")
+    if not (a0 < b1 and b0 < a1):
+        return
+    import numpy as np
+
+    ra, rb = _runs(a), _runs(b)
+    if ra is not None and rb is not None:
+        (as_, ae), (bs, be) = ra, rb
+        # for every run of b, the last run of a starting before b's end
+        j = np.searchsorted(as_, be, side="left") - 1
+        ok = j >= 0
+        if not np.any(ae[j[ok]] > bs[ok]):
+            return
+    raise AliasedBuffers("source and destination must not share storage")
 
 
 def same_device(*ts) -> None:

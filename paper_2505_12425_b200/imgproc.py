@@ -12,6 +12,7 @@ there is no CPU fallback: CPU tensors raise `UnsupportedDevice`.
 from __future__ import annotations
 
 import ctypes
+import functools
 
 import numpy as np
 import torch
@@ -110,7 +111,13 @@ def normalize_lut(mean, std) -> np.ndarray:
     return np.ascontiguousarray(((unit[None, :] - mean[:, None]) / std[:, None]).astype(np.float32))
 
 
-_LUT_CACHE: dict = {}
+@functools.lru_cache(maxsize=64)
+def _cached_lut(mean: tuple, std: tuple) -> np.ndarray:
+    """normalize_lut per (mean, std) as f32 tuples; bounded (a service that
+    normalises with per-request statistics does not grow it without limit)."""
+    lut = normalize_lut(mean, std)
+    lut.setflags(write=False)
+    return lut
 
 
 def resize_normalize_chw(src: torch.Tensor, dst: torch.Tensor, mean, std) -> None:
@@ -130,12 +137,8 @@ def resize_normalize_chw(src: torch.Tensor, dst: torch.Tensor, mean, std) -> Non
         raise SizeMismatch(f"source batch {s.n} and destination batch {n} differ")
     if c > 4:
         raise ShapeMismatch(f"fused preprocessing supports up to 4 channels, got {c}")
-    key = (tuple(np.asarray(mean, np.float32).reshape(-1).tolist()),
-           tuple(np.asarray(std, np.float32).reshape(-1).tolist()))
-    lut = _LUT_CACHE.get(key)
-    if lut is None:
-        lut = normalize_lut(mean, std)
-        _LUT_CACHE[key] = lut
+    lut = _cached_lut(tuple(np.asarray(mean, np.float32).reshape(-1).tolist()),
+                      tuple(np.asarray(std, np.float32).reshape(-1).tolist()))
     if lut.shape[0] != c:
         raise ShapeMismatch(f"mean/std have {lut.shape[0]} channels, image has {c}")
     check_distinct(src, dst)

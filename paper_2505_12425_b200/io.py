@@ -108,7 +108,8 @@ def decode_jpeg(data, device=None) -> torch.Tensor:
     dev = _device(device)
     info = jpeg_info(buf)
     coef, width = _decode_coeffs(buf, info, pinned=True)
-    return _reconstruct(info, coef, width, dev)
+    with torch.cuda.device(dev):  # the library launches on the current device's stream
+        return _reconstruct(info, coef, width, dev)
 
 
 class _Staging:
@@ -182,6 +183,13 @@ def decode_jpeg_batch(streams: Sequence, device=None, threads: int | None = None
     if entropy not in ("gpu", "host"):
         raise ValueError(f"entropy must be 'gpu' or 'host', got {entropy!r}")
     dev = _device(device)
+    # every native call below allocates / launches on the current device
+    # (pinned staging, streams): make it `dev` even when it is not current
+    with torch.cuda.device(dev):
+        return _decode_batch(streams, dev, threads, entropy, out)
+
+
+def _decode_batch(streams, dev, threads, entropy, out):
     bufs = [_bytes(d) for d in streams]
     n = len(bufs)
     if n == 0:

@@ -103,6 +103,24 @@ class TestCheckOrder:
         with pytest.raises(AliasedBuffers):
             fv.resize_bilinear(p[:4], p[2:6])
 
+    def test_alias_test_is_exact_like_np_shares_memory(self):
+        """imgproc.py:38-40 uses np.shares_memory: interleaved views of one
+        parent that share no element pass, any shared element is rejected."""
+        import numpy as np
+
+        from paper_2505_12425_b200._tensors import check_distinct
+
+        p = f32(6, 10, 3)
+        cases = [(p[:, :5], p[:, 5:]), (p[:, :6], p[:, 5:]), (p[:3], p[3:]), (p[:4], p[3:]),
+                 (p[::2], p[1::2]), (p[:, ::2], p[:, 1::2]), (p[1:3, 2:7], p[2:5, 6:9]), (p[1:3, 2:6], p[2:5, 6:9])]
+        for a, b in cases:
+            shares = np.shares_memory(a.numpy(), b.numpy())
+            if shares:
+                with pytest.raises(AliasedBuffers):
+                    check_distinct(a, b)
+            else:
+                check_distinct(a, b)
+
     def test_to_float_scaled_order(self):
         with pytest.raises(UnsupportedDtype):
             fv.to_float_scaled(f32(2, 2, 3), f32(2, 2, 3))
