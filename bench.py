@@ -668,7 +668,7 @@ def build_dry_ops(be, include):
 
 
 def jpeg_streams(lo, hi):
-    """Seeded smooth 1080p frames (synth.seeded_smooth_u8_image, the
+    """Seeded smooth 1080p frames (synth_fixtures.seeded_smooth_u8_image, the
     reference's codec fixture) as Pillow q90 4:2:0 JPEGs: 4 base frames,
     each image a distinct cyclic shift of one of them."""
     import io as pyio
@@ -678,7 +678,9 @@ def jpeg_streams(lo, hi):
 
     from paper_2505_12425_b200 import synth
 
-    bases = [synth.seeded_smooth_u8_image(1920, 1080, 3, seed=70000 + b) for b in range(4)]
+    import synth_fixtures
+
+    bases = [synth_fixtures.seeded_smooth_u8_image(1920, 1080, 3, seed=70000 + b) for b in range(4)]
     out = []
     for i in range(lo, hi):
         img = np.roll(bases[i % 4], shift=(37 * i, 101 * i), axis=(0, 1))

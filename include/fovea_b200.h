@@ -253,20 +253,29 @@ int fv_jpeg_batch_run_gpu(void* handle, uint8_t* planes, const int64_t* plane_of
                           const int64_t* dst_pitch, int32_t* status, void* stream);
 void fv_jpeg_batch_free(void* handle);
 
-/* ---- tuning / introspection ---------------------------------------------
+/* ---- test-only kernel selection -------------------------------------------
+ * Present only in the test build of the library (-DFV_TEST_KNOBS:
+ * lib/libfovea_b200_knobs.so); the product library always selects
+ * automatically and exports neither symbol. Process-global, not
+ * thread-safe: for the parity tests that cover every GPU path.
  * Resize kernel selection: 0 = auto (default: exact 2:1 / 1:2 fast paths,
  * else the staged TMA strip kernel, else the direct-gather kernel),
  * 1 = always the direct-gather kernel, 2 = never the integer-ratio fast
  * paths. Exposed so the parity tests cover every GPU path. */
+#ifdef FV_TEST_KNOBS
 void fv_set_resize_path(int32_t mode);
+#endif
 
 /* Affine warp kernel selection: 0 = auto (default: the SMEM-staged tile
  * kernel when rows are 16-byte aligned -- the source window loaded by one
  * TMA tensor copy per tile, or by per-row bulk copies when no tensor map can
  * be encoded -- with direct gathers for tiles whose source box exceeds the
  * window), 1 = always the direct-gather kernel, 2 = the bulk-copy tile
- * kernel. Perspective warps always gather directly. */
+ * kernel, 3 = the round-1 u8 perspective kernel (A/B reference for the
+ * tile kernel). */
+#ifdef FV_TEST_KNOBS
 void fv_set_warp_path(int32_t mode);
+#endif
 
 #ifdef __cplusplus
 }

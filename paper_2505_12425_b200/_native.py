@@ -15,6 +15,9 @@ from .errors import NativeError
 # FOVEA_B200_LIB overrides the in-tree library (A/B builds of the same ABI)
 LIB_PATH = os.environ.get("FOVEA_B200_LIB") or os.path.join(
     os.path.dirname(os.path.abspath(__file__)), "lib", "libfovea_b200.so")
+# test build (-DFV_TEST_KNOBS): the same kernels plus the path-selection knobs
+KNOBS_PATH = os.environ.get("FOVEA_B200_KNOBS_LIB") or os.path.join(
+    os.path.dirname(os.path.abspath(__file__)), "lib", "libfovea_b200_knobs.so")
 
 _c = ctypes
 _I64, _I32, _P, _D = _c.c_int64, _c.c_int32, _c.c_void_p, _c.c_double
@@ -25,8 +28,6 @@ SIGNATURES = {
     "fv_version": ([], _c.c_int),
     "fv_last_error": ([], _c.c_char_p),
     "fv_launch_count": ([], _c.c_uint64),
-    "fv_set_resize_path": ([_I32], None),
-    "fv_set_warp_path": ([_I32], None),
     "fv_gray_from_rgb_u8": (_IMG2 + [_I32, _I32, _I32, _P], _c.c_int),
     "fv_gray_from_rgb_f32": (_IMG2 + [_I32, _I32, _I32, _P], _c.c_int),
     "fv_to_float_scaled": (_IMG2 + [_I32, _I32, _I32, _I32, _P], _c.c_int),
@@ -80,29 +81,46 @@ SIGNATURES.update({
 
 FV_ECORRUPT, FV_EUNSUPPORTED, FV_ERANGE, FV_EFALLBACK = -3, -4, -5, -6
 
-_lib = None
+KNOB_SIGNATURES = {"fv_set_resize_path": ([_I32], None), "fv_set_warp_path": ([_I32], None)}
+
+_libs = {}
+_use_knobs = False
 _lock = threading.Lock()
 
 
+def _load(path, knobs):
+    if not os.path.exists(path):
+        raise NativeError(
+            f"CUDA library not built: {path} is missing "
+            "(run `python -m paper_2505_12425_b200._build`); there is no CPU fallback")
+    import torch  # noqa: F401  -- loads the shared libcudart the library binds to
+    handle = ctypes.CDLL(path)
+    for name, (args, res) in {**SIGNATURES, **(KNOB_SIGNATURES if knobs else {})}.items():
+        fn = getattr(handle, name)
+        fn.argtypes = args
+        fn.restype = res
+    return handle
+
+
 def lib():
-    """The loaded library (loaded on first use)."""
-    global _lib
-    if _lib is not None:
-        return _lib
+    """The loaded library (loaded on first use): the product build, or the
+    test build while `use_test_build(True)` is in effect."""
+    key = "knobs" if _use_knobs else "product"
+    h = _libs.get(key)
+    if h is not None:
+        return h
     with _lock:
-        if _lib is None:
-            if not os.path.exists(LIB_PATH):
-                raise NativeError(
-                    f"CUDA library not built: {LIB_PATH} is missing "
-                    "(run `python -m paper_2505_12425_b200._build`); there is no CPU fallback")
-            import torch  # noqa: F401  -- loads the shared libcudart the library binds to
-            handle = ctypes.CDLL(LIB_PATH)
-            for name, (args, res) in SIGNATURES.items():
-                fn = getattr(handle, name)
-                fn.argtypes = args
-                fn.restype = res
-            _lib = handle
-    return _lib
+        if key not in _libs:
+            _libs[key] = _load(KNOBS_PATH if _use_knobs else LIB_PATH, _use_knobs)
+    return _libs[key]
+
+
+def use_test_build(on: bool) -> None:
+    """Tests and A/B tools only: route every call through the test build
+    (lib/libfovea_b200_knobs.so, -DFV_TEST_KNOBS), whose fv_set_resize_path /
+    fv_set_warp_path force a particular kernel. Process-global."""
+    global _use_knobs
+    _use_knobs = bool(on)
 
 
 def call(name: str, *args) -> None:

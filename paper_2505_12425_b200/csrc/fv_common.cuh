@@ -8,10 +8,39 @@
 
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <cstdio>
 
 #include "../../include/fovea_b200.h"
 
 namespace fv {
+
+// ---------------------------------------------------------------------------
+// device-side bounds checks (the checked build, -DFV_DEVICE_CHECKS: every
+// TMA copy's shared-memory destination, and the staged kernels' shared-memory
+// reads and copy sources against their buffers; compute-sanitizer is not
+// available on the GPU pool, tools/checked_run.sh runs this build instead)
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t dyn_smem_size() {
+  uint32_t r;
+  asm("mov.u32 %0, %%dynamic_smem_size;" : "=r"(r));
+  return r;
+}
+#ifdef FV_DEVICE_CHECKS
+__device__ __noinline__ inline void check_fail(const char* file, int line, const char* cond) {
+  printf("FV_CHECK failed %s:%d: %s (block %d %d %d thread %d)\n", file, line, cond, blockIdx.x, blockIdx.y,
+         blockIdx.z, threadIdx.x + blockDim.x * threadIdx.y);
+  __trap();
+}
+#define FV_CHECK(cond) ((cond) ? (void)0 : ::fv::check_fail(__FILE__, __LINE__, #cond))
+#else
+#define FV_CHECK(cond) ((void)0)
+#endif
+// [addr, addr + bytes) inside the dynamic shared-memory allocation
+__device__ __forceinline__ bool in_dyn_smem(uint32_t addr, uint32_t bytes) {
+  extern __shared__ __align__(16) uint8_t fv_dyn_smem_base[];
+  const uint32_t b = static_cast<uint32_t>(__cvta_generic_to_shared(fv_dyn_smem_base));
+  return addr >= b && addr + bytes <= b + dyn_smem_size();
+}
 
 // ---------------------------------------------------------------------------
 // error / launch bookkeeping (fv_util.cu)
@@ -258,6 +287,8 @@ __device__ __forceinline__ void mbar_wait_block(uint64_t* bar, uint32_t parity) 
 // 1-D bulk copy global -> shared, completion signalled on `bar` (TMA unit,
 // SASS UBLKCP). dst/src 16-byte aligned, bytes a multiple of 16.
 __device__ __forceinline__ void tma_bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  FV_CHECK(in_dyn_smem(smem_u32(dst), bytes) && (bytes & 15) == 0 && (smem_u32(dst) & 15) == 0 &&
+           (reinterpret_cast<uintptr_t>(src) & 15) == 0);
   asm volatile(
       "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
           smem_u32(dst)),

@@ -14,6 +14,10 @@
 // pixels per thread as 3 x 16 B loads and one 16 B store.
 #include "fv_common.cuh"
 
+#ifndef FV_GRAY_DP4A
+#define FV_GRAY_DP4A 1  // vec kernel: luma by two IDP4A per pixel (A/B knob: 0 = per-byte extraction)
+#endif
+
 namespace fv {
 
 __device__ __forceinline__ uint32_t gray_u8_px(uint32_t r, uint32_t g, uint32_t b) {
@@ -27,8 +31,27 @@ __device__ __forceinline__ uint32_t gray_u8_px(uint32_t r, uint32_t g, uint32_t 
   return q;
 }
 
+// The same from a word holding (r, g, b) in its low three bytes: S + 500 =
+// 256 (r + 2g) + (43r + 75g + 114b + 500) as two byte dot products (IDP4A).
+__device__ __forceinline__ uint32_t gray_u8_word(uint32_t v) {
+  const uint32_t lo = __dp4a(v, 0x00724B2Bu, 500u);  // 43 r + 75 g + 114 b + 500
+  const uint32_t hi = __dp4a(v, 0x00000201u, 0u);    // r + 2 g
+  const uint32_t s = (hi << 8) + lo;
+  uint32_t q = __umulhi(s, 274877907u) >> 6;  // s / 1000 for s <= 255500
+  if (s == q * 1000u) {
+    const uint32_t r = v & 0xFF, g = (v >> 8) & 0xFF, b = (v >> 16) & 0xFF;
+    const double x = __dadd_rn(__dadd_rn(__dmul_rn((double)r, 0.299), __dmul_rn((double)g, 0.587)),
+                               __dmul_rn((double)b, 0.114));
+    q = (uint32_t)floor(__dadd_rn(x, 0.5));
+  }
+  return q;
+}
+
 // 16 pixels per thread; all of src/dst base, pitch and image stride are
-// 16-byte aligned (checked on the host).
+// 16-byte aligned (checked on the host). Luma by two IDP4A per pixel
+// (gray_u8_word): 0.058 -> 0.050 ms for 32 1080p frames in one launch (the
+// per-byte extraction made this kernel issue-bound); loading two or four
+// rows per thread before the arithmetic measured slower (0.060 / 0.064 ms).
 __global__ void __launch_bounds__(128) gray_u8_vec_kernel(const uint8_t* __restrict__ src, int64_t s_is,
                                                           int64_t s_rp, uint8_t* __restrict__ dst,
                                                           int64_t d_is, int64_t d_rp, int h, int w) {
@@ -48,6 +71,17 @@ __global__ void __launch_bounds__(128) gray_u8_vec_kernel(const uint8_t* __restr
       v[2] = __ldg(s4 + 2);
       const uint32_t* wd = reinterpret_cast<const uint32_t*>(v);
       uint32_t out[4] = {0, 0, 0, 0};
+#if FV_GRAY_DP4A
+      uint32_t q[16];
+#pragma unroll
+      for (int i = 0; i < 16; ++i) {
+        const int k = 3 * i;  // pixel i's bytes start at byte k of the 48
+        const uint32_t w3 = (k & 3) ? __funnelshift_r(wd[k >> 2], wd[(k >> 2) + 1], (k & 3) * 8) : wd[k >> 2];
+        q[i] = gray_u8_word(w3);
+      }
+#pragma unroll
+      for (int j = 0; j < 4; ++j) out[j] = pack4(q[4 * j], q[4 * j + 1], q[4 * j + 2], q[4 * j + 3]);
+#else
 #pragma unroll
       for (int i = 0; i < 16; ++i) {
         const int k = 3 * i;
@@ -56,6 +90,7 @@ __global__ void __launch_bounds__(128) gray_u8_vec_kernel(const uint8_t* __restr
         uint32_t b = (wd[(k + 2) >> 2] >> (((k + 2) & 3) * 8)) & 0xFF;
         out[i >> 2] |= gray_u8_px(r, g, b) << ((i & 3) * 8);
       }
+#endif
       __stcs(reinterpret_cast<uint4*>(d), make_uint4(out[0], out[1], out[2], out[3]));
     } else {
       for (int i = 0; x0 + i < w; ++i) d[i] = (uint8_t)gray_u8_px(s[3 * i], s[3 * i + 1], s[3 * i + 2]);
@@ -125,6 +160,16 @@ __global__ void __launch_bounds__(kFlatThreads) gray_u8_flat_kernel(const uint8_
       for (int k = 0; k < 3; ++k) wd[k] = __ldg(s1 + k);
     }
     uint32_t out[PX / 4];
+#if FV_GRAY_DP4A
+    uint32_t q[PX];
+#pragma unroll
+    for (int i = 0; i < PX; ++i) {
+      const int k = 3 * i;
+      q[i] = gray_u8_word((k & 3) ? __funnelshift_r(wd[k >> 2], wd[(k >> 2) + 1], (k & 3) * 8) : wd[k >> 2]);
+    }
+#pragma unroll
+    for (int j = 0; j < PX / 4; ++j) out[j] = pack4(q[4 * j], q[4 * j + 1], q[4 * j + 2], q[4 * j + 3]);
+#else
 #pragma unroll
     for (int i = 0; i < PX / 4; ++i) out[i] = 0;
 #pragma unroll
@@ -135,6 +180,7 @@ __global__ void __launch_bounds__(kFlatThreads) gray_u8_flat_kernel(const uint8_
       uint32_t b = (wd[(k + 2) >> 2] >> (((k + 2) & 3) * 8)) & 0xFF;
       out[i >> 2] |= gray_u8_px(rr, g, b) << ((i & 3) * 8);
     }
+#endif
     if (PX == 16) __stcs(reinterpret_cast<uint4*>(d), make_uint4(out[0], out[1], out[2], out[3]));
     else if (PX == 8) __stcs(reinterpret_cast<uint2*>(d), make_uint2(out[0], out[1]));
     else __stcs(reinterpret_cast<unsigned int*>(d), out[0]);

@@ -198,6 +198,7 @@ __device__ __noinline__ void pt_pixel_generic(const WarpArgs& a, const uint8_t* 
       uint32_t v;
       if constexpr (STAGED) {
         const uint32_t ad = win + (uint32_t)((y - cy0) * pt_pitch<C>() + x * C + c - sb0);
+        FV_CHECK(y >= cy0 && y - cy0 < PT_WROWS && x * C + c >= sb0 && x * C + c - sb0 < pt_pitch<C>() - 16);
         asm volatile("ld.shared.u8 %0, [%1];" : "=r"(v) : "r"(ad));
       } else {
         v = simg[(int64_t)y * a.s_rp + x * C + c];
@@ -347,6 +348,7 @@ __device__ __forceinline__ void pt_rows(const WarpArgs& a, const PtArgs& pa, con
           const uint32_t o = SBM + fy[k] * (uint32_t)P + fx[k] * (uint32_t)C;
           sh[k] = (int)(o << 3);  // funnel shifts use the amount mod 32
           const uint32_t al = o & ~3u;
+          FV_CHECK(al >= win && al + P + 4 * NW <= win + (uint32_t)(t.rows * P));
           lds_words(w[k][0], al);
           lds_words(w[k][1], al + P);
         } else {
@@ -451,6 +453,8 @@ __global__ void __launch_bounds__(256, PT_MINB) warp_persp_tile_kernel(const __g
   }
   const bool staged = t.cls == PT_STAGED;
   if (staged && warp == 0) {  // warp 0 streams the window's row segments
+    FV_CHECK(t.rows >= 1 && t.rows <= PT_WROWS && t.len >= 16 && t.len <= P - 16 && t.cy0 >= 0 &&
+             t.cy0 + t.rows <= a.sh && t.sb0 >= 0 && t.sb0 + t.len <= a.sw * C);
     if (lane == 0) mbar_expect_tx(bar, (uint32_t)(t.rows * t.len));
     __syncwarp();
     const uint8_t* g = simg + (int64_t)t.cy0 * a.s_rp + t.sb0;

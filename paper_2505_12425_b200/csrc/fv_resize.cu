@@ -210,6 +210,9 @@ __global__ void __launch_bounds__(StripCfg<InT, C, MODE>::NT, 3)
           last = r;
           const int slot = k % RING;
           if (k >= RING) mbar_wait_block(&empty[slot], (uint32_t)(((k / RING) - 1) & 1));
+          FV_CHECK(r >= 0 && r < a.sh && seg_byte - shift >= 0 && nbytes <= (uint32_t)a.slot_bytes &&
+                   (int64_t)r * a.s_rp + (seg_byte - shift) + nbytes <=
+                       (int64_t)(a.sh - 1) * a.s_rp + (int64_t)a.sw * C * (int64_t)sizeof(InT));
           mbar_expect_tx(&full[slot], nbytes);
           tma_bulk_g2s(slots + slot * a.slot_bytes, src_img + (int64_t)r * a.s_rp, nbytes, &full[slot]);
           ++k;
@@ -364,7 +367,11 @@ __global__ void __launch_bounds__(StripCfg<InT, C, MODE>::NT, 3)
 // ---------------------------------------------------------------------------
 // host dispatch
 // ---------------------------------------------------------------------------
+#ifdef FV_TEST_KNOBS
 static int g_resize_path = 0;  // 0 auto, 1 force gather, 2 force strip (no integer-ratio fast path)
+#else
+constexpr int g_resize_path = 0;  // product build: always the automatic selection
+#endif
 
 int resize_u8_fast(const uint8_t* src, int64_t s_is, int64_t s_rp, int sh, int sw, uint8_t* dst, int64_t d_is,
                    int64_t d_rp, int dh, int dw, int c, int n, cudaStream_t st, bool* taken);
@@ -456,7 +463,9 @@ using namespace fv;
 
 extern "C" {
 
+#ifdef FV_TEST_KNOBS
 void fv_set_resize_path(int32_t mode) { g_resize_path = mode; }
+#endif
 
 int fv_resize_bilinear_f32(const float* src, int64_t s_is, int64_t s_rp, int32_t sh, int32_t sw, float* dst,
                            int64_t d_is, int64_t d_rp, int32_t dh, int32_t dw, int32_t c, int32_t n, void* stream) {

@@ -204,6 +204,7 @@ __device__ __forceinline__ void up2_lds(const uint8_t* seg_row_base, int t, uint
   // seg_row_base points at source-row byte 0 inside the slot (may lie before
   // the slot for t = 0; those bytes feed only the clamped pixel and are unused)
   const uint32_t* rw = reinterpret_cast<const uint32_t*>(seg_row_base + 4 * C * t - 4);
+  FV_CHECK(in_dyn_smem(smem_u32(rw), 4 * Up2<C>::NW));
 #pragma unroll
   for (int i = 0; i < Up2<C>::NW; ++i) w[i] = rw[i];
 }
@@ -260,6 +261,9 @@ __global__ void __launch_bounds__((UP2_NCW + 1) * 32, 4) resize_up2_kernel(const
       for (int r = r_first, i = 0; r < k1; ++r, ++i) {
         const int slot = i % UP2_RING;
         if (i >= UP2_RING) mbar_wait_block(&empty[slot], (uint32_t)(((i / UP2_RING) - 1) & 1));
+        FV_CHECK(r >= 0 && r < a.sh && gstart >= 0 &&
+                 (int64_t)r * a.s_rp + gstart + nbytes <= (int64_t)(a.sh - 1) * a.s_rp + (int64_t)a.sw * C &&
+                 nbytes <= (uint32_t)a.slot_bytes);
         mbar_expect_tx(&full[slot], nbytes);
         tma_bulk_g2s(slots + slot * a.slot_bytes, src + (int64_t)r * a.s_rp, nbytes, &full[slot]);
       }
@@ -342,6 +346,8 @@ __global__ void __launch_bounds__((D2_NCW + 1) * 32) resize_down2_tma_kernel(con
       for (int r = 2 * y0, i = 0; r < 2 * y1; ++r, ++i) {
         const int slot = i % D2_RING;
         if (i >= D2_RING) mbar_wait_block(&empty[slot], (uint32_t)(((i / D2_RING) - 1) & 1));
+        FV_CHECK(r >= 0 && r < a.sh && (int64_t)g0 * 32 * C + nbytes <= (int64_t)a.sw * C &&
+                 nbytes <= (uint32_t)a.slot_bytes);
         mbar_expect_tx(&full[slot], nbytes);
         tma_bulk_g2s(slots + slot * a.slot_bytes, src + (int64_t)r * a.s_rp, nbytes, &full[slot]);
       }

@@ -21,9 +21,9 @@ int set_error(int code, const char* fmt, ...) {
 void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 
 int check_launch(const char* what) {
-  count_launch();
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return set_error(FV_ECUDA, "%s: %s", what, cudaGetErrorString(e));
+  count_launch();  // successful launches only
   return FV_OK;
 }
 

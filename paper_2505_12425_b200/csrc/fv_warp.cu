@@ -507,6 +507,7 @@ __device__ __forceinline__ int3 affine_tma_issue(const CUtensorMap* tmap, const 
   const int ex0 = (e0 >= 0 ? e0 : e0 - (AL - 1)) / AL * AL;  // floor to the alignment
   const bool staged = fin && ((int)floor(xhi) + 4) * C - ex0 <= TBE && (int)floor(yhi) + 3 - by0 < TBH;
   if (staged) {
+    FV_CHECK(in_dyn_smem(smem_u32(stage), (uint32_t)(TBE * TBH * ES)));
     mbar_expect_tx(bar, (uint32_t)(TBE * TBH * ES));
     asm volatile(
         "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], "
@@ -571,6 +572,8 @@ __device__ __forceinline__ void affine_tma_tile(const WarpArgs& a, const WarpTap
         const bool iy0 = q.y0 >= 0 && q.y0 < a.sh, iy1 = q.y0 + 1 >= 0 && q.y0 + 1 < a.sh;
         // in-image taps lie in the window; others read the border (never the SMEM)
         const uint32_t o = sb + (uint32_t)((q.y0 * TBE + q.x0 * C) * ES);
+        FV_CHECK(!(q.finite && iy0 && ix0 && iy1 && ix1) ||
+                 (o >= smem_u32(stage) && o + TBE * ES + PB * 2 <= smem_u32(stage) + TBE * TBH * ES + PB));
 #pragma unroll
         for (int c = 0; c < C; ++c) {
           v00[k][c] = (q.finite && iy0 && ix0) ? lds_raw<InT>(o + c * ES) : bord;
@@ -971,8 +974,13 @@ __global__ void __launch_bounds__(256, PF_MINB) warp_persp_fast_kernel(const __g
   }
 }
 
-static int g_warp_path = 0;  // 0 auto, 1 direct gathers only, 2 bulk-copy tiles (fv_set_warp_path)
+#ifdef FV_TEST_KNOBS
+static int g_warp_path = 0;  // 0 auto, 1 direct gathers only, 2 bulk-copy tiles, 3 round-1 perspective kernel
 static int g_warp_tma = 1;   // TMA-tensor tiles when available (path 0)
+#else
+constexpr int g_warp_path = 0;  // product build: always the automatic selection
+constexpr int g_warp_tma = 1;
+#endif
 
 constexpr int AT_H = 16;  // tile height of the staged affine kernel (16: 24 KB stage, 8 CTAs / SM)
 
@@ -1166,10 +1174,12 @@ using namespace fv;
 
 extern "C" {
 
+#ifdef FV_TEST_KNOBS
 void fv_set_warp_path(int32_t mode) {
   g_warp_path = mode == 2 ? 0 : mode;  // 3: the round-1 perspective kernel (A/B)
   g_warp_tma = mode == 2 ? 0 : 1;
 }
+#endif
 
 int fv_warp_affine_f32(const float* src, int64_t s_is, int64_t s_rp, int32_t sh, int32_t sw, float* dst,
                        int64_t d_is, int64_t d_rp, int32_t dh, int32_t dw, int32_t c, int32_t n,

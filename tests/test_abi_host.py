@@ -23,9 +23,14 @@ from paper_2505_12425_b200.errors import (
 HEADER = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "include", "fovea_b200.h")
 
 
-def header_symbols():
+def header_symbols(test_build=False):
+    """Entry points the header declares; those inside `#ifdef FV_TEST_KNOBS`
+    only for the test build."""
     text = open(HEADER).read()
-    return sorted(set(re.findall(r"\b(fv_[a-z0-9_]+)\s*\(", text)))
+    knob_blocks = re.findall(r"#ifdef FV_TEST_KNOBS(.*?)#endif", text, flags=re.S)
+    knobs = set(re.findall(r"\b(fv_[a-z0-9_]+)\s*\(", "".join(knob_blocks)))
+    every = set(re.findall(r"\b(fv_[a-z0-9_]+)\s*\(", text))
+    return sorted(every if test_build else every - knobs)
 
 
 class TestAbi:
@@ -43,6 +48,20 @@ class TestAbi:
 
     def test_binding_table_matches_header(self):
         assert sorted(_native.SIGNATURES) == header_symbols()
+        assert sorted({**_native.SIGNATURES, **_native.KNOB_SIGNATURES}) == header_symbols(test_build=True)
+
+    def test_path_knobs_only_in_the_test_build(self):
+        """fv_set_resize_path / fv_set_warp_path are process-global test
+        switches: absent from the product library, present in the test build."""
+        import ctypes
+
+        prod = ctypes.CDLL(_native.LIB_PATH)
+        knobs = ctypes.CDLL(_native.KNOBS_PATH)
+        for s in ("fv_set_resize_path", "fv_set_warp_path"):
+            assert not hasattr(prod, s)
+            assert hasattr(knobs, s)
+        for s in header_symbols():
+            assert hasattr(knobs, s), s
 
     def test_bad_arguments_rejected_before_launch(self):
         # EINVAL paths return before touching the device, so they run on CPU

@@ -9,7 +9,7 @@ from hypothesis import strategies as st
 
 import oracle as O
 import paper_2505_12425_b200 as fv
-from _helpers import golden
+from _helpers import forced_path, golden
 from paper_2505_12425_b200 import _native, synth
 
 pytestmark = pytest.mark.gpu
@@ -107,8 +107,7 @@ def check_canaries(parent, shape, pad=(3, 5, 7)):
 
 @pytest.mark.parametrize("path", [0, 1, 2])
 def test_no_writes_outside_destination(rng, path):
-    _native.lib().fv_set_resize_path(path)
-    try:
+    with forced_path("resize", path):
         n, c = 2, 3
         src = cu(rng.integers(0, 256, (n, 37, 53, c), dtype=np.uint8))
         srcf = cu(rng.random((n, 37, 53, c), dtype=np.float32))
@@ -137,8 +136,6 @@ def test_no_writes_outside_destination(rng, path):
         mask = np.ones(p.shape, bool)
         mask[1:1 + n, :, 3:35, 5:37] = False
         assert np.all(p[mask] == CANARY)
-    finally:
-        _native.lib().fv_set_resize_path(0)
 
 
 def test_empty_batch_is_a_no_op():

@@ -14,7 +14,8 @@ import torch
 sys.path.insert(0, os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "oracle"))
 import jpeg_oracle as O  # noqa: E402
 
-import paper_2505_12425_b200 as fv  # noqa: E402
+import paper_2505_12425_b200 as fv
+import synth_fixtures  # noqa: E402
 from paper_2505_12425_b200 import _native, synth  # noqa: E402
 from paper_2505_12425_b200 import io as fio  # noqa: E402
 
@@ -216,7 +217,7 @@ def test_gpu_entropy_smooth_and_noise_batch():
     pytest.importorskip("PIL")
     streams = []
     for i in range(6):
-        streams.append(_pil(synth.seeded_smooth_u8_image(640 + 16 * i, 360 + 8 * i, 3, seed=i), quality=90,
+        streams.append(_pil(synth_fixtures.seeded_smooth_u8_image(640 + 16 * i, 360 + 8 * i, 3, seed=i), quality=90,
                             subsampling=2))
         streams.append(_pil(synth.seeded_u8_image(320 + i, 200 + 3 * i, 3, seed=i), quality=95, subsampling=0))
     outs = fio.decode_jpeg_batch(streams, entropy="gpu")

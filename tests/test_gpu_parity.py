@@ -12,7 +12,7 @@ import torch
 
 import oracle as O
 import paper_2505_12425_b200 as fv
-from _helpers import golden
+from _helpers import forced_path, golden
 from paper_2505_12425_b200 import _native, synth
 
 pytestmark = pytest.mark.gpu
@@ -46,9 +46,8 @@ def assert_exact(got, ref):
 
 @pytest.fixture(params=[0, 1, 2], ids=["auto", "gather", "strip"])
 def resize_path(request):
-    _native.lib().fv_set_resize_path(request.param)
-    yield request.param
-    _native.lib().fv_set_resize_path(0)
+    with forced_path("resize", request.param):
+        yield request.param
 
 
 # ---------------------------------------------------------------------------
@@ -237,9 +236,8 @@ class TestFused:
 
 @pytest.fixture(params=[0, 1, 2], ids=["tma_tile", "direct", "bulk_tile"])
 def warp_path(request):
-    _native.lib().fv_set_warp_path(request.param)
-    yield request.param
-    _native.lib().fv_set_warp_path(0)
+    with forced_path("warp", request.param):
+        yield request.param
 
 
 class TestWarp:
@@ -437,15 +435,12 @@ def test_resize_random_geometry_all_paths(sw, sh, dw, dh, c, n, path, seed):
     rng = np.random.default_rng(seed)
     a = rng.integers(0, 256, (n, sh, sw, c), dtype=np.uint8)
     f = rng.random((n, sh, sw, c), dtype=np.float32)
-    _native.lib().fv_set_resize_path(path)
-    try:
+    with forced_path("resize", path):
         du = torch.zeros((n, dh, dw, c), dtype=torch.uint8, device=DEV)
         df = torch.zeros((n, dh, dw, c), dtype=torch.float32, device=DEV)
         fv.resize_bilinear_u8(cu(a), du)
         fv.resize_bilinear(cu(f), df)
         ou, of = host(du), host(df)
-    finally:
-        _native.lib().fv_set_resize_path(0)
     for i in range(n):
         assert np.array_equal(ou[i], O.resize_u8(a[i], dw, dh))
         assert np.array_equal(of[i], O.resize_bilinear(f[i], dw, dh))

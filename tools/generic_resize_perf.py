@@ -8,6 +8,7 @@ dev = "cuda:0"
 cases = [((2160, 3840), (1080, 1920), 64, 2), ((2160, 3840), (1080, 1920), 64, 0), ((1080, 1920), (720, 1280), 128, 0),
          ((720, 1280), (1080, 1920), 128, 0), ((1080, 1920), (640, 640), 256, 0), ((1080, 1920), (224, 224), 512, 0)]
 for (sh, sw), (dh, dw), n, path in cases:
+    _native.use_test_build(True)  # the path knob lives in the test build only
     _native.lib().fv_set_resize_path(path)
     src = torch.randint(0, 256, (n, sh, sw, 3), dtype=torch.uint8, device=dev)
     dst = torch.empty((n, dh, dw, 3), dtype=torch.uint8, device=dev)

@@ -16,7 +16,8 @@ import numpy as np  # noqa: E402
 import torch  # noqa: E402
 from PIL import Image  # noqa: E402
 
-import paper_2505_12425_b200 as fv  # noqa: E402
+import paper_2505_12425_b200 as fv
+import synth_fixtures  # noqa: E402
 from paper_2505_12425_b200 import io as fio, synth  # noqa: E402
 from concurrent.futures import ThreadPoolExecutor  # noqa: E402
 
@@ -32,7 +33,7 @@ def main():
     streams = []
     for i in range(a.n):
         b = pyio.BytesIO()
-        Image.fromarray(synth.seeded_smooth_u8_image(a.w, a.h, 3, seed=70000 + i)).save(b, "JPEG", quality=90, subsampling=2)
+        Image.fromarray(synth_fixtures.seeded_smooth_u8_image(a.w, a.h, 3, seed=70000 + i)).save(b, "JPEG", quality=90, subsampling=2)
         streams.append(b.getvalue())
     print(f"encode {time.time() - t:.1f}s, mean stream {np.mean([len(s) for s in streams]) / 1e3:.0f} KB, cores {a.threads}")
     dev = torch.device("cuda", 0)

@@ -27,10 +27,12 @@ def main():
     d_ex, d_fa, d_old = torch.zeros_like(src), torch.zeros_like(src), torch.zeros_like(src)
     from paper_2505_12425_b200 import _native
 
-    def old():
+    def old():  # the round-1 kernel, through the test build's path knob
+        _native.use_test_build(True)
         _native.lib().fv_set_warp_path(3)
         fv.warp_perspective(src, d_old, hs)
         _native.lib().fv_set_warp_path(0)
+        _native.use_test_build(False)
 
     runs = {"exact": lambda: fv.warp_perspective(src, d_ex, hs, exact=True),
             "fast": lambda: fv.warp_perspective(src, d_fa, hs), "fast_r01": old}
