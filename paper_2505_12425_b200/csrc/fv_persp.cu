@@ -48,8 +48,11 @@
 namespace fv {
 
 constexpr int PT_TW = 128;          // tile width, destination pixels (4 anchor groups of 32)
-constexpr int PT_TH = 32;           // tile height: 8 warps x 4 rows
-constexpr int PT_RPW = PT_TH / 8;   // rows per warp
+constexpr int PT_TH = 32;           // tile height: PT_NW warps x PT_RPW rows
+#ifndef PT_NW
+#define PT_NW 8  // warps per CTA
+#endif
+constexpr int PT_RPW = PT_TH / PT_NW;  // rows per warp (rows warp, warp + PT_NW, ...)
 constexpr int PT_WROWS = 56;        // SMEM window rows
 constexpr float PT_MAX_ERR = 5e-4f;
 #ifndef PT_MINB
@@ -64,9 +67,9 @@ template <int C>
 constexpr int pt_obuf() { return PT_TW * C; }  // one output row segment
 constexpr int PT_ANC_OFF = 64;                                   // 8 warps x 8 slots x 48 B (tile info at 16)
 template <int C>
-constexpr int pt_obuf_off() { return PT_ANC_OFF + 8 * 8 * 48; }  // 8 warps x 2 rows
+constexpr int pt_obuf_off() { return PT_ANC_OFF + PT_TH * 2 * 48; }  // anchor slots: 2 per tile row
 template <int C>
-constexpr int pt_win_off() { return pt_obuf_off<C>() + 8 * 2 * pt_obuf<C>(); }
+constexpr int pt_win_off() { return pt_obuf_off<C>() + PT_NW * 2 * pt_obuf<C>(); }  // 2 row buffers per warp
 template <int C>
 constexpr int pt_smem() { return pt_win_off<C>() + PT_WROWS * pt_pitch<C>(); }
 
@@ -268,7 +271,7 @@ __device__ __forceinline__ void pt_rows(const WarpArgs& a, const PtArgs& pa, con
   // lanes past the destination's right edge: a safe in-window / in-image tap
   const uint32_t safe_fx = (uint32_t)((STAGED ? t.cx0 : 0) - t.ox) + MB;
   const uint32_t safe_fy = (uint32_t)((STAGED ? t.cy0 : 0) - t.oy) + MB;
-  const uint32_t anc = smem0 + PT_ANC_OFF + warp * 8 * 48;
+  const uint32_t anc = smem0 + PT_ANC_OFF + warp * PT_RPW * 2 * 48;
   const uint32_t obw = smem0 + pt_obuf_off<C>() + warp * 2 * OB;  // this warp's two row buffers
   const float lf = (float)lane;
   const f2_t LL = f2(lf, lf);
@@ -280,7 +283,7 @@ __device__ __forceinline__ void pt_rows(const WarpArgs& a, const PtArgs& pa, con
   const int xbytes = min(PT_TW, a.dw - tx0) * C;
 #pragma unroll 1
   for (int r = 0; r < PT_RPW; ++r) {
-    const int y = ty0 + warp + 8 * r;
+    const int y = ty0 + warp + PT_NW * r;
     if (y >= a.dh) break;  // warp-uniform
     const uint32_t ob = obw + (r & 1) * OB + lane * C;
 #pragma unroll
@@ -406,7 +409,7 @@ __device__ __forceinline__ void pt_rows(const WarpArgs& a, const PtArgs& pa, con
 }
 
 template <int C>
-__global__ void __launch_bounds__(256, PT_MINB) warp_persp_tile_kernel(const __grid_constant__ WarpArgs a,
+__global__ void __launch_bounds__(PT_NW * 32, PT_MINB) warp_persp_tile_kernel(const __grid_constant__ WarpArgs a,
                                                                       const __grid_constant__ PtArgs pa,
                                                                       const __grid_constant__ WarpMats mats) {
   extern __shared__ __align__(128) uint8_t smem[];
@@ -440,7 +443,7 @@ __global__ void __launch_bounds__(256, PT_MINB) warp_persp_tile_kernel(const __g
     const int xbytes = min(PT_TW, a.dw - tx0) * C;
 #pragma unroll 1
     for (int r = 0; r < PT_RPW; ++r) {
-      const int y = ty0 + warp + 8 * r;
+      const int y = ty0 + warp + PT_NW * r;
       if (y >= a.dh) break;
       uint8_t* d = dimg + (int64_t)y * a.d_rp + tx0 * C;
       if (pa.dst_vec && xbytes == OB) {
@@ -465,9 +468,9 @@ __global__ void __launch_bounds__(256, PT_MINB) warp_persp_tile_kernel(const __g
   // slot (row, pair) as f32x2-ready pairs (group 2p, group 2p + 1) per field:
   // {srx, sry, kx, ky, W_a, flags}; slot stride 12 words: the 16 writers of a
   // field hit 16 distinct banks.
-  if (lane < 16) {
+  if (lane < 4 * PT_RPW) {
     const int r = lane >> 2, g = lane & 3;
-    const double yd = (double)(ty0 + warp + 8 * r), xd = (double)(tx0 + 32 * g);
+    const double yd = (double)(ty0 + warp + PT_NW * r), xd = (double)(tx0 + 32 * g);
     const double rx = m[1] * yd + m[2], ry = m[4] * yd + m[5];
     const double Wa = m[6] * xd + (m[7] * yd + m[8]);
     const double We = Wa + m[6] * 31.0;
@@ -500,13 +503,19 @@ __global__ void __launch_bounds__(256, PT_MINB) warp_persp_tile_kernel(const __g
           flags |= PG_INTERIOR;
       }
     }
-    const uint32_t sl = smem_u32(smem) + PT_ANC_OFF + ((warp * 8 + r * 2 + (g >> 1)) * 12 + (g & 1)) * 4;
-    asm volatile("st.shared.f32 [%0], %1;" ::"r"(sl), "f"(srx));
-    asm volatile("st.shared.f32 [%0], %1;" ::"r"(sl + 8), "f"(sry));
-    asm volatile("st.shared.f32 [%0], %1;" ::"r"(sl + 16), "f"(kx));
-    asm volatile("st.shared.f32 [%0], %1;" ::"r"(sl + 24), "f"(ky));
-    asm volatile("st.shared.f32 [%0], %1;" ::"r"(sl + 32), "f"(waf));
-    asm volatile("st.shared.u32 [%0], %1;" ::"r"(sl + 40), "r"(flags));
+    const uint32_t sl = smem_u32(smem) + PT_ANC_OFF + ((warp * PT_RPW * 2 + r * 2 + (g >> 1)) * 12 + (g & 1)) * 4;
+    // 16 writers per store instruction (rows 0-3, then 4-7): distinct banks
+#pragma unroll
+    for (int hb = 0; hb < (PT_RPW + 3) / 4; ++hb) {
+      if ((lane >> 4) == hb) {
+        asm volatile("st.shared.f32 [%0], %1;" ::"r"(sl), "f"(srx));
+        asm volatile("st.shared.f32 [%0], %1;" ::"r"(sl + 8), "f"(sry));
+        asm volatile("st.shared.f32 [%0], %1;" ::"r"(sl + 16), "f"(kx));
+        asm volatile("st.shared.f32 [%0], %1;" ::"r"(sl + 24), "f"(ky));
+        asm volatile("st.shared.f32 [%0], %1;" ::"r"(sl + 32), "f"(waf));
+        asm volatile("st.shared.u32 [%0], %1;" ::"r"(sl + 40), "r"(flags));
+      }
+    }
   }
   __syncwarp();
   const uint32_t smem0 = smem_u32(smem);
@@ -526,7 +535,7 @@ static int launch_persp_tile_c(const WarpArgs& a, const PtArgs& pa, const WarpMa
   static unsigned long long attr_mask[2] = {0, 0};
   if (ensure_smem_attr(kern, smem, attr_mask) != FV_OK) return set_error(FV_ECUDA, "warp_persp_tile_kernel: smem attribute");
   dim3 grid((a.dw + PT_TW - 1) / PT_TW, (a.dh + PT_TH - 1) / PT_TH, nb);
-  kern<<<grid, 256, smem, st>>>(a, pa, mats);
+  kern<<<grid, PT_NW * 32, smem, st>>>(a, pa, mats);
   return FV_OK;
 }
 

@@ -156,6 +156,18 @@ __device__ __forceinline__ void up2_h(const uint32_t (&w)[Up2<C>::NW], int t, in
   for (int i = 0; i < 4 * C; ++i) h[i] = f2(hs[2 * i], hs[2 * i + 1]);
 }
 
+#ifndef FV_UP2_CS
+#define FV_UP2_CS 0  // 1: evict-first stores (st.global.cs); ptxas builds a cache-policy descriptor and
+                     // moves it into uniform registers (2 R2UR) before every such store
+#endif
+__device__ __forceinline__ void up2_store(uint2* p, uint2 v) {
+#if FV_UP2_CS
+  __stcs(p, v);
+#else
+  *p = v;
+#endif
+}
+
 // one destination row from two h rows: o = fma(hb, 0.25, qa), epilogue in
 // f32x2, packed 4 bytes at a time and written as 8-byte stores (8*C bytes)
 template <int C>
@@ -170,7 +182,7 @@ __device__ __forceinline__ void up2_emit(uint8_t* drow, const f2_t (&hb)[4 * C],
       const f2_t r1 = scale_to_u8_bits2(ffma2(hb[e + 1], f2(0.25f, 0.25f), qa[e + 1]), 255.0f);
       w[j] = pack4x2(r0, r1);
     }
-    __stcs(reinterpret_cast<uint2*>(drow) + i, make_uint2(w[0], w[1]));
+    up2_store(reinterpret_cast<uint2*>(drow) + i, make_uint2(w[0], w[1]));
   }
 }
 // a row that is a plain copy of h (clamped rows 0 and 2H-1, fy = 0)
@@ -184,7 +196,7 @@ __device__ __forceinline__ void up2_emit_copy(uint8_t* drow, const f2_t (&h)[4 *
       const int e = 4 * i + 2 * j;
       w[j] = pack4x2(scale_to_u8_bits2(h[e], 255.0f), scale_to_u8_bits2(h[e + 1], 255.0f));
     }
-    __stcs(reinterpret_cast<uint2*>(drow) + i, make_uint2(w[0], w[1]));
+    up2_store(reinterpret_cast<uint2*>(drow) + i, make_uint2(w[0], w[1]));
   }
 }
 
