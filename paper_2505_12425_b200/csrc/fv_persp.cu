@@ -53,7 +53,10 @@ constexpr int PT_TH = 32;           // tile height: PT_NW warps x PT_RPW rows
 #define PT_NW 8  // warps per CTA
 #endif
 constexpr int PT_RPW = PT_TH / PT_NW;  // rows per warp (rows warp, warp + PT_NW, ...)
-constexpr int PT_WROWS = 56;        // SMEM window rows
+#ifndef FV_PT_WROWS
+#define FV_PT_WROWS 56
+#endif
+constexpr int PT_WROWS = FV_PT_WROWS;  // SMEM window rows
 constexpr float PT_MAX_ERR = 5e-4f;
 #ifndef PT_MINB
 #define PT_MINB 4

@@ -1,7 +1,7 @@
 """Run one BASELINE config's kernel(s) a few times at full size -- the short
 command that `ncu` wraps (see profiles/README.md). Not a benchmark: no timing.
 
-    python tools/profile_ops.py --op resize|down|up|gray|affine|persp|fused|jpeg [--reps 2] [--images N]
+    python tools/profile_ops.py --op resize|down|up|gray|graybatch|affine|persp|fused|jpeg [--reps 2] [--images N]
 """
 import argparse
 import os
@@ -38,6 +38,11 @@ def main():
         src = synth.device_u8_batch(n, 1080, 1920, 3, synth.SEED_GRAY, dev)
         dst = torch.zeros((n, 1080, 1920, 1), dtype=torch.uint8, device=dev)
         runs.append(lambda: [fv.gray_from_rgb(src[i], dst[i]) for i in range(n)])
+    elif a.op == "graybatch":  # the same 32 frames in one launch
+        n = a.images or 32
+        src = synth.device_u8_batch(n, 1080, 1920, 3, synth.SEED_GRAY, dev)
+        dst = torch.zeros((n, 1080, 1920, 1), dtype=torch.uint8, device=dev)
+        runs.append(lambda: fv.gray_from_rgb(src, dst))
     elif a.op == "affine":
         n = a.images or 32
         src = synth.device_f32_batch(n, 1080, 1920, 3, synth.SEED_AFFINE, dev)
