@@ -53,6 +53,9 @@ constexpr int PT_TH = 32;           // tile height: PT_NW warps x PT_RPW rows
 #define PT_NW 8  // warps per CTA
 #endif
 constexpr int PT_RPW = PT_TH / PT_NW;  // rows per warp (rows warp, warp + PT_NW, ...)
+#ifndef FV_PT_PITCH3
+#define FV_PT_PITCH3 656  // C = 3 window pitch (bytes)
+#endif
 #ifndef FV_PT_WROWS
 #define FV_PT_WROWS 56
 #endif
@@ -65,7 +68,7 @@ constexpr float PT_MAX_ERR = 5e-4f;
 // 16-byte aligned; rows rotate banks), wide enough for a 1.6x zoom-in of a
 // 128-pixel row plus the tap window's 12-byte overhang
 template <int C>
-constexpr int pt_pitch() { return C == 1 ? 240 : (C == 3 ? 656 : 848); }
+constexpr int pt_pitch() { return C == 1 ? 240 : (C == 3 ? FV_PT_PITCH3 : 848); }
 template <int C>
 constexpr int pt_obuf() { return PT_TW * C; }  // one output row segment
 constexpr int PT_ANC_OFF = 64;                                   // 8 warps x 8 slots x 48 B (tile info at 16)
