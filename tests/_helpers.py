@@ -34,3 +34,19 @@ class forced_path:
             getattr(_native.lib(), f"fv_set_{self.kind}_path")(0)
             _native.use_test_build(False)
         return False
+
+
+def _call(job):
+    fn, args = job
+    return fn(*args)
+
+
+def oracle_map(fn, arglist, procs=None):
+    """fn(*args) for every args tuple on forked host processes (the oracle is
+    single-threaded NumPy); fn must be a module-level function. The children
+    never touch CUDA."""
+    import multiprocessing as mp
+
+    procs = procs or min(len(arglist), max(1, (os.cpu_count() or 2) - 1))
+    with mp.get_context("fork").Pool(procs) as pool:
+        return pool.map(_call, [(fn, a) for a in arglist], chunksize=1)

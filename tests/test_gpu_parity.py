@@ -12,7 +12,7 @@ import torch
 
 import oracle as O
 import paper_2505_12425_b200 as fv
-from _helpers import forced_path, golden
+from _helpers import forced_path, golden, oracle_map
 from paper_2505_12425_b200 import _native, synth
 
 pytestmark = pytest.mark.gpu
@@ -206,6 +206,22 @@ class TestResize:
 # a10 fused
 # ---------------------------------------------------------------------------
 
+def _fused_ref(i):
+    a = synth.seeded_u8_image(1920, 1080, 3, seed=synth.SEED_FUSED + i)
+    return O.resize_normalize_chw(a, 640, 640, synth.MEAN, synth.STD)
+
+
+def _affine_ref(i):
+    a = synth.seeded_f32_image(1920, 1080, 3, seed=synth.SEED_AFFINE + i)
+    m = synth.affine_forward(synth.SEED_AFFINE_PARAMS + i, 1920, 1080)
+    return O.warp_affine(a, O.invert_affine(m), 1080, 1920, border=0.0)
+
+
+def _persp_exact_ref(i):
+    a = synth.seeded_u8_image(3840, 2160, 3, seed=synth.SEED_PERSP + i)
+    return O.warp_perspective(a, O.invert_homography(synth.perspective_forward(synth.SEED_PERSP_PARAMS + i)),
+                              2160, 3840, border=0)
+
 class TestFused:
     def test_cfg4_full_images(self, resize_path):
         imgs = np.stack([synth.seeded_u8_image(1920, 1080, 3, seed=synth.SEED_FUSED + i) for i in range(3)])
@@ -214,6 +230,17 @@ class TestFused:
         out = host(dst)
         for i in range(3):
             assert_exact(out[i], O.resize_normalize_chw(imgs[i], 640, 640, synth.MEAN, synth.STD))
+
+    def test_cfg4_64_images_across_the_batch(self):
+        """64 of cfg4's 512 images (every 8th seed) at full size through the
+        default path in one launch, against the oracle (bit-exact)."""
+        idx = list(range(0, 512, 8))
+        imgs = np.stack([synth.seeded_u8_image(1920, 1080, 3, seed=synth.SEED_FUSED + i) for i in idx])
+        dst = torch.zeros((len(idx), 3, 640, 640), dtype=torch.float32, device=DEV)
+        fv.resize_normalize_chw(cu(imgs), dst, synth.MEAN, synth.STD)
+        out = host(dst)
+        for k, ref in enumerate(oracle_map(_fused_ref, [(i,) for i in idx])):
+            assert_exact(out[k], ref)
 
     def test_golden_geometry_and_odd_shapes(self, resize_path, rng):
         g = golden("resize_u8.npz")
@@ -250,6 +277,29 @@ class TestWarp:
         out = host(dst)
         for i in range(n):
             assert_exact(out[i], O.warp_affine(imgs[i], O.invert_affine(ms[i]), 1080, 1920, border=0.0))
+
+    def test_cfg2_affine_all_32_images(self):
+        """All 32 cfg2 images (their seeded rotations / scales / shifts) at
+        full size through the default path in one launch (bit-exact)."""
+        n = 32
+        imgs = np.stack([synth.seeded_f32_image(1920, 1080, 3, seed=synth.SEED_AFFINE + i) for i in range(n)])
+        ms = np.stack([synth.affine_forward(synth.SEED_AFFINE_PARAMS + i, 1920, 1080) for i in range(n)])
+        dst = torch.zeros_like(cu(imgs))
+        fv.warp_affine(cu(imgs), dst, ms, border=0.0)
+        out = host(dst)
+        for i, ref in enumerate(oracle_map(_affine_ref, [(i,) for i in range(n)])):
+            assert_exact(out[i], ref)
+
+    def test_cfg3_perspective_exact_all_16_images(self):
+        """exact=True on all 16 cfg3 images, full frames (bit-exact)."""
+        n = 16
+        imgs = np.stack([synth.seeded_u8_image(3840, 2160, 3, seed=synth.SEED_PERSP + i) for i in range(n)])
+        hs = np.stack([synth.perspective_forward(synth.SEED_PERSP_PARAMS + i) for i in range(n)])
+        dst = torch.zeros_like(cu(imgs))
+        fv.warp_perspective(cu(imgs), dst, hs, border=0, exact=True)
+        out = host(dst)
+        for i, ref in enumerate(oracle_map(_persp_exact_ref, [(i,) for i in range(n)])):
+            assert_exact(out[i], ref)
 
     def test_cfg3_perspective_row_bands(self):
         n = 2
