@@ -21,10 +21,14 @@ All arithmetic is Python/NumPy int64, like the reference. Parity pinned by
 tests/golden/jpeg.npz: streams from the reference encoder and from Pillow,
 decoded by the reference itself (tests/golden/make_golden_jpeg.py).
 
-Divergence, deliberate: a DHT whose code counts overflow the code space makes
-the reference raise IndexError while building its 8-bit lookup table; here
-(and in the C ABI) it is CorruptStream. The reference's fuzz tests only
-require "no crash other than FoveaError".
+Divergence, deliberate: a DHT whose code counts overflow the code space is
+CorruptStream here and in the C ABI. The reference (io/jpeg.py:274-296)
+raises IndexError (not a FoveaError) when the overflow happens at a code
+length <= 8, while filling its 8-bit lookup table; when it happens only at
+lengths 9-16 it builds the table and decodes any stream that never uses the
+unreachable codes. The C decoders' fast tables assume a valid code space, so
+such tables are rejected up front (the reference's fuzz tests only require
+"no crash other than FoveaError"; no encoder emits them).
 """
 from __future__ import annotations
 
