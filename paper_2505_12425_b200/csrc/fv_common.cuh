@@ -151,11 +151,26 @@ __device__ __forceinline__ f2_t fadd2_rd(f2_t a, f2_t b) {
   return r;
 }
 // two u8_to_unit at once from two magic words 0x4B0000uu
+#ifndef FV_UNIT2_FMA
+#define FV_UNIT2_FMA 1  // two-FFMA2 form below (0: the subtract + split-constant three-op form)
+#endif
 __device__ __forceinline__ f2_t unit2(uint32_t m_lo, uint32_t m_hi) {
+#if FV_UNIT2_FMA
+  // y = u*257/2^16 is exact (17 significant bits), taken straight from the
+  // magic word M = 2^23 + u: fma(M, 257/2^16, -2^23*257/2^16) = RN(y) = y.
+  // Then RN(u/255) = RN(y * (1 + 2^-16 + 2^-32)): the dropped tail of
+  // 65536/65535 is < 2^-47 relative and moves no u in [0, 255] across a
+  // rounding boundary (checked exhaustively against exact rationals).
+  const float K257 = __uint_as_float(0x3B808000u);  // 257 / 2^16
+  const float CT = __uint_as_float(0x37800080u);    // 2^-16 + 2^-32
+  const f2_t y = ffma2(f2u(m_lo, m_hi), f2(K257, K257), f2(-32896.0f, -32896.0f));
+  return ffma2(y, f2(CT, CT), y);
+#else
   const float RHI = __uint_as_float(0x3B808081u);
   const float RLO = __uint_as_float(0xAF7EFEFFu);
   const f2_t f = fadd2(f2u(m_lo, m_hi), f2(-8388608.0f, -8388608.0f));
   return ffma2(f, f2(RHI, RHI), fmul2(f, f2(RLO, RLO)));
+#endif
 }
 // magic word 0x4B0000uu of byte i of a word array: PRMT puts the byte under
 // the exponent of 2^23 (i compile-time after unrolling)

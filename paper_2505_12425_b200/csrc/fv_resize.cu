@@ -31,6 +31,12 @@
 namespace fv {
 
 enum { MODE_U8 = 0, MODE_F32 = 1, MODE_CHW = 2 };
+#ifndef FV_STRIP_U8_IMM
+#define FV_STRIP_U8_IMM 1  // u8 taps at immediate channel offsets from per-pixel shared addresses (A/B knob)
+#endif
+#ifndef FV_STRIP_ADAPT
+#define FV_STRIP_ADAPT 1  // per-launch consumer-warp count (tile width) in the u8 / CHW strip modes (A/B knob)
+#endif
 constexpr int MAX_LUT = 4 * 256;
 constexpr int kMaxStripSmem = 96 * 1024;
 
@@ -45,6 +51,7 @@ struct ResizeArgs {
   double scale_x, scale_y;  // src_n / dst_n, computed once in f64 (imgproc.py:77)
   // strip kernel only
   int tile_px, band_rows, tiles_x, slot_bytes;
+  int ncw;  // consumer warps per CTA (tile_px = ncw * 32 * G in the pixel-tile modes)
   int vec_store;
   f2_t one2;  // runtime {1.0f, 1.0f} (f32x2 contraction guard, fv_common.cuh)
 };
@@ -92,7 +99,7 @@ __global__ void __launch_bounds__(128) resize_gather_kernel(const __grid_constan
 // staged strip kernel
 // ---------------------------------------------------------------------------
 
-template <typename InT, int C, int MODE>
+template <typename InT, int C, int MODE, bool AD = false>
 struct StripCfg {
   // Lane ownership. MODE_U8: 4 consecutive pixels per lane (all channels:
   // per-pixel taps, one 4C-byte run per row -> C 32-bit stores). MODE_CHW: 4
@@ -105,6 +112,13 @@ struct StripCfg {
   static constexpr int TW_PX = MODE == MODE_F32 ? NCW * 32 * G / C : NCW * 32 * G;
   static constexpr int RING = 8;
   static constexpr int NT = (NCW + 1) * 32;  // + one producer warp
+  // AD: the pixel-tile modes' variant with a per-launch consumer-warp count
+  // (NCW_MIN..NCW_MAX, tile = ncw * 32 * G pixels), launched when it covers
+  // the destination width with clearly fewer idle lanes than NCW; NT_MAX
+  // bounds its block. The default variant keeps NCW a compile-time constant.
+  static constexpr bool ADAPT = AD && MODE != MODE_F32;
+  static constexpr int NCW_MIN = ADAPT ? 2 : NCW, NCW_MAX = ADAPT ? 6 : NCW;
+  static constexpr int NT_MAX = (NCW_MAX + 1) * 32;
 };
 
 // Weights whose products are exact for every operand of this mode: any
@@ -114,6 +128,43 @@ template <int MODE>
 __device__ __forceinline__ bool exact_weight(float w) {
   return MODE == MODE_F32 ? (w == 0.0f || w == 1.0f) : pow2_or_zero(w);
 }
+
+// u8 pixel-tap modes: byte `CH` of tap pixel `addr` (a shared-space address)
+template <int CH>
+__device__ __forceinline__ uint32_t lds_u8_at(uint32_t addr) {
+  uint32_t v;
+  asm volatile("ld.shared.u8 %0, [%1+%2];" : "=r"(v) : "r"(addr), "n"(CH));
+  return v;
+}
+
+// The u8 per-pixel-tap horizontal pass with the taps' shared addresses
+// formed once per pixel (pa / pb = slot + tap offset) and each channel read
+// at an immediate offset: element pair P of the thread's EPT elements.
+template <int C, int MODE, int HM, int NA, int NP, int P>
+struct HPassU8 {
+  static __device__ __forceinline__ void run(const uint32_t (&pa)[NA], const uint32_t (&pb)[NA],
+                                             const float (&wa)[NA], const float (&wb)[NA], f2_t one, f2_t (&h)[NP]) {
+    constexpr int e0 = 2 * P, e1 = 2 * P + 1;
+    constexpr int j0 = e0 / C, c0 = e0 % C, j1 = e1 / C, c1 = e1 % C;
+    const f2_t va = unit2(0x4B000000u | lds_u8_at<c0>(pa[j0]), 0x4B000000u | lds_u8_at<c1>(pa[j1]));
+    if constexpr (HM == 2) {
+      h[P] = va;
+    } else {
+      const f2_t vb = unit2(0x4B000000u | lds_u8_at<c0>(pb[j0]), 0x4B000000u | lds_u8_at<c1>(pb[j1]));
+      if constexpr (HM == 1) {
+        h[P] = ffma2(vb, f2(wb[j0], wb[j1]), fmul2(va, f2(wa[j0], wa[j1])));
+      } else {
+        h[P] = ffma2(fmul2(vb, f2(wb[j0], wb[j1])), one, fmul2(va, f2(wa[j0], wa[j1])));
+      }
+    }
+    HPassU8<C, MODE, HM, NA, NP, P + 1>::run(pa, pb, wa, wb, one, h);
+  }
+};
+template <int C, int MODE, int HM, int NA, int NP>
+struct HPassU8<C, MODE, HM, NA, NP, NP> {
+  static __device__ __forceinline__ void run(const uint32_t (&)[NA], const uint32_t (&)[NA], const float (&)[NA],
+                                             const float (&)[NA], f2_t, f2_t (&)[NP]) {}
+};
 
 // Horizontal pass of one staged source row into the h pairs. HM: 2 = copy
 // (fx == 0), 1 = one exact product (fma form), 0 = the 3-op form -- chosen
@@ -149,11 +200,11 @@ __device__ __forceinline__ void strip_hpass(const InT* seg, const int (&oa)[NA],
   }
 }
 
-template <typename InT, int C, int MODE>
-__global__ void __launch_bounds__(StripCfg<InT, C, MODE>::NT, 3)
+template <typename InT, int C, int MODE, bool AD>
+__global__ void __launch_bounds__(StripCfg<InT, C, MODE, AD>::NT_MAX, 3)
     resize_strip_kernel(const __grid_constant__ ResizeArgs a, const __grid_constant__ LutArg lut_arg) {
-  using Cfg = StripCfg<InT, C, MODE>;
-  constexpr int NCW = Cfg::NCW, V = Cfg::V, G = Cfg::G, EPT = Cfg::EPT, RING = Cfg::RING;
+  using Cfg = StripCfg<InT, C, MODE, AD>;
+  constexpr int V = Cfg::V, G = Cfg::G, EPT = Cfg::EPT, RING = Cfg::RING;
   extern __shared__ __align__(128) uint8_t smem[];
   uint64_t* full = reinterpret_cast<uint64_t*>(smem);
   uint64_t* empty = full + RING;
@@ -164,8 +215,10 @@ __global__ void __launch_bounds__(StripCfg<InT, C, MODE>::NT, 3)
   const int tid = threadIdx.x;
   const int warp = tid >> 5, lane = tid & 31;
   const int n = blockIdx.z;
-  const int p0 = blockIdx.x * Cfg::TW_PX;
-  const int p1 = min(p0 + Cfg::TW_PX, a.dw);
+  const int NCW = Cfg::ADAPT ? a.ncw : Cfg::NCW;
+  const int tile_px = Cfg::ADAPT ? a.tile_px : Cfg::TW_PX;
+  const int p0 = blockIdx.x * tile_px;
+  const int p1 = min(p0 + tile_px, a.dw);
   const int yb = blockIdx.y * a.band_rows;
   const int nrows = min(a.band_rows, a.dh - yb);
 
@@ -273,7 +326,22 @@ __global__ void __launch_bounds__(StripCfg<InT, C, MODE>::NT, 3)
     const int slot = k % RING;
     mbar_wait(&full[slot], (uint32_t)((k / RING) & 1));
     const InT* seg = reinterpret_cast<const InT*>(slots + slot * slot_bytes);
-    if (hmode == 2) {
+    if constexpr (sizeof(InT) == 1 && MODE != MODE_F32 && FV_STRIP_U8_IMM) {
+      const uint32_t sb = smem_u32(seg);
+      uint32_t pa[NA], pb[NA];
+#pragma unroll
+      for (int j = 0; j < NA; ++j) {
+        pa[j] = sb + (uint32_t)oa[j];
+        pb[j] = sb + (uint32_t)ob[j];
+      }
+      if (hmode == 2) {
+        HPassU8<C, MODE, 2, NA, NP, 0>::run(pa, pb, wa, wb, one, h);
+      } else if (hmode == 1) {
+        HPassU8<C, MODE, 1, NA, NP, 0>::run(pa, pb, wa, wb, one, h);
+      } else {
+        HPassU8<C, MODE, 0, NA, NP, 0>::run(pa, pb, wa, wb, one, h);
+      }
+    } else if (hmode == 2) {
       strip_hpass<InT, C, MODE, 2, NA, NP>(seg, oa, ob, wa, wb, one, h);
     } else if (hmode == 1) {
       strip_hpass<InT, C, MODE, 1, NA, NP>(seg, oa, ob, wa, wb, one, h);
@@ -380,8 +448,24 @@ static inline bool al16(const void* p) { return (reinterpret_cast<uintptr_t>(p) 
 
 template <typename InT, int C, int MODE>
 static int launch_strip(ResizeArgs a, int n, const LutArg& lut, cudaStream_t st, bool* launched) {
-  using Cfg = StripCfg<InT, C, MODE>;
-  a.tile_px = Cfg::TW_PX;
+  using Cfg = StripCfg<InT, C, MODE, true>;
+  // consumer warps: the tuned default NCW unless another count covers dw
+  // with >= 10% fewer warp-tiles (idle lanes in the last tile); ties -> wider
+  a.ncw = Cfg::NCW;
+  if (Cfg::ADAPT && FV_STRIP_ADAPT) {
+    auto cost = [&](int w) { return (int64_t)((a.dw + w * 32 * Cfg::G - 1) / (w * 32 * Cfg::G)) * w; };
+    int64_t best = cost(Cfg::NCW);
+    const int64_t limit = best * 9 / 10;
+    for (int w = Cfg::NCW_MAX; w >= Cfg::NCW_MIN; --w) {
+      const int64_t c = cost(w);
+      if (c <= limit && (a.ncw == Cfg::NCW || c < best)) {
+        best = c;
+        a.ncw = w;
+      }
+    }
+  }
+  const bool adapt = a.ncw != Cfg::NCW;
+  a.tile_px = adapt ? a.ncw * 32 * Cfg::G : Cfg::TW_PX;
   a.tiles_x = (a.dw + a.tile_px - 1) / a.tile_px;
   // source footprint of one tile, upper bound: tile_px * scale_x + 3 px
   const double fp = (double)a.tile_px * a.scale_x;
@@ -395,11 +479,15 @@ static int launch_strip(ResizeArgs a, int n, const LutArg& lut, cudaStream_t st,
   if (smem > kMaxStripSmem) return FV_OK;  // not eligible: caller falls back to gather
   a.slot_bytes = (int)slot;
   const int bands = (a.dh + a.band_rows - 1) / a.band_rows;
-  auto kern = resize_strip_kernel<InT, C, MODE>;
-  static unsigned long long attr_mask[2] = {0, 0};  // per instantiation
-  if (ensure_smem_attr(kern, kMaxStripSmem, attr_mask) != FV_OK) return check_launch("resize_strip_kernel (smem attribute)");
+  auto kern = resize_strip_kernel<InT, C, MODE, false>;
+  if constexpr (Cfg::ADAPT) {
+    if (adapt) kern = resize_strip_kernel<InT, C, MODE, true>;
+  }
+  static unsigned long long attr_mask[2][2] = {{0, 0}, {0, 0}};  // per instantiation
+  if (ensure_smem_attr(kern, kMaxStripSmem, attr_mask[adapt]) != FV_OK)
+    return check_launch("resize_strip_kernel (smem attribute)");
   dim3 grid(a.tiles_x, bands, n);
-  kern<<<grid, Cfg::NT, (size_t)smem, st>>>(a, lut);
+  kern<<<grid, (a.ncw + 1) * 32, (size_t)smem, st>>>(a, lut);
   *launched = true;
   return check_launch("resize_strip_kernel");
 }

@@ -184,6 +184,23 @@ class TestResize:
         for i in range(2):
             assert_exact(out[i], O.resize_u8(a[i], dw, dh))
 
+    @pytest.mark.parametrize("dw", [224, 300, 512, 640, 1000, 1280, 1920, 2048])
+    @pytest.mark.parametrize("ratio", [4.8, 1.5, 2 / 3])
+    def test_strip_tile_widths(self, rng, dw, ratio):
+        """The strip kernel's consumer-warp count follows the destination
+        width (the tuned default, or a narrower / wider tile when that idles
+        >= 10% fewer lanes): both variants, u8 HWC and the fused CHW mode."""
+        sw, sh, dh = max(1, round(dw * ratio)), 11, 7
+        a = rng.integers(0, 256, (sh, sw, 3), dtype=np.uint8)
+        with forced_path("resize", 2):
+            dst = torch.zeros((dh, dw, 3), dtype=torch.uint8, device=DEV)
+            fv.resize_bilinear_u8(cu(a), dst)
+            dc = torch.zeros((3, dh, dw), dtype=torch.float32, device=DEV)
+            fv.resize_normalize_chw(cu(a), dc, synth.MEAN, synth.STD)
+            out, outc = host(dst), host(dc)
+        assert_exact(out, O.resize_u8(a, dw, dh))
+        assert_exact(outc, O.resize_normalize_chw(a, dw, dh, synth.MEAN, synth.STD))
+
     def test_cfg1_downscale_full_image(self):
         a = synth.seeded_u8_image(3840, 2160, 3, seed=synth.SEED_RESIZE)
         dst = torch.zeros((1080, 1920, 3), dtype=torch.uint8, device=DEV)

@@ -38,6 +38,12 @@ def main():
         src = synth.device_u8_batch(n, 1080, 1920, 3, synth.SEED_GRAY, dev)
         dst = torch.zeros((n, 1080, 1920, 1), dtype=torch.uint8, device=dev)
         runs.append(lambda: [fv.gray_from_rgb(src[i], dst[i]) for i in range(n)])
+    elif a.op in ("r720", "r1080"):  # generic ratios: 1080p -> 720p, 720p -> 1080p (strip kernel)
+        n = a.images or 128
+        (sh, sw), (dh, dw) = ((1080, 1920), (720, 1280)) if a.op == "r720" else ((720, 1280), (1080, 1920))
+        src = synth.device_u8_batch(n, sh, sw, 3, 1, dev)
+        dst = torch.zeros((n, dh, dw, 3), dtype=torch.uint8, device=dev)
+        runs.append(lambda: fv.resize_bilinear_u8(src, dst))
     elif a.op == "graybatch":  # the same 32 frames in one launch
         n = a.images or 32
         src = synth.device_u8_batch(n, 1080, 1920, 3, synth.SEED_GRAY, dev)
