@@ -207,6 +207,9 @@ __device__ __forceinline__ void up2_emit_copy(uint8_t* drow, const f2_t (&h)[4 *
 // their 4-byte aligned windows with LDS (lane stride 12 B: conflict-free) and
 // release the slot on its "empty" mbarrier.
 constexpr int UP2_NCW = 3, UP2_GROUPS = UP2_NCW * 32, UP2_RING = 8;
+#ifndef FV_UP2_CLAMP
+#define FV_UP2_CLAMP 1  // 0: lanes past the tile's last group skip the row work (divergent stores)
+#endif
 #ifndef UP2_BAND
 #define UP2_BAND 32  // source rows per CTA (one halo row re-read per band); 16 / 64 / 128 measured slower
 #endif
@@ -283,8 +286,15 @@ __global__ void __launch_bounds__((UP2_NCW + 1) * 32, 4) resize_up2_kernel(const
     return;
   }
 
+#if FV_UP2_CLAMP
+  // lanes past the tile's last group redo that group (same window, same
+  // bytes to the same addresses): no divergent store region
+  const int t = min(g0 + warp * 32 + lane, g1 - 1);
+  constexpr bool active = true;
+#else
   const int t = g0 + warp * 32 + lane;  // this thread's column group
   const bool active = t < g1;
+#endif
   uint8_t* dimg = a.dst + n * a.d_is + (int64_t)t * 8 * C;
   f2_t h0[NP], h1[NP], q[NP];
   uint32_t w[NW];
