@@ -184,6 +184,24 @@ class TestResize:
         for i in range(2):
             assert_exact(out[i], O.resize_u8(a[i], dw, dh))
 
+    @pytest.mark.parametrize("geom", [(64, 48, 32, 24), (64, 48, 128, 96), (64, 48, 96, 72), (64, 48, 40, 30)])
+    @pytest.mark.parametrize("path", [0, 1, 2])
+    def test_u8_every_byte_value(self, geom, path):
+        """Every u8 value enters the kernels' u8 -> RN(u/255) conversion (the
+        two-FMA form in fv_common.cuh:unit2) through every path: 2:1, 1:2,
+        generic ratios, gather; u8 HWC and the fused CHW mode."""
+        sw, sh, dw, dh = geom
+        a = (np.arange(sh * sw * 3) * 7 % 256).astype(np.uint8).reshape(sh, sw, 3)
+        assert len(np.unique(a)) == 256
+        with forced_path("resize", path):
+            dst = torch.zeros((dh, dw, 3), dtype=torch.uint8, device=DEV)
+            fv.resize_bilinear_u8(cu(a), dst)
+            dc = torch.zeros((3, dh, dw), dtype=torch.float32, device=DEV)
+            fv.resize_normalize_chw(cu(a), dc, synth.MEAN, synth.STD)
+            out, outc = host(dst), host(dc)
+        assert_exact(out, O.resize_u8(a, dw, dh))
+        assert_exact(outc, O.resize_normalize_chw(a, dw, dh, synth.MEAN, synth.STD))
+
     @pytest.mark.parametrize("dw", [224, 300, 512, 640, 1000, 1280, 1920, 2048])
     @pytest.mark.parametrize("ratio", [4.8, 1.5, 2 / 3])
     def test_strip_tile_widths(self, rng, dw, ratio):
