@@ -16,7 +16,7 @@ timeout 600 python bench.py $short > /dev/null 2>&1 && \
     -k "regex:resize_|warp_|gray_u8|k_|jpeg_" --log-file $out/${tag}_launches.csv \
     python bench.py $short > $out/${tag}_ncu_launch.log 2>&1
 echo "launch list rc=$?"
-for op in resize fused affine persp gray graybatch jpeg; do
+for op in resize fused affine persp gray graybatch jpeg r720 r1080; do
   n=1; kre="regex:resize_|warp_|gray_u8"
   [ $op = resize ] && n=2
   [ $op = gray ] && n=4
