@@ -218,7 +218,7 @@ def warp_perspective(src: torch.Tensor, dst: torch.Tensor, h, border=0, inverse:
 
     u8 images: by default within 1 LSB of the builder oracle (the north-star
     gate for u8 results of float interpolation; f64 anchor + f32 projective
-    correction per 8 pixels, `fv_warp_perspective_u8_fast`); `exact=True`
+    correction per 32-pixel group, `fv_warp_perspective_u8_fast`); `exact=True`
     runs the bit-exact f64-per-pixel kernel. f32 images are always exact."""
     _warp(src, dst, h, border, inverse, perspective=True, exact=exact)
 
