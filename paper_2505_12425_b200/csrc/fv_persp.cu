@@ -414,6 +414,86 @@ __device__ __forceinline__ void pt_rows(const WarpArgs& a, const PtArgs& pa, con
   }
 }
 
+// Step 2 of the kernel, split around the CTA barrier. Lanes 0..4*PT_RPW-1:
+// row r = lane / 4, group g = lane % 4 of this warp's rows.
+struct PtAnchor {
+  double sax, say;         // f64 map of the group's first pixel (absolute)
+  double xl, xh, yl, yh;   // box of the group's first and last pixel maps
+  float kx, ky, waf, iw;   // correction slopes, W_a, 1 / min |W| over the group
+  float rho;               // (|W_a| + 31 |m6|) / min |W|
+  bool sign_ok;            // W keeps one strict sign over the group
+};
+
+__device__ __forceinline__ PtAnchor pt_anchor_map(const double* m, int tx0, int ty0, int warp, int lane) {
+  PtAnchor p;
+  p.sign_ok = false;
+  if (lane < 4 * PT_RPW) {
+    const int r = lane >> 2, g = lane & 3;
+    const double yd = (double)(ty0 + warp + PT_NW * r), xd = (double)(tx0 + 32 * g);
+    const double rx = m[1] * yd + m[2], ry = m[4] * yd + m[5];
+    const double Wa = m[6] * xd + (m[7] * yd + m[8]);
+    const double We = Wa + m[6] * 31.0;
+    const double ra = __drcp_rn(Wa), re = __drcp_rn(We);
+    p.sax = (m[0] * xd + rx) * ra;
+    p.say = (m[3] * xd + ry) * ra;
+    const double sex = (m[0] * (xd + 31.0) + rx) * re, sey = (m[3] * (xd + 31.0) + ry) * re;
+    p.xl = fmin(p.sax, sex);
+    p.xh = fmax(p.sax, sex);
+    p.yl = fmin(p.say, sey);
+    p.yh = fmax(p.say, sey);
+    p.sign_ok = (Wa > 0.0 && We > 0.0) || (Wa < 0.0 && We < 0.0);
+    p.kx = (float)(m[0] - p.sax * m[6]);
+    p.ky = (float)(m[3] - p.say * m[6]);
+    p.waf = (float)Wa;
+    p.iw = __frcp_rn((float)fmin(fabs(Wa), fabs(We)));
+    p.rho = (fabsf(p.waf) + 31.0f * fabsf((float)m[6])) * p.iw;
+  }
+  return p;
+}
+
+// Anchors written to slot (row, pair) as f32x2-ready pairs (group 2p, group
+// 2p + 1) per field: {srx, sry, kx, ky, W_a, flags}; slot stride 12 words:
+// the 16 writers of a field hit 16 distinct banks.
+template <int C>
+__device__ __forceinline__ void pt_anchor_store(const WarpArgs& a, const PtAnchor& p, const PtTile& t, bool staged,
+                                                uint8_t* smem, int tx0, int warp, int lane) {
+  if (lane < 4 * PT_RPW) {
+    const int r = lane >> 2, g = lane & 3;
+    const double dx = p.sax - (double)t.ox, dy = p.say - (double)t.oy;
+    const bool fast = p.sign_ok && fabs(dx) < 1048576.0 && fabs(dy) < 1048576.0;  // false for NaN too
+    const float srx = (float)dx, sry = (float)dy;
+    int flags = 0;
+    if (fast) {
+      const float cx = fabsf(p.kx) * 31.0f * p.iw, cy = fabsf(p.ky) * 31.0f * p.iw;
+      // u (Cmax (rho + 6) + 2 |s_rel|), with slack for the bound's own f32 roundings
+      const float ex = 6.0e-8f * (cx * (p.rho + 7.0f) + 2.0f * fabsf(srx) + 1.0f);
+      const float ey = 6.0e-8f * (cy * (p.rho + 7.0f) + 2.0f * fabsf(sry) + 1.0f);
+      if (ex <= PT_MAX_ERR && ey <= PT_MAX_ERR) {  // false for inf / NaN
+        flags = PG_F32;
+        // the map is monotone along the group (W keeps its sign): its taps lie
+        // between those of the first and last pixel (+-1e-3 px > the bound)
+        const int xlim = a.sw - (staged ? 2 : pt_xmargin<C, false>());
+        if (tx0 + 32 * g + 31 < a.dw && p.xl >= 1e-3 && p.xh <= (double)(xlim + 1) - 1e-3 && p.yl >= 1e-3 &&
+            p.yh <= (double)(a.sh - 1) - 1e-3)
+          flags |= PG_INTERIOR;
+      }
+    }
+    const uint32_t sl = smem_u32(smem) + PT_ANC_OFF + ((warp * PT_RPW * 2 + r * 2 + (g >> 1)) * 12 + (g & 1)) * 4;
+    // 16 writers per store instruction (rows 0-3, then 4-7): distinct banks
+#pragma unroll
+    for (int hb = 0; hb < (PT_RPW + 3) / 4; ++hb) {
+      if ((lane >> 4) == hb) {
+        asm volatile("st.shared.f32 [%0], %1;" ::"r"(sl), "f"(srx));
+        asm volatile("st.shared.f32 [%0], %1;" ::"r"(sl + 8), "f"(sry));
+        asm volatile("st.shared.f32 [%0], %1;" ::"r"(sl + 16), "f"(p.kx));
+        asm volatile("st.shared.f32 [%0], %1;" ::"r"(sl + 24), "f"(p.ky));
+        asm volatile("st.shared.f32 [%0], %1;" ::"r"(sl + 32), "f"(p.waf));
+        asm volatile("st.shared.u32 [%0], %1;" ::"r"(sl + 40), "r"(flags));
+      }
+    }
+  }
+}
+
 template <int C>
 __global__ void __launch_bounds__(PT_NW * 32, PT_MINB) warp_persp_tile_kernel(const __grid_constant__ WarpArgs a,
                                                                       const __grid_constant__ PtArgs pa,
@@ -431,12 +511,17 @@ __global__ void __launch_bounds__(PT_NW * 32, PT_MINB) warp_persp_tile_kernel(co
   const uint8_t* simg = reinterpret_cast<const uint8_t*>(a.src) + (int64_t)n * a.s_is;
   uint8_t* dimg = reinterpret_cast<uint8_t*>(a.dst) + (int64_t)n * a.d_is;
 
+  // Step 2 (first half): the f64 anchor maps. Warps 1.. compute them while
+  // warp 0 classifies the tile (they do not depend on the class); warp 0
+  // after the barrier.
+  PtAnchor ap;
+  if (warp != 0) ap = pt_anchor_map(m, tx0, ty0, warp, lane);
   if (warp == 0) {
     const PtTile tt = pt_classify<C>(a, pa, m, tx0, ty0, lane);
     if (lane == 0) {
       *tile = tt;
       if (tt.cls == PT_STAGED) {
-        mbar_init(bar, 1);
+        mbar_init(bar, PT_NW);  // one arrive.expect_tx per warp
         fence_mbar_init();
       }
     }
@@ -461,68 +546,21 @@ __global__ void __launch_bounds__(PT_NW * 32, PT_MINB) warp_persp_tile_kernel(co
     return;
   }
   const bool staged = t.cls == PT_STAGED;
-  if (staged && warp == 0) {  // warp 0 streams the window's row segments
+  if (warp == 0) ap = pt_anchor_map(m, tx0, ty0, warp, lane);
+  if (staged) {  // every warp streams its share of the window's row segments (rows warp, warp + PT_NW, ...):
+    // a bulk copy takes uniform operands, so one warp would issue the rows one at a time
     FV_CHECK(t.rows >= 1 && t.rows <= PT_WROWS && t.len >= 16 && t.len <= P - 16 && t.cy0 >= 0 &&
              t.cy0 + t.rows <= a.sh && t.sb0 >= 0 && t.sb0 + t.len <= a.sw * C);
-    if (lane == 0) mbar_expect_tx(bar, (uint32_t)(t.rows * t.len));
+    const int nr = max(0, (t.rows - warp + PT_NW - 1) / PT_NW);
+    if (lane == 0) mbar_expect_tx(bar, (uint32_t)(nr * t.len));
     __syncwarp();
     const uint8_t* g = simg + (int64_t)t.cy0 * a.s_rp + t.sb0;
-    for (int r = lane; r < t.rows; r += 32) tma_bulk_g2s(win + r * P, g + (int64_t)r * a.s_rp, (uint32_t)t.len, bar);
+    for (int r = warp + PT_NW * lane; r < t.rows; r += PT_NW * 32)
+      tma_bulk_g2s(win + r * P, g + (int64_t)r * a.s_rp, (uint32_t)t.len, bar);
   }
 
-  // Step 2: anchors of this warp's 4 rows x 4 groups (lanes 0-15), written to
-  // slot (row, pair) as f32x2-ready pairs (group 2p, group 2p + 1) per field:
-  // {srx, sry, kx, ky, W_a, flags}; slot stride 12 words: the 16 writers of a
-  // field hit 16 distinct banks.
-  if (lane < 4 * PT_RPW) {
-    const int r = lane >> 2, g = lane & 3;
-    const double yd = (double)(ty0 + warp + PT_NW * r), xd = (double)(tx0 + 32 * g);
-    const double rx = m[1] * yd + m[2], ry = m[4] * yd + m[5];
-    const double Wa = m[6] * xd + (m[7] * yd + m[8]);
-    const double We = Wa + m[6] * 31.0;
-    const double ra = __drcp_rn(Wa);
-    const double sax = (m[0] * xd + rx) * ra, say = (m[3] * xd + ry) * ra;
-    const double dx = sax - (double)t.ox, dy = say - (double)t.oy;
-    bool fast = ((Wa > 0.0 && We > 0.0) || (Wa < 0.0 && We < 0.0)) && fabs(dx) < 1048576.0 &&
-                fabs(dy) < 1048576.0;  // false for NaN too
-    const float srx = (float)dx, sry = (float)dy;
-    const float kx = (float)(m[0] - sax * m[6]), ky = (float)(m[3] - say * m[6]);
-    const float waf = (float)Wa, m6f = (float)m[6];
-    int flags = 0;
-    if (fast) {
-      const float iw = __frcp_rn((float)fmin(fabs(Wa), fabs(We)));
-      const float rho = (fabsf(waf) + 31.0f * fabsf(m6f)) * iw;
-      const float cx = fabsf(kx) * 31.0f * iw, cy = fabsf(ky) * 31.0f * iw;
-      // u (Cmax (rho + 6) + 2 |s_rel|), with slack for the bound's own f32 roundings
-      const float ex = 6.0e-8f * (cx * (rho + 7.0f) + 2.0f * fabsf(srx) + 1.0f);
-      const float ey = 6.0e-8f * (cy * (rho + 7.0f) + 2.0f * fabsf(sry) + 1.0f);
-      if (ex <= PT_MAX_ERR && ey <= PT_MAX_ERR) {  // false for inf / NaN
-        flags = PG_F32;
-        // the map is monotone along the group (W keeps its sign): its taps lie
-        // between those of the first and last pixel (+-1e-3 px > the bound)
-        const double re = __drcp_rn(We);
-        const double sex = (m[0] * (xd + 31.0) + rx) * re, sey = (m[3] * (xd + 31.0) + ry) * re;
-        const double xl = fmin(sax, sex), xh = fmax(sax, sex), yl = fmin(say, sey), yh = fmax(say, sey);
-        const int xlim = a.sw - (staged ? 2 : pt_xmargin<C, false>());
-        if (tx0 + 32 * g + 31 < a.dw && xl >= 1e-3 && xh <= (double)(xlim + 1) - 1e-3 && yl >= 1e-3 &&
-            yh <= (double)(a.sh - 1) - 1e-3)
-          flags |= PG_INTERIOR;
-      }
-    }
-    const uint32_t sl = smem_u32(smem) + PT_ANC_OFF + ((warp * PT_RPW * 2 + r * 2 + (g >> 1)) * 12 + (g & 1)) * 4;
-    // 16 writers per store instruction (rows 0-3, then 4-7): distinct banks
-#pragma unroll
-    for (int hb = 0; hb < (PT_RPW + 3) / 4; ++hb) {
-      if ((lane >> 4) == hb) {
-        asm volatile("st.shared.f32 [%0], %1;" ::"r"(sl), "f"(srx));
-        asm volatile("st.shared.f32 [%0], %1;" ::"r"(sl + 8), "f"(sry));
-        asm volatile("st.shared.f32 [%0], %1;" ::"r"(sl + 16), "f"(kx));
-        asm volatile("st.shared.f32 [%0], %1;" ::"r"(sl + 24), "f"(ky));
-        asm volatile("st.shared.f32 [%0], %1;" ::"r"(sl + 32), "f"(waf));
-        asm volatile("st.shared.u32 [%0], %1;" ::"r"(sl + 40), "r"(flags));
-      }
-    }
-  }
+  // Step 2 (second half): anchors relative to the tile origin, flags, SMEM slots
+  pt_anchor_store<C>(a, ap, t, staged, smem, tx0, warp, lane);
   __syncwarp();
   const uint32_t smem0 = smem_u32(smem);
   if (staged) {

@@ -977,7 +977,9 @@ __global__ void __launch_bounds__(256, PF_MINB) warp_persp_fast_kernel(const __g
 #ifdef FV_TEST_KNOBS
 static int g_warp_path = 0;  // 0 auto, 1 direct gathers only, 2 bulk-copy tiles, 3 round-1 perspective kernel
 static int g_warp_tma = 1;   // TMA-tensor tiles when available (path 0)
+static int g_warp_src = 1;   // source-tiled affine kernel when applicable (path 0)
 #else
+constexpr int g_warp_src = 1;
 constexpr int g_warp_path = 0;  // product build: always the automatic selection
 constexpr int g_warp_tma = 1;
 #endif
@@ -997,7 +999,7 @@ static int launch_tile(int dw, int dh, int nb, cudaStream_t st, const WarpArgs& 
 
 // cuTensorMapEncodeTiled through the runtime's driver entry point (no
 // libcuda link); null when unavailable (then the bulk-copy tile kernel runs)
-static PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
+PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
   static std::once_flag once;
   static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
   std::call_once(once, [] {
@@ -1136,7 +1138,9 @@ static int launch_warp(const InT* src, int64_t s_is, int64_t s_rp, int sh, int s
     const bool rows16 = (reinterpret_cast<uintptr_t>(a.src) & 15) == 0 && (s_rp & 15) == 0 &&
                         (nb == 1 || (s_is & 15) == 0) && ((pb * sw) & 15) == 0;
     if (!PERSP && g_warp_path == 0 && rows16 && (c == 1 || c == 3 || c == 4)) {
-      int rc = 1;
+      int rc = g_warp_src ? launch_affine_src(a, mats, nb, (int)sizeof(InT), st) : 1;
+      if (rc == 0) continue;
+      if (rc != 1) return rc;
       if (g_warp_tma) {
         switch (c) {
           case 1: rc = launch_tma<InT, 1>(dw, dh, nb, st, a, mats); break;
@@ -1176,8 +1180,11 @@ extern "C" {
 
 #ifdef FV_TEST_KNOBS
 void fv_set_warp_path(int32_t mode) {
-  g_warp_path = mode == 2 ? 0 : mode;  // 3: the round-1 perspective kernel (A/B)
+  // 2: affine without TMA tensor maps; 3: the round-1 perspective kernel (A/B);
+  // 4: affine on the destination-tiled TMA kernel (no source tiles)
+  g_warp_path = (mode == 2 || mode == 4) ? 0 : mode;
   g_warp_tma = mode == 2 ? 0 : 1;
+  g_warp_src = (mode == 2 || mode == 4) ? 0 : 1;
 }
 #endif
 

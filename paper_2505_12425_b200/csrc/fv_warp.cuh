@@ -3,6 +3,9 @@
 // per-pixel map of the builder contract.
 #pragma once
 
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
 #include "fv_common.cuh"
 
 namespace fv {
@@ -72,6 +75,14 @@ __device__ __forceinline__ WarpTap warp_tap(const double (&m)[9], double rx, dou
 // fv_persp.cu: the tile-classified u8 perspective kernel (<= 1 LSB); 0 =
 // launched, 1 = not applicable (channel count / grid), else an error code
 int launch_persp_tile(const WarpArgs& a, const WarpMats& mats, int nb, cudaStream_t st);
+
+// fv_affine.cu: the source-tiled affine kernel (+ its outside-pixel pass) for
+// 16-byte aligned rows, C in {1, 3, 4}, es = element size (1 or 4); 0 =
+// launched, 1 = not applicable, else an error code
+int launch_affine_src(const WarpArgs& a, const WarpMats& mats, int nb, int es, cudaStream_t st);
+
+// cuTensorMapEncodeTiled through the runtime's driver entry point (fv_warp.cu)
+PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder();
 
 __device__ __forceinline__ float rcp_approx(float x) {
   float r;

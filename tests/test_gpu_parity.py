@@ -296,7 +296,7 @@ class TestFused:
 # a8 / a9 warps
 # ---------------------------------------------------------------------------
 
-@pytest.fixture(params=[0, 1, 2], ids=["tma_tile", "direct", "bulk_tile"])
+@pytest.fixture(params=[0, 4, 1, 2], ids=["auto_src_tile", "tma_tile", "direct", "bulk_tile"])
 def warp_path(request):
     with forced_path("warp", request.param):
         yield request.param
@@ -445,6 +445,34 @@ class TestWarp:
                     inv = O.invert_affine(m)
                     for i in range(3):
                         assert_exact(got[i], O.warp_affine(np.ascontiguousarray(view[i]), inv, oh, ow, border=b))
+
+    @pytest.mark.parametrize("dtype", [np.uint8, np.float32])
+    def test_affine_source_tiles_degenerate_axes(self, rng, dtype, warp_path):
+        """Maps whose inverse has zero entries (m0 = 0: a 90-degree turn, so a
+        destination row runs along a source column; m3 = m1 = 0: a pure
+        shift / scale), exact half-pixel shifts that put taps on tile
+        boundaries, mirror images, and a shift that moves the source partly
+        off the destination: every pixel is owned by one source tile or the
+        outside pass, bit-exact."""
+        h, w, c = 75, 96, 3
+        a = rng.integers(0, 256, (h, w, c), dtype=np.uint8)
+        if dtype == np.float32:
+            a = (a / np.float32(255)).astype(np.float32)
+        invs = [
+            np.array([[0.0, 1.0, 0.0], [-1.0, 0.0, h - 1.0]]),           # 90-degree turn
+            np.array([[0.0, -1.25, 80.0], [1.25, 0.0, -7.0]]),           # turn + zoom-out 1.25
+            np.array([[1.0, 0.0, 0.5], [0.0, 1.0, -0.5]]),               # half-pixel shift
+            np.array([[1.0, 0.0, 32.0], [0.0, 1.0, 24.0]]),              # shift by one source tile
+            np.array([[-1.0, 0.0, w - 1.0], [0.0, 1.0, 0.0]]),           # mirror
+            np.array([[0.5, 0.0, -10.0], [0.0, 0.5, 40.0]]),             # 2x zoom-in, partly outside
+            np.array([[1.0, 1e-17, 3.0], [0.0, 1.0, 2.0]]),              # near-degenerate m1
+        ]
+        for inv in invs:
+            for oh, ow, b in [(h, w, 0), (100, 130, 5)]:
+                bb = b if dtype == np.uint8 else b / 255.0
+                dst = torch.zeros((oh, ow, c), dtype=torch.from_numpy(a).dtype, device=DEV)
+                fv.warp_affine(cu(a), dst, inv, border=bb, inverse=True)
+                assert_exact(host(dst), O.warp_affine(a, inv, oh, ow, border=bb))
 
     def test_identity_and_zero_w(self, rng):
         a = rng.integers(0, 256, (10, 12, 3), dtype=np.uint8)
