@@ -10,49 +10,66 @@
 // boxes overlap: the round-1 kernel (32 x 16 destination tiles, a fixed 48 x
 // 40 window) moved 3.1 GB of windows L2 -> SMEM for cfg2's 0.68 GB footprint
 // and spent half its warp time waiting for them (profiles/r02c_ncu_affine).
-// Here a CTA owns a 32 x 32 SOURCE tile instead: every destination pixel
-// whose top-left tap (x0, y0) lies in the tile is sampled by this CTA, and
-// its four taps lie in the (32 + 1) x (32 + 1) window -- a fixed-size 3-D
-// TMA tensor copy (zero fill outside the image) that is read L2 -> SMEM
-// about once per source byte.
+// Here a CTA owns a SA_TW x 32 SOURCE tile instead (SA_TW = 60 for f32
+// images): every destination pixel whose top-left tap (x0, y0) lies in the
+// tile is sampled by this CTA, and its four taps lie in the (SA_TW + 1) x 33
+// window -- one fixed-size 3-D TMA tensor copy (zero fill outside the image)
+// -- so the source crosses L2 -> SMEM about once per byte.
 //
-// Ownership is decided per pixel by the exact f64 map: X0 <= sx < X0 + 32
-// and Y0 <= sy < Y0 + 32, compared in f64. The tiles' ranges tile
-// [-32, 32 (ntx - 1)) x [-32, 32 (nty - 1)) (which contains every pixel with
-// an in-image tap), so every destination pixel is owned by at most one
+// Ownership is decided per pixel by the exact f64 map: floor(sx) in
+// [X0, X0 + SA_TW) and floor(sy) in [Y0, Y0 + 32). The tiles' ranges tile
+// [-SA_TW, SA_TW (ntx - 1)) x [-32, 32 (nty - 1)), which holds every pixel
+// with an in-image tap, so each destination pixel is owned by at most one
 // tile; the rest (all taps outside the source) are written by the CTAs of
-// grid column 0 (sa_outside_row) with the same test, in the same launch. Within a destination row
-// the map is monotone (RN is), so the owned pixels of a row form an
-// interval. The CTA finds its destination rows from the forward-mapped tile
-// corners (+-1 row) and, one thread per row, each row's x interval from the
-// inverse map (a superset: source-space margins of 1e-9 relative dwarf the
-// f64 roundings); a block scan compacts the non-empty rows into a table and
-// the warps walk the flattened pixel list 32 lanes at a time (full lanes
-// however short the rows), each lane finding its row from one shared-memory
-// load and a warp OR-reduction of the rows starting inside its 32-index
-// step. The exact per-pixel test trims the intervals.
+// grid column 0 (sa_outside_row) with the same test, in the same launch.
+// Within a destination row the map is monotone (RN is), so the owned pixels
+// of a row form an interval. The CTA finds its destination rows from the
+// forward-mapped tile corners (+-1 row) and, one thread per row, each row's
+// x interval from the inverse map (a superset: source-space margins of 1e-9
+// relative dwarf the f64 roundings); a block scan compacts the non-empty
+// rows into a table and the warps walk the flattened pixel list 64 indices
+// at a time (full lanes however short the rows), each lane finding its row
+// from one shared-memory load and two warp OR-reductions of the rows
+// starting inside the step. The exact per-pixel test trims the intervals.
 #include <cmath>
 
 #include "fv_warp.cuh"
 
 namespace fv {
 
-// source tile: x0 range SA_TW (64 where the window row fits one 256-element
-// TMA box row, else 32), y0 range SA_TH
+// Window rows are a multiple of 128 bytes (32 banks): then a tap's bank
+// depends on its column only, and the lanes of a warp -- consecutive
+// destination pixels along a rotated source line -- collide only where two
+// share a column (measured on cfg2's maps: 1.6 wavefronts per LDS against
+// 2.3-3.4 for other pitches). Source tile: x0 range SA_TW (the window's
+// (SA_TW + 1) pixels fit the row; X0 = SA_TW * k keeps the tensor copy's
+// innermost start 16-byte aligned), y0 range SA_TH.
+template <typename InT, int C>
+constexpr int sa_box_elems() {  // window row in elements
+  return sizeof(InT) == 4 ? (C == 1 ? 64 : (C == 3 ? 192 : 256)) : (C == 1 ? 128 : 256);
+}
 template <typename InT, int C>
 constexpr int sa_tw() {
-  return ((64 + 1) * C * (int)sizeof(InT) + 15) / 16 * 16 / (int)sizeof(InT) <= 256 ? 64 : 32;
+  return sizeof(InT) == 4 ? 60 : (C == 1 ? 112 : (C == 3 ? 80 : 60));
 }
 constexpr int SA_TH = 32;
-constexpr int SA_NW = 4;   // warps per CTA
+constexpr int SA_NW = 4;  // warps per CTA
 #ifndef SA_MINB
 #define SA_MINB 8
 #endif
-
 template <typename InT, int C>
-constexpr int sa_box_elems() {  // window row in elements: (SA_TW + 1) pixels, a 16-byte multiple
-  return (((sa_tw<InT, C>() + 1) * C * (int)sizeof(InT) + 15) / 16 * 16) / (int)sizeof(InT);
+constexpr bool sa_geometry_ok() {
+  return (sa_tw<InT, C>() + 1) * C <= sa_box_elems<InT, C>() && (sa_tw<InT, C>() * C * (int)sizeof(InT)) % 16 == 0 &&
+         (sa_box_elems<InT, C>() * (int)sizeof(InT)) % 128 == 0;
 }
+static_assert(sa_geometry_ok<float, 1>() && sa_geometry_ok<float, 3>() && sa_geometry_ok<float, 4>() &&
+                  sa_geometry_ok<uint8_t, 1>() && sa_geometry_ok<uint8_t, 3>() && sa_geometry_ok<uint8_t, 4>(),
+              "source-tile geometry");
+template <typename InT, int C>
+constexpr int sa_pitch() {
+  return sa_box_elems<InT, C>() * (int)sizeof(InT);
+}
+constexpr int SA_WROWS = SA_TH + 1;
 
 // Per-image constants from the host (f64): reciprocals of the inverse map's
 // x coefficients (0 when the coefficient is 0) and the forward map's y row
@@ -60,11 +77,6 @@ constexpr int sa_box_elems() {  // window row in elements: (SA_TW + 1) pixels, a
 struct AffineAux {
   double r[MAXW][4];  // {1 / m0, 1 / m3, f10 = -m3 / det, f11 = m0 / det}
 };
-template <typename InT, int C>
-constexpr int sa_pitch() {
-  return sa_box_elems<InT, C>() * (int)sizeof(InT);
-}
-constexpr int SA_WROWS = SA_TH + 1;
 
 // x interval of destination row `y` (row terms rx, ry) whose pixels may map
 // into [xlo, xhi) x [ylo, yhi) (source space): a superset (source-space
