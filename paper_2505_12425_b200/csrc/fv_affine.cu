@@ -52,7 +52,10 @@ template <typename InT, int C>
 constexpr int sa_tw() {
   return sizeof(InT) == 4 ? 60 : (C == 1 ? 112 : (C == 3 ? 80 : 60));
 }
-constexpr int SA_TH = 32;
+#ifndef FV_SA_TH
+#define FV_SA_TH 32
+#endif
+constexpr int SA_TH = FV_SA_TH;  // A/B: 24 / 40 / 48
 constexpr int SA_NW = 4;  // warps per CTA
 #ifndef SA_MINB
 #define SA_MINB 8

@@ -16,7 +16,7 @@ LABELS = {
     "resize_down": ("resize", r"resize_down2_tma_kernel<3>"),
     "resize_up": ("resize", r"resize_up2_kernel<3>"),
     "resize_normalize_chw": ("fused", r"resize_strip_kernel<unsigned char, 3, 2(, 0)?>"),
-    "warp_affine": ("affine", r"warp_affine_tma_kernel<float, 3>"),
+    "warp_affine": ("affine", r"warp_affine_src_kernel<float, 3>"),
     "warp_perspective": ("persp", r"warp_persp_tile_kernel<3>"),
     "gray_u8 32-frame batch (one launch)": ("graybatch", r"gray_u8_vec_kernel"),
     "gray_u8 per frame (graph of 32 launches)": ("gray", r"gray_u8_flat_kernel<8>"),
