@@ -252,6 +252,15 @@ def _affine_ref(i):
     return O.warp_affine(a, O.invert_affine(m), 1080, 1920, border=0.0)
 
 
+def _affine_src_ref(i, u8, c, border):
+    """Full 1080p frames for the source-tiled affine kernel's other
+    instantiations: u8 (80-px tiles) and C = 4 f32, a non-zero border."""
+    a = (synth.seeded_u8_image(1920, 1080, c, seed=synth.SEED_AFFINE + 100 + i) if u8
+         else synth.seeded_f32_image(1920, 1080, c, seed=synth.SEED_AFFINE + 100 + i))
+    m = synth.affine_forward(synth.SEED_AFFINE_PARAMS + 100 + i, 1920, 1080)
+    return a, m, O.warp_affine(a, O.invert_affine(m), 1080, 1920, border=border)
+
+
 def _persp_exact_ref(i):
     a = synth.seeded_u8_image(3840, 2160, 3, seed=synth.SEED_PERSP + i)
     return O.warp_perspective(a, O.invert_homography(synth.perspective_forward(synth.SEED_PERSP_PARAMS + i)),
@@ -324,6 +333,20 @@ class TestWarp:
         out = host(dst)
         for i, ref in enumerate(oracle_map(_affine_ref, [(i,) for i in range(n)])):
             assert_exact(out[i], ref)
+
+    @pytest.mark.parametrize("u8,c", [(True, 3), (True, 1), (False, 4), (True, 4)])
+    def test_affine_source_tiles_full_frames(self, u8, c):
+        """The source-tiled kernel's other tile geometries on full 1080p
+        frames (two images with their own cfg2-style maps in one launch, a
+        non-zero border so the outside pass blends border taps), bit-exact."""
+        border = 37 if u8 else 0.3
+        refs = oracle_map(_affine_src_ref, [(i, u8, c, border) for i in range(2)])
+        src = cu(np.stack([r[0] for r in refs]))
+        dst = torch.zeros_like(src)
+        fv.warp_affine(src, dst, np.stack([r[1] for r in refs]), border=border)
+        out = host(dst)
+        for i, r in enumerate(refs):
+            assert_exact(out[i], r[2])
 
     def test_cfg3_perspective_exact_all_16_images(self):
         """exact=True on all 16 cfg3 images, full frames (bit-exact)."""
