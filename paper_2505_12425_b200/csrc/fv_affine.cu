@@ -467,14 +467,22 @@ __global__ void __launch_bounds__(SA_NW * 32, SA_MINB) warp_affine_src_kernel(co
         const double rx_ = __hiloint2double(e1.y, e1.x), ry_ = __hiloint2double(e1.w, e1.z);
         double sx, sy;
         sa_map(m, x[p], rx_, ry_, sx, sy);
+        // floor on the FP64 pipe instead of the conversion unit: RD(s + 1.5 *
+        // 2^52) = 1.5 * 2^52 + floor(s) exactly for |s| < 2^51 (an enumerated
+        // pixel's map lies within a few tile widths of the tile: its row
+        // interval is a superset of the owned pixels by 1e-9 relative), its
+        // low word is floor(s) as an int, and subtracting the magic back is
+        // exact (cfg2: 0.303 -> 0.298 ms)
+        const double MF = 6755399441055744.0;  // 1.5 * 2^52
+        const double tx = __dadd_rd(sx, MF), ty = __dadd_rd(sy, MF);
+        const int fxi = __double2loint(tx), fyi = __double2loint(ty);
         // owned: X0 <= sx < X0 + SA_TW and likewise y, i.e. floor(sx) in
-        // [X0, X0 + SA_TW) (X0 integral); cvt.rmi saturates out-of-range maps
-        const int fxi = __double2int_rd(sx), fyi = __double2int_rd(sy);
+        // [X0, X0 + SA_TW) (X0 integral)
         ox[p] = (int)((unsigned)fxi - (unsigned)X0);
         oy[p] = (int)((unsigned)fyi - (unsigned)Y0);
         own[p] = valid && (unsigned)ox[p] < (unsigned)SA_TW && (unsigned)oy[p] < (unsigned)SA_TH;
-        wx1[p] = __double2float_rn(__dadd_rn(sx, -(double)fxi));
-        wy1[p] = __double2float_rn(__dadd_rn(sy, -(double)fyi));
+        wx1[p] = __double2float_rn(__dadd_rn(sx, -__dadd_rn(tx, -MF)));
+        wy1[p] = __double2float_rn(__dadd_rn(sy, -__dadd_rn(ty, -MF)));
         if (!own[p]) {
           ox[p] = 0;
           oy[p] = 0;
