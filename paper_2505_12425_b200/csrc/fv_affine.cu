@@ -108,7 +108,8 @@ __device__ __forceinline__ void sa_row_span(double rm0, double rm3, double rx, d
     hi = -INFINITY;
   }
   // integer bounds: the margins ex, ey dwarf the roundings of the product
-  // with the reciprocal (<= 2 ulp relative) and of the per-pixel map, so every owned x lies in [ceil(lo), floor(hi)]
+  // with the reciprocal (<= 2 ulp relative) and of the per-pixel map, so
+  // every owned x lies in [ceil(lo), floor(hi)]
   lo = ceil(lo);
   hi = floor(hi);
 }
@@ -237,7 +238,8 @@ __device__ __forceinline__ void sa_rows_of64(const int* off, int nne, int base, 
 // SMEM layout of the source-tiled kernel
 constexpr int SA_MAXR = SA_NW * 32;                 // destination rows per batch (one per thread)
 constexpr int SA_OFF = 64;                          // int off[SA_MAXR + 1]
-constexpr int SA_TAB = (SA_OFF + 4 * (SA_MAXR + 1) + 127) / 128 * 128;  // row entries, 32 B: {x - index, y, rx, ry}
+// row entries, 32 B: {x - index, byte offset of (row, x - index) in the image (64-bit), pad, rx, ry}
+constexpr int SA_TAB = (SA_OFF + 4 * (SA_MAXR + 1) + 127) / 128 * 128;
 constexpr int SA_WIN = SA_TAB + 32 * SA_MAXR;       // the window (128-byte aligned)
 template <typename InT, int C>
 constexpr int sa_smem2() {
