@@ -1078,7 +1078,7 @@ def parse_args(argv=None):
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--dry-run", action="store_true", help="CPU/gloo stand-in ops: exercises the rank plumbing")
     ap.add_argument("--soak", type=float, default=1.0,
-                    help="seconds of untimed cfg1 steps before timing (clock sampler sees a loaded GPU)")
+                    help="seconds of untimed steps of each op before timing it (sustained clocks; the sampler sees a loaded GPU)")
     return ap.parse_args(argv)
 
 
@@ -1144,7 +1144,10 @@ def run_fovea(args, world, rank, local):
         sampler.start()
     results = {}
     for op in ops:
-        soak = args.soak if (op.key == "resize" and not be.dry) else 0.0
+        # every op soaks with itself first, so each is timed at its own
+        # sustained operating point (power cap, clocks), not in the state the
+        # previous op left (cfg2 after cfg1's soak: 0.353 ms; after its own: ~0.30)
+        soak = args.soak if not be.dry else 0.0
         ms, per, lc = time_op(be, op, args.steps, max(3, args.warmup), stream, soak_s=soak)
         kern = []
         for (lname, _, nbytes), t in zip(op.launches, per):
