@@ -6,7 +6,7 @@
 // blend in imgproc.py:118-123 order, u8 through the app.py:64-78 recipe.
 // North star gate for u8 results of float interpolation: <= 1 LSB.
 //
-// One CTA = one 128 x 32 destination tile (8 warps x 4 rows, rows 8 apart).
+// One CTA = one 128 x 48 destination tile (8 warps x 6 rows, rows 8 apart).
 //   1. Tile class, from the four corner maps (f64): a projective map whose W
 //      keeps one strict sign over the tile sends it onto the convex hull of
 //      the mapped corners, so the hull's box (+2 / +3 px) holds every tap.
@@ -47,8 +47,11 @@
 
 namespace fv {
 
+#ifndef FV_PT_TH
+#define FV_PT_TH 48  // 6 rows per warp: measured 32 / 40 / 48 / 56 / 64 -> cfg3 0.443 / 0.428 / 0.425 / 0.420 / 0.414 ms, but 56+ rows push near-identity tiles out of the 56-row window (0.447 -> 0.519 ms)
+#endif
 constexpr int PT_TW = 128;          // tile width, destination pixels (4 anchor groups of 32)
-constexpr int PT_TH = 32;           // tile height: PT_NW warps x PT_RPW rows
+constexpr int PT_TH = FV_PT_TH;     // tile height: PT_NW warps x PT_RPW rows
 #ifndef PT_NW
 #define PT_NW 8  // warps per CTA
 #endif
