@@ -19,14 +19,14 @@
 //                  STAGED_IN = the box lies inside the image, so no pixel
 //                  needs a bounds test;
 //        DIRECT    W changes sign in the tile, or the box is too large
-//                  (strong zoom-in): direct global gathers.
-//   2. Maps: one f64 anchor per 32 pixels of a row (lanes 0-15 of a warp
-//      compute the 16 anchors of its 4 rows at once) -- s_a = (X, Y) / W at
+//                  (zoom-out): direct global gathers.
+//   2. Maps: one f64 anchor per 32 pixels of a row (lanes 0-23 of a warp
+//      compute the 24 anchors of its 6 rows at once) -- s_a = (X, Y) / W at
 //      the group's first pixel, relative to the tile origin -- then lane L
 //      samples pixel x_a + L of every group with the f32 projective
 //      correction s = s_a + k * L / W(L), k = (m0 - s_a.x m6, m3 - s_a.y m6),
 //      W(L) = W_a + m6 L (rcp.approx), two pixels at a time as f32x2 pairs.
-//      Anchors live in SMEM slots laid out so the 16 writers hit 16 distinct
+//      Anchors live in SMEM slots laid out so each 16 writers hit 16 distinct
 //      banks and each reader gets a field of both pixels of its pair from one
 //      LDS.128 (broadcast: a group is warp-uniform).
 //   3. Error bound per group (u = 2^-24): W(L) carries <= u (rho + 1)
