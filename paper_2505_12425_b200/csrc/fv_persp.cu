@@ -57,10 +57,10 @@ constexpr int PT_TH = FV_PT_TH;     // tile height: PT_NW warps x PT_RPW rows
 #endif
 constexpr int PT_RPW = PT_TH / PT_NW;  // rows per warp (rows warp, warp + PT_NW, ...)
 #ifndef FV_PT_PITCH3
-#define FV_PT_PITCH3 656  // C = 3 window pitch (bytes)
+#define FV_PT_PITCH3 592  // C = 3 window pitch (bytes); 48-row tiles: 56 x 656 / 60 x 624 / 64 x 592 / 56 x 720 -> cfg3 0.425 / 0.423 / 0.421 / 0.487 ms
 #endif
 #ifndef FV_PT_WROWS
-#define FV_PT_WROWS 56
+#define FV_PT_WROWS 64
 #endif
 constexpr int PT_WROWS = FV_PT_WROWS;  // SMEM window rows
 constexpr float PT_MAX_ERR = 5e-4f;
@@ -68,8 +68,8 @@ constexpr float PT_MAX_ERR = 5e-4f;
 #define PT_MINB 4
 #endif
 // window pitch in bytes: an odd multiple of 16 (bulk-copy destinations are
-// 16-byte aligned; rows rotate banks), wide enough for a 1.6x zoom-in of a
-// 128-pixel row plus the tap window's 12-byte overhang
+// 16-byte aligned; rows rotate banks), wide enough for a 1.4x zoom-out of a
+// 128-pixel row plus the tap window's 12-byte overhang (C = 3)
 template <int C>
 constexpr int pt_pitch() { return C == 1 ? 240 : (C == 3 ? FV_PT_PITCH3 : 848); }
 template <int C>
