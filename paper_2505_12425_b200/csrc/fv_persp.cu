@@ -103,7 +103,12 @@ struct PtTile {
 template <int C>
 __device__ __forceinline__ PtTile pt_classify(const WarpArgs& a, const PtArgs& pa, const double* m, int tx0, int ty0,
                                               int lane) {
-  double sx = 0.0, sy = 0.0;
+  // the corner maps in f64, then the box in f32: coordinates are clamped to
+  // +-2^30 and the box carries 2 px margins (+1e-6 relative), far above
+  // f32's rounding of any coordinate that can reach the window (|s| < 2^13);
+  // the f64 min / max chains and double shuffles cost warp 0 -- the CTA's
+  // critical path -- more than they buy
+  float sx = 0.0f, sy = 0.0f;
   int sg = 0;
   if (lane < 4) {
     const double cx = (double)(tx0 + ((lane & 1) ? PT_TW - 1 : 0));
@@ -111,34 +116,35 @@ __device__ __forceinline__ PtTile pt_classify(const WarpArgs& a, const PtArgs& p
     const double X = m[0] * cx + m[1] * cy + m[2], Y = m[3] * cx + m[4] * cy + m[5];
     const double W = m[6] * cx + m[7] * cy + m[8];
     const double r = __drcp_rn(W);  // the box has 2 px margins: no need for a division
-    sx = X * r;
-    sy = Y * r;
+    const double dx = X * r, dy = Y * r;
     sg = (W > 0.0) ? 1 : (W < 0.0 ? 2 : 0);
-    if (!(isfinite(sx) && isfinite(sy))) sg = 0;
+    if (!(isfinite(dx) && isfinite(dy))) sg = 0;
+    const double L = 1073741824.0;
+    sx = (float)(dx < -L ? -L : (dx > L ? L : dx));
+    sy = (float)(dy < -L ? -L : (dy > L ? L : dy));
   }
   const unsigned F = 0xffffffffu;
-  double cxs[4], cys[4];
-  int sgall = 3;
+  float xlo = __shfl_sync(F, sx, 0), ylo = __shfl_sync(F, sy, 0);
+  float xhi = xlo, yhi = ylo;
+  int sgall = __shfl_sync(F, sg, 0);
 #pragma unroll
-  for (int k = 0; k < 4; ++k) {
-    cxs[k] = __shfl_sync(F, sx, k);
-    cys[k] = __shfl_sync(F, sy, k);
+  for (int k = 1; k < 4; ++k) {
+    const float ux = __shfl_sync(F, sx, k), uy = __shfl_sync(F, sy, k);
+    xlo = fminf(xlo, ux);
+    xhi = fmaxf(xhi, ux);
+    ylo = fminf(ylo, uy);
+    yhi = fmaxf(yhi, uy);
     sgall &= __shfl_sync(F, sg, k);
   }
-  const double xlo = fmin(fmin(cxs[0], cxs[1]), fmin(cxs[2], cxs[3]));
-  const double xhi = fmax(fmax(cxs[0], cxs[1]), fmax(cxs[2], cxs[3]));
-  const double ylo = fmin(fmin(cys[0], cys[1]), fmin(cys[2], cys[3]));
-  const double yhi = fmax(fmax(cys[0], cys[1]), fmax(cys[2], cys[3]));
   PtTile t{PT_DIRECT, 0, 0, 0, 0, 0, 0, 0};
   if (sgall == 0) return t;  // W changes sign or vanishes in the tile: no hull
-  const double mx = 2.0 + 1e-6 * fmax(fabs(xlo), fabs(xhi)), my = 2.0 + 1e-6 * fmax(fabs(ylo), fabs(yhi));
-  if (xhi < -1.0 - mx || xlo > (double)a.sw + mx || yhi < -1.0 - my || ylo > (double)a.sh + my) {
+  const float mx = 2.0f + 1e-6f * fmaxf(fabsf(xlo), fabsf(xhi)), my = 2.0f + 1e-6f * fmaxf(fabsf(ylo), fabsf(yhi));
+  if (xhi < -1.0f - mx || xlo > (float)a.sw + mx || yhi < -1.0f - my || ylo > (float)a.sh + my) {
     t.cls = PT_BORDER;
     return t;
   }
-  const double L = 1073741824.0;  // keep the box in int range (far boxes fail the anchor bound)
-  const double bx0 = fmin(fmax(floor(xlo) - 2.0, -L), L), bx1 = fmin(fmax(floor(xhi) + 3.0, -L), L);
-  const double by0 = fmin(fmax(floor(ylo) - 2.0, -L), L), by1 = fmin(fmax(floor(yhi) + 3.0, -L), L);
+  const float bx0 = floorf(xlo) - 2.0f, bx1 = floorf(xhi) + 3.0f;
+  const float by0 = floorf(ylo) - 2.0f, by1 = floorf(yhi) + 3.0f;
   t.ox = (int)bx0;
   t.oy = (int)by0;
   const int cx0 = max(t.ox, 0), cx1 = min((int)bx1, a.sw - 1);
