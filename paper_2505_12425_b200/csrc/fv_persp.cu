@@ -427,9 +427,9 @@ __device__ __forceinline__ void pt_rows(const WarpArgs& a, const PtArgs& pa, con
 // row r = lane / 4, group g = lane % 4 of this warp's rows.
 struct PtAnchor {
   double sax, say;         // f64 map of the group's first pixel (absolute)
-  double xl, xh, yl, yh;   // box of the group's first and last pixel maps
   float kx, ky, waf, iw;   // correction slopes, W_a, 1 / min |W| over the group
   float rho;               // (|W_a| + 31 |m6|) / min |W|
+  float wef;               // W at the group's last pixel
   bool sign_ok;            // W keeps one strict sign over the group
 };
 
@@ -442,14 +442,10 @@ __device__ __forceinline__ PtAnchor pt_anchor_map(const double* m, int tx0, int 
     const double rx = m[1] * yd + m[2], ry = m[4] * yd + m[5];
     const double Wa = m[6] * xd + (m[7] * yd + m[8]);
     const double We = Wa + m[6] * 31.0;
-    const double ra = __drcp_rn(Wa), re = __drcp_rn(We);
+    const double ra = __drcp_rn(Wa);
     p.sax = (m[0] * xd + rx) * ra;
     p.say = (m[3] * xd + ry) * ra;
-    const double sex = (m[0] * (xd + 31.0) + rx) * re, sey = (m[3] * (xd + 31.0) + ry) * re;
-    p.xl = fmin(p.sax, sex);
-    p.xh = fmax(p.sax, sex);
-    p.yl = fmin(p.say, sey);
-    p.yh = fmax(p.say, sey);
+    p.wef = (float)We;
     p.sign_ok = (Wa > 0.0 && We > 0.0) || (Wa < 0.0 && We < 0.0);
     p.kx = (float)(m[0] - p.sax * m[6]);
     p.ky = (float)(m[3] - p.say * m[6]);
@@ -480,10 +476,16 @@ __device__ __forceinline__ void pt_anchor_store(const WarpArgs& a, const PtAncho
       if (ex <= PT_MAX_ERR && ey <= PT_MAX_ERR) {  // false for inf / NaN
         flags = PG_F32;
         // the map is monotone along the group (W keeps its sign): its taps lie
-        // between those of the first and last pixel (+-1e-3 px > the bound)
+        // between those of the first and last pixel. The last one from the
+        // f32 correction s_a + 31 k / W_e (relative coordinates, |s| < 4200
+        // px under the bound: within ~6e-4 px), offset in f64; 2e-3 px margins
+        const float rex = __frcp_rn(p.wef);
+        const float sex = __fmaf_rn(31.0f * p.kx, rex, srx), sey = __fmaf_rn(31.0f * p.ky, rex, sry);
+        const double xl = (double)fminf(srx, sex) + (double)t.ox, xh = (double)fmaxf(srx, sex) + (double)t.ox;
+        const double yl = (double)fminf(sry, sey) + (double)t.oy, yh = (double)fmaxf(sry, sey) + (double)t.oy;
         const int xlim = a.sw - (staged ? 2 : pt_xmargin<C, false>());
-        if (tx0 + 32 * g + 31 < a.dw && p.xl >= 1e-3 && p.xh <= (double)(xlim + 1) - 1e-3 && p.yl >= 1e-3 &&
-            p.yh <= (double)(a.sh - 1) - 1e-3)
+        if (tx0 + 32 * g + 31 < a.dw && xl >= 2e-3 && xh <= (double)(xlim + 1) - 2e-3 && yl >= 2e-3 &&
+            yh <= (double)(a.sh - 1) - 2e-3)
           flags |= PG_INTERIOR;
       }
     }
