@@ -242,6 +242,16 @@ __device__ __forceinline__ T* row_ptr_mut(void* base, int64_t img_stride, int64_
 __device__ __forceinline__ float tap_value(uint8_t u) { return u8_to_unit(u); }
 __device__ __forceinline__ float tap_value(float f) { return f; }
 
+// Warp index as a value ptxas can prove warp-uniform (a shuffle from lane
+// 0). threadIdx.x >> 5 is uniform per warp, but ptxas treats it as per-thread:
+// code after a warp-role branch on it then counts as divergent, and ptxas
+// keeps the global-memory descriptor in ordinary registers and copies it into
+// uniform ones (2 R2UR) before every global access in the loop. Branching on
+// this value keeps the descriptor and the loop's address arithmetic uniform.
+__device__ __forceinline__ int warp_index_uniform() {
+  return __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0);
+}
+
 // ---------------------------------------------------------------------------
 // mbarrier + TMA bulk copy (cp.async.bulk) PTX wrappers
 // ---------------------------------------------------------------------------

@@ -119,41 +119,51 @@ struct Up2 {
 };
 
 // h for the thread's 8 destination pixels from one source row's window, as
-// E/2 packed pairs of consecutive destination elements
+// 4C packed pairs laid out for FFMA2 (the destination element of each half is
+// up2_elem below). Per channel, with v[m] the unit value of source pixel
+// 4t + m (m = -1..4) and P[m] = RN(0.75 v[m]):
+//   h[4c]     = {E0, E1}, h[4c + 1] = {E2, E3}   E[m] = fma(v[m-1], 0.25, P[m])  -> dst px 2m
+//   h[4c + 2] = {O0, O1}, h[4c + 3] = {O2, O3}   O[m] = fma(v[m+1], 0.25, P[m])  -> dst px 2m+1
+// The unit conversions are done in the pairs {v-1, v0}, {v1, v2}, {v3, v4};
+// the P pairs {P0, P1}, {P2, P3} come from the two re-paired {v0, v1},
+// {v2, v3} (register moves), so every product and sum is one f32x2 op.
 template <int C>
 __device__ __forceinline__ void up2_h(const uint32_t (&w)[Up2<C>::NW], int t, int last_t, f2_t (&h)[4 * C]) {
-  // v for source pixels m = -1..4 relative to 4t (window bytes 4-C .. 4+5C-1),
-  // converted two at a time
-  float v[6 * C];
+  const f2_t q4 = f2(0.25f, 0.25f), t4 = f2(0.75f, 0.75f);
 #pragma unroll
-  for (int j = 0; j < 6 * C; j += 2) {
-    uint32_t lo, hi;
-    f2split(unit2(magic_of(w, 4 - C + j), magic_of(w, 4 - C + j + 1)), lo, hi);
-    v[j] = __uint_as_float(lo);
-    v[j + 1] = __uint_as_float(hi);
-  }
-  // v[m][c] = v[(m + 1) * C + c]
-  float P[4 * C];
-#pragma unroll
-  for (int i = 0; i < 4 * C; ++i) P[i] = __fmul_rn(v[C + i], 0.75f);
-  float hs[8 * C];
-#pragma unroll
-  for (int m = 0; m < 4; ++m)
-#pragma unroll
-    for (int c = 0; c < C; ++c) {
-      hs[(2 * m) * C + c] = __fmaf_rn(v[m * C + c], 0.25f, P[m * C + c]);
-      hs[(2 * m + 1) * C + c] = __fmaf_rn(v[(m + 2) * C + c], 0.25f, P[m * C + c]);
+  for (int c = 0; c < C; ++c) {
+    // window byte of source pixel 4t + m, channel c: 4 + m*C + c
+    const f2_t A = unit2(magic_of(w, 4 - C + c), magic_of(w, 4 + c));
+    const f2_t B = unit2(magic_of(w, 4 + C + c), magic_of(w, 4 + 2 * C + c));
+    const f2_t D = unit2(magic_of(w, 4 + 3 * C + c), magic_of(w, 4 + 4 * C + c));
+    uint32_t a0, a1, b0, b1, d0, d1;
+    f2split(A, a0, a1);
+    f2split(B, b0, b1);
+    f2split(D, d0, d1);
+    const f2_t PX = fmul2(f2u(a1, b0), t4), PY = fmul2(f2u(b1, d0), t4);
+    f2_t E01 = ffma2(A, q4, PX);
+    const f2_t E23 = ffma2(B, q4, PY), O01 = ffma2(B, q4, PX);
+    f2_t O23 = ffma2(D, q4, PY);
+    if (t == 0) {  // destination pixel 0: clamped, fx = 0 -> copy of v0
+      uint32_t lo, hi;
+      f2split(E01, lo, hi);
+      E01 = f2u(a1, hi);
     }
-  if (t == 0) {  // destination pixel 0: clamped, fx = 0 -> copy
-#pragma unroll
-    for (int c = 0; c < C; ++c) hs[c] = v[C + c];
+    if (t == last_t) {  // destination pixel 2W-1: clamped, fx = 0 -> copy of v3
+      uint32_t lo, hi;
+      f2split(O23, lo, hi);
+      O23 = f2u(lo, d0);
+    }
+    h[4 * c] = E01;
+    h[4 * c + 1] = E23;
+    h[4 * c + 2] = O01;
+    h[4 * c + 3] = O23;
   }
-  if (t == last_t) {  // destination pixel 2W-1: clamped, fx = 0 -> copy
-#pragma unroll
-    for (int c = 0; c < C; ++c) hs[7 * C + c] = v[4 * C + c];
-  }
-#pragma unroll
-  for (int i = 0; i < 4 * C; ++i) h[i] = f2(hs[2 * i], hs[2 * i + 1]);
+}
+// destination element (px * C + c) of half `hi` of pair p in up2_h's layout
+template <int C>
+__host__ __device__ constexpr int up2_elem(int p, int hi) {
+  return (2 * (2 * ((p & 3) & 1) + hi) + ((p & 3) >> 1)) * C + p / 4;
 }
 
 #ifndef FV_UP2_CS
@@ -168,36 +178,34 @@ __device__ __forceinline__ void up2_store(uint2* p, uint2 v) {
 #endif
 }
 
-// one destination row from two h rows: o = fma(hb, 0.25, qa), epilogue in
-// f32x2, packed 4 bytes at a time and written as 8-byte stores (8*C bytes)
+// the 4C result pairs of one destination row (float-bit words, low byte =
+// value) -> 2C words in memory order, written as C 8-byte stores
 template <int C>
-__device__ __forceinline__ void up2_emit(uint8_t* drow, const f2_t (&hb)[4 * C], const f2_t (&qa)[4 * C], f2_t one) {
+__device__ __forceinline__ void up2_pack_store(uint8_t* drow, const f2_t (&r)[4 * C]) {
+  uint32_t e[8 * C];
 #pragma unroll
-  for (int i = 0; i < C; ++i) {
-    uint32_t w[2];
+  for (int p = 0; p < 4 * C; ++p) f2split(r[p], e[up2_elem<C>(p, 0)], e[up2_elem<C>(p, 1)]);
 #pragma unroll
-    for (int j = 0; j < 2; ++j) {
-      const int e = 4 * i + 2 * j;  // pair index
-      const f2_t r0 = scale_to_u8_bits2(ffma2(hb[e], f2(0.25f, 0.25f), qa[e]), 255.0f);
-      const f2_t r1 = scale_to_u8_bits2(ffma2(hb[e + 1], f2(0.25f, 0.25f), qa[e + 1]), 255.0f);
-      w[j] = pack4x2(r0, r1);
-    }
-    up2_store(reinterpret_cast<uint2*>(drow) + i, make_uint2(w[0], w[1]));
-  }
+  for (int i = 0; i < C; ++i)
+    up2_store(reinterpret_cast<uint2*>(drow) + i,
+              make_uint2(pack4(e[8 * i], e[8 * i + 1], e[8 * i + 2], e[8 * i + 3]),
+                         pack4(e[8 * i + 4], e[8 * i + 5], e[8 * i + 6], e[8 * i + 7])));
+}
+// one destination row from two h rows: o = fma(hb, 0.25, qa), epilogue in f32x2
+template <int C>
+__device__ __forceinline__ void up2_emit(uint8_t* drow, const f2_t (&hb)[4 * C], const f2_t (&qa)[4 * C]) {
+  f2_t r[4 * C];
+#pragma unroll
+  for (int p = 0; p < 4 * C; ++p) r[p] = scale_to_u8_bits2(ffma2(hb[p], f2(0.25f, 0.25f), qa[p]), 255.0f);
+  up2_pack_store<C>(drow, r);
 }
 // a row that is a plain copy of h (clamped rows 0 and 2H-1, fy = 0)
 template <int C>
-__device__ __forceinline__ void up2_emit_copy(uint8_t* drow, const f2_t (&h)[4 * C], f2_t one) {
+__device__ __forceinline__ void up2_emit_copy(uint8_t* drow, const f2_t (&h)[4 * C]) {
+  f2_t r[4 * C];
 #pragma unroll
-  for (int i = 0; i < C; ++i) {
-    uint32_t w[2];
-#pragma unroll
-    for (int j = 0; j < 2; ++j) {
-      const int e = 4 * i + 2 * j;
-      w[j] = pack4x2(scale_to_u8_bits2(h[e], 255.0f), scale_to_u8_bits2(h[e + 1], 255.0f));
-    }
-    up2_store(reinterpret_cast<uint2*>(drow) + i, make_uint2(w[0], w[1]));
-  }
+  for (int p = 0; p < 4 * C; ++p) r[p] = scale_to_u8_bits2(h[p], 255.0f);
+  up2_pack_store<C>(drow, r);
 }
 
 // TMA-staged variant: a CTA = 4 consumer warps (128 column groups = 512
@@ -224,19 +232,20 @@ __device__ __forceinline__ void up2_lds(const uint8_t* seg_row_base, int t, uint
   for (int i = 0; i < Up2<C>::NW; ++i) w[i] = rw[i];
 }
 
+// source row k: destination rows 2k-1 and 2k; dr points at row 2k
 template <int C>
-__device__ __forceinline__ void up2_step_s(uint8_t* dimg, const FastArgs& a, int t, int k,
+__device__ __forceinline__ void up2_step_s(uint8_t* dr, int64_t rp, int t, int last_t, bool first,
                                            const uint32_t (&w)[Up2<C>::NW], const f2_t (&hp)[4 * C],
                                            f2_t (&q)[4 * C], f2_t (&hn)[4 * C]) {
-  up2_h<C>(w, t, a.groups - 1, hn);
-  if (k == 0) {
-    up2_emit_copy<C>(dimg, hn, a.one2);
+  up2_h<C>(w, t, last_t, hn);
+  if (first) {
+    up2_emit_copy<C>(dr, hn);
   } else {
-    up2_emit<C>(dimg + (int64_t)(2 * k - 1) * a.d_rp, hn, q, a.one2);
+    up2_emit<C>(dr - rp, hn, q);
   }
 #pragma unroll
   for (int e = 0; e < 4 * C; ++e) q[e] = fmul2(hn[e], f2(0.75f, 0.75f));
-  if (k > 0) up2_emit<C>(dimg + (int64_t)(2 * k) * a.d_rp, hp, q, a.one2);
+  if (!first) up2_emit<C>(dr, hp, q);
 }
 
 template <int C>
@@ -247,7 +256,7 @@ __global__ void __launch_bounds__((UP2_NCW + 1) * 32, 4) resize_up2_kernel(const
   uint64_t* empty = full + UP2_RING;
   uint8_t* slots = smem + 16 * UP2_RING + 16;  // 16 bytes of slack before slot 0
 
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int warp = warp_index_uniform(), lane = threadIdx.x & 31;
   const int n = blockIdx.z;
   const int k0 = blockIdx.y * a.band;
   const int k1 = min(k0 + a.band, a.sh);
@@ -296,39 +305,45 @@ __global__ void __launch_bounds__((UP2_NCW + 1) * 32, 4) resize_up2_kernel(const
   const bool active = t < g1;
 #endif
   uint8_t* dimg = a.dst + n * a.d_is + (int64_t)t * 8 * C;
+  const int64_t rp = a.d_rp;
+  const int last_t = a.groups - 1;
   f2_t h0[NP], h1[NP], q[NP];
   uint32_t w[NW];
-  int i = 0;
-  auto take = [&](int r) {  // window of source row r from the ring
-    const int slot = i % UP2_RING;
-    mbar_wait(&full[slot], (uint32_t)((i / UP2_RING) & 1));
+  int slot = 0;
+  uint32_t phase = 0;
+  auto take = [&]() {  // window of the next source row from the ring
+    mbar_wait(&full[slot], phase);
     up2_lds<C>(slots + slot * a.slot_bytes - gstart, t, w);
     slot_release(&empty[slot], lane);
-    ++i;
-    (void)r;
+    if (++slot == UP2_RING) {
+      slot = 0;
+      phase ^= 1u;
+    }
   };
   if (k0 > 0) {
-    take(k0 - 1);
-    up2_h<C>(w, t, a.groups - 1, h0);
+    take();  // row k0 - 1
+    up2_h<C>(w, t, last_t, h0);
 #pragma unroll
     for (int e = 0; e < NP; ++e) q[e] = fmul2(h0[e], f2(0.75f, 0.75f));
   }
   int k = k0;
+  uint8_t* dr = dimg + (int64_t)(2 * k0) * rp;  // destination row 2k
 #pragma unroll 1
   for (; k + 1 < k1; k += 2) {
-    take(k);
-    if (active) up2_step_s<C>(dimg, a, t, k, w, h0, q, h1);
-    take(k + 1);
-    if (active) up2_step_s<C>(dimg, a, t, k + 1, w, h1, q, h0);
+    take();
+    if (active) up2_step_s<C>(dr, rp, t, last_t, k == 0, w, h0, q, h1);
+    take();
+    if (active) up2_step_s<C>(dr + 2 * rp, rp, t, last_t, false, w, h1, q, h0);
+    dr += 4 * rp;
   }
   if (k < k1) {
-    take(k);
+    take();
     if (active) {
-      up2_step_s<C>(dimg, a, t, k, w, h0, q, h1);
-      if (k1 == a.sh) up2_emit_copy<C>(dimg + (int64_t)(2 * a.sh - 1) * a.d_rp, h1, a.one2);
+      up2_step_s<C>(dr, rp, t, last_t, k == 0, w, h0, q, h1);
+      if (k1 == a.sh) up2_emit_copy<C>(dr + rp, h1);
     }
   } else if (k1 == a.sh && active) {
-    up2_emit_copy<C>(dimg + (int64_t)(2 * a.sh - 1) * a.d_rp, h0, a.one2);
+    up2_emit_copy<C>(dr - rp, h0);
   }
 }
 
@@ -347,7 +362,7 @@ __global__ void __launch_bounds__((D2_NCW + 1) * 32) resize_down2_tma_kernel(con
   uint64_t* empty = full + D2_RING;
   uint8_t* slots = smem + 16 * D2_RING;
 
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int warp = warp_index_uniform(), lane = threadIdx.x & 31;
   const int n = blockIdx.z;
   const int y0 = blockIdx.y * a.band, y1 = min(y0 + a.band, a.dh);
   const int g0 = blockIdx.x * D2_GROUPS, g1 = min(g0 + D2_GROUPS, a.groups);
