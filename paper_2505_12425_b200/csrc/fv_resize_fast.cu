@@ -140,7 +140,10 @@ __device__ __forceinline__ void up2_h(const uint32_t (&w)[Up2<C>::NW], int t, in
     f2split(A, a0, a1);
     f2split(B, b0, b1);
     f2split(D, d0, d1);
-    const f2_t PX = fmul2(f2u(a1, b0), t4), PY = fmul2(f2u(b1, d0), t4);
+    // scalar products written straight into the two halves of a pair (an
+    // f32x2 product of the re-paired {v0, v1} would first need two moves)
+    const f2_t PX = f2(__fmul_rn(__uint_as_float(a1), 0.75f), __fmul_rn(__uint_as_float(b0), 0.75f));
+    const f2_t PY = f2(__fmul_rn(__uint_as_float(b1), 0.75f), __fmul_rn(__uint_as_float(d0), 0.75f));
     f2_t E01 = ffma2(A, q4, PX);
     const f2_t E23 = ffma2(B, q4, PY), O01 = ffma2(B, q4, PX);
     f2_t O23 = ffma2(D, q4, PY);
