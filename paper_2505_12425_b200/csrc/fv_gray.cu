@@ -106,6 +106,12 @@ __global__ void __launch_bounds__(128) gray_u8_vec_kernel(const uint8_t* __restr
 #define FV_GRAY_THREADS 512
 #endif
 constexpr int kFlatThreads = FV_GRAY_THREADS;
+#ifndef FV_GRAY_GY
+#define FV_GRAY_GY 65535  // vec kernel: grid rows (each thread loops over h / FV_GRAY_GY rows)
+#endif
+#ifndef FV_GRAY_FLAT_MAX
+#define FV_GRAY_FLAT_MAX (148 * 2048 * 4)  // 16-pixel groups up to which the flat kernel runs
+#endif
 #ifndef FV_GRAY_PX
 #define FV_GRAY_PX 8  // measured: 16 -> 8 pixels per thread 3.3 -> 2.9 us per 1080p frame; 4 is slower
 #endif
@@ -262,12 +268,12 @@ int fv_gray_from_rgb_u8(const uint8_t* src, int64_t s_is, int64_t s_rp, uint8_t*
   int rc = check_common(src, dst, n, h, w, "fv_gray_from_rgb_u8");
   if (rc || n == 0) return rc;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  const int gy = h < 65535 ? h : 65535;
+  const int gy = h < FV_GRAY_GY ? h : FV_GRAY_GY;
   if (al16(src) && al16(dst) && al16(s_is) && al16(s_rp) && al16(d_is) && al16(d_rp)) {
     const int groups = (w + 15) / 16;
     const int64_t total16 = (int64_t)n * h * groups;
     const int64_t total = (int64_t)n * h * ((w + FV_GRAY_PX - 1) / FV_GRAY_PX);
-    if (total16 <= (int64_t)148 * 2048 * 4) {  // small batches: one flat wave of large CTAs
+    if (total16 <= (int64_t)FV_GRAY_FLAT_MAX) {  // small batches: one flat wave of large CTAs
       cudaLaunchConfig_t cfg = {};
       cfg.gridDim = dim3((unsigned)((total + kFlatThreads - 1) / kFlatThreads));
       cfg.blockDim = dim3(kFlatThreads);
