@@ -19,7 +19,8 @@
 //                  STAGED_IN = the box lies inside the image, so no pixel
 //                  needs a bounds test;
 //        DIRECT    W changes sign in the tile, or the box is too large
-//                  (zoom-out): direct global gathers.
+//                  (zoom-out): direct global gathers, after one bulk L2
+//                  prefetch per box row (boxes <= FV_PT_PF_MAX bytes).
 //   2. Maps: one f64 anchor per 32 pixels of a row (lanes 0-23 of a warp
 //      compute the 24 anchors of its 6 rows at once) -- s_a = (X, Y) / W at
 //      the group's first pixel, relative to the tile origin -- then lane L
@@ -64,6 +65,9 @@ constexpr int PT_RPW = PT_TH / PT_NW;  // rows per warp (rows warp, warp + PT_NW
 #endif
 constexpr int PT_WROWS = FV_PT_WROWS;  // SMEM window rows
 constexpr float PT_MAX_ERR = 5e-4f;
+#ifndef FV_PT_PF_MAX
+#define FV_PT_PF_MAX 196608  // DIRECT tiles: L2 prefetch of the box when it holds at most this many bytes (0 = off)
+#endif
 #ifndef PT_MINB
 #define PT_MINB 4
 #endif
@@ -557,6 +561,15 @@ __global__ void __launch_bounds__(PT_NW * 32, PT_MINB) warp_persp_tile_kernel(co
     return;
   }
   const bool staged = t.cls == PT_STAGED;
+  if (FV_PT_PF_MAX > 0 && !staged && pa.stage_ok && t.rows > 0 && t.rows * t.len <= FV_PT_PF_MAX) {
+    // a DIRECT tile's gathers walk its box row by row, each step waiting
+    // on DRAM: one bulk L2 prefetch per box row (one per thread) starts the
+    // whole box's DRAM reads now, so the later steps hit L2
+    const uint8_t* g = simg + (int64_t)t.cy0 * a.s_rp + t.sb0;
+    for (int r = threadIdx.x; r < t.rows; r += PT_NW * 32)
+      asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(g + (int64_t)r * a.s_rp), "r"((uint32_t)t.len)
+                   : "memory");
+  }
   if (warp == 0) ap = pt_anchor_map(m, tx0, ty0, warp, lane);
   if (staged) {  // every warp streams its share of the window's row segments (rows warp, warp + PT_NW, ...):
     // a bulk copy takes uniform operands, so one warp would issue the rows one at a time
