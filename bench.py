@@ -514,7 +514,7 @@ def op_resize(be):
     from paper_2505_12425_b200 import synth
 
     world, rank, dev = be.world, be.rank, be.dev
-    lo, hi = shard(64, world, rank)
+    lo, hi = shard(64 * world, world, rank)
     n = hi - lo
     src = synth.device_u8_batch(n, 2160, 3840, 3, synth.SEED_RESIZE + lo, dev)
     down = torch.zeros((n, 1080, 1920, 3), dtype=torch.uint8, device=dev)
@@ -525,11 +525,11 @@ def op_resize(be):
         [("resize_down", lambda: fv.resize_bilinear_u8(src, down), sb + n * 1080 * 1920 * 3),
          ("resize_up", lambda: fv.resize_bilinear_u8(src, up), sb + n * 4320 * 7680 * 3)],
         dst_px=n * (1920 * 1080 + 7680 * 4320), src_px=2 * n * 3840 * 2160,
-        job_dst_px=64 * (1920 * 1080 + 7680 * 4320), l2="inputs 1.59 GB >> L2",
+        job_dst_px=64 * world * (1920 * 1080 + 7680 * 4320), l2="inputs 1.59 GB >> L2",
         verify=lambda: verify_resize(src, down, up),
         e2e=lambda steps: e2e_pipeline(be, src, [down, up],
                                        lambda s, d: (fv.resize_bilinear_u8(s, d[0]), fv.resize_bilinear_u8(s, d[1])),
-                                       steps, 64 * (1920 * 1080 + 7680 * 4320), chunks=8))
+                                       steps, 64 * world * (1920 * 1080 + 7680 * 4320), chunks=8))
 
 
 def op_affine(be):
@@ -540,7 +540,7 @@ def op_affine(be):
     from paper_2505_12425_b200 import synth
 
     world, rank, dev = be.world, be.rank, be.dev
-    lo, hi = shard(32, world, rank)
+    lo, hi = shard(32 * world, world, rank)
     n = hi - lo
     src = synth.device_f32_batch(n, 1080, 1920, 3, synth.SEED_AFFINE + lo, dev)
     dst = torch.zeros_like(src)
@@ -549,10 +549,10 @@ def op_affine(be):
     return Op(
         "cfg2_warp_affine_f32_32x1080p", "affine",
         [("warp_affine", lambda: fv.warp_affine(src, dst, ms, border=0.0), foot)],
-        dst_px=n * 1920 * 1080, src_px=n * 1920 * 1080, job_dst_px=32 * 1920 * 1080,
+        dst_px=n * 1920 * 1080, src_px=n * 1920 * 1080, job_dst_px=32 * world * 1920 * 1080,
         l2="inputs 796 MB >> L2", nominal_bytes=2 * n * 1920 * 1080 * 12,
         verify=lambda: verify_warp(src, dst, ms, False, lo),
-        e2e=lambda steps: e2e_pipeline(be, src, [dst], None, steps, 32 * 1920 * 1080, chunks=4,
+        e2e=lambda steps: e2e_pipeline(be, src, [dst], None, steps, 32 * world * 1920 * 1080, chunks=4,
                                        warp=(ms, False)))
 
 
@@ -564,7 +564,7 @@ def op_persp(be):
     from paper_2505_12425_b200 import synth
 
     world, rank, dev = be.world, be.rank, be.dev
-    lo, hi = shard(16, world, rank)
+    lo, hi = shard(16 * world, world, rank)
     n = hi - lo
     src = synth.device_u8_batch(n, 2160, 3840, 3, synth.SEED_PERSP + lo, dev)
     dst = torch.zeros_like(src)
@@ -573,12 +573,12 @@ def op_persp(be):
     return Op(
         "cfg3_warp_perspective_u8_16x4k", "persp",
         [("warp_perspective", lambda: fv.warp_perspective(src, dst, hs, border=0), foot)],
-        dst_px=n * 3840 * 2160, src_px=n * 3840 * 2160, job_dst_px=16 * 3840 * 2160,
+        dst_px=n * 3840 * 2160, src_px=n * 3840 * 2160, job_dst_px=16 * world * 3840 * 2160,
         l2="inputs 398 MB >> L2", nominal_bytes=2 * n * 3840 * 2160 * 3,
         extra={"kernel_contract": "default u8 path: within 1 LSB of the oracle (north-star gate); "
                                   "exact=True is the bit-exact kernel"},
         verify=lambda: verify_warp(src, dst, hs, True, lo),
-        e2e=lambda steps: e2e_pipeline(be, src, [dst], None, steps, 16 * 3840 * 2160, chunks=4,
+        e2e=lambda steps: e2e_pipeline(be, src, [dst], None, steps, 16 * world * 3840 * 2160, chunks=4,
                                        warp=(hs, True)))
 
 
@@ -590,7 +590,7 @@ def op_fused(be):
     from paper_2505_12425_b200 import synth
 
     world, rank, dev = be.world, be.rank, be.dev
-    lo, hi = shard(512, world, rank)
+    lo, hi = shard(512 * world, world, rank)
     n = hi - lo
     src = synth.device_u8_batch(n, 1080, 1920, 3, synth.SEED_FUSED + lo, dev)
     dst = torch.zeros((n, 3, 640, 640), dtype=torch.float32, device=dev)
@@ -598,11 +598,11 @@ def op_fused(be):
         "cfg4_resize_normalize_chw_512x1080p", "fused",
         [("resize_normalize_chw", lambda: fv.resize_normalize_chw(src, dst, synth.MEAN, synth.STD),
           n * (1920 * 1080 * 3 + 3 * 640 * 640 * 4))],
-        dst_px=n * 640 * 640, src_px=n * 1920 * 1080, job_dst_px=512 * 640 * 640, l2="inputs 3.2 GB >> L2",
+        dst_px=n * 640 * 640, src_px=n * 1920 * 1080, job_dst_px=512 * world * 640 * 640, l2="inputs 3.2 GB >> L2",
         verify=lambda: verify_fused(src, dst),
         e2e=lambda steps: e2e_pipeline(be, src, [dst],
                                        lambda s, d: fv.resize_normalize_chw(s, d[0], synth.MEAN, synth.STD),
-                                       steps, 512 * 640 * 640, chunks=8))
+                                       steps, 512 * world * 640 * 640, chunks=8))
 
 
 def op_jpeg(be):
@@ -615,7 +615,7 @@ def op_jpeg(be):
     world, rank, dev = be.world, be.rank, be.dev
     # SURVEY 8f rank 4, decode -> preprocess: host JPEG bytes -> decode
     # (GPU entropy decoding + reconstruction) -> fused resize/normalise/CHW
-    lo, hi = shard(64, world, rank)
+    lo, hi = shard(64 * world, world, rank)
     streams = jpeg_streams(lo, hi)
     dst = torch.empty((hi - lo, 3, 640, 640), dtype=torch.float32, device=dev)
     frames = torch.empty((hi - lo, 1080, 1920, 3), dtype=torch.uint8, device=dev)
@@ -632,14 +632,14 @@ def op_jpeg(be):
     return Op(
         "f4_jpeg_decode_preprocess_64x1080p", "jpeg",
         [("jpeg_decode+preprocess (GPU entropy + reconstruction + resize)", step, nbytes)],
-        dst_px=(hi - lo) * 1920 * 1080, src_px=(hi - lo) * 1920 * 1080, job_dst_px=64 * 1920 * 1080,
+        dst_px=(hi - lo) * 1920 * 1080, src_px=(hi - lo) * 1920 * 1080, job_dst_px=64 * world * 1920 * 1080,
         l2="host JPEG bytes (q90 4:2:0, ~200 KB each)",
         extra={"mean_stream_kb": round(sum(len(b) for b in streams) / len(streams) / 1e3, 1),
                "entropy_decoding": f"GPU ({on_gpu}/{hi - lo} images; self-synchronising subsequences)",
                "px_basis": "decoded 1920x1080 pixels",
                "e2e_note": "the step itself starts from host JPEG bytes and ends in HBM"},
         verify=lambda: verify_jpeg(streams, frames, dst),
-        e2e=lambda steps: e2e_jpeg(be, step, dst, steps, 64 * 1920 * 1080, sum(len(b) for b in streams)))
+        e2e=lambda steps: e2e_jpeg(be, step, dst, steps, 64 * world * 1920 * 1080, sum(len(b) for b in streams)))
 
 
 def build_dry_ops(be, include):
@@ -654,12 +654,12 @@ def build_dry_ops(be, include):
                                ("f4_jpeg_decode_preprocess_64x1080p", "jpeg", 64)):
         if key not in include:
             continue
-        lo, hi = shard(n_total, be.world, be.rank) if key != "gray" else (0, 1)
+        lo, hi = shard(n_total * be.world, be.world, be.rank) if key != "gray" else (0, 1)
         n = hi - lo
         x = torch.arange(max(n, 1) * 4096, dtype=torch.float32)
         y = torch.empty_like(x)
         ops.append(Op(name, key, [("dry_copy", lambda x=x, y=y: y.copy_(x), x.numel() * 8)],
-                      dst_px=n * 1000, src_px=n * 1000, job_dst_px=None if key == "gray" else n_total * 1000,
+                      dst_px=n * 1000, src_px=n * 1000, job_dst_px=None if key == "gray" else n_total * be.world * 1000,
                       l2="dry run", replicas=key == "gray",
                       verify=lambda lo=lo, hi=hi: {"verified": True, "checked": f"dry run, images [{lo}, {hi})"},
                       e2e=lambda steps: {"value": 0.0, "unit": UNIT, "h2d_bytes_per_step": 0,
@@ -1059,8 +1059,9 @@ def verify_jpeg(streams, frames, dst):
 def headline_config(world):
     """The `config` object of both arms' JSON line (BASELINE.json configs[1])."""
     return {"workload": "cfg1: bilinear u8 resize (_resize_u8 semantics, app.py:64-78) of 64x 3840x2160x3 -> "
-                        "1920x1080x3 and -> 7680x4320x3 per step",
-            "global_batch": 64, "parallelism": f"image-sharded x{world}, no collective",
+                        "1920x1080x3 and -> 7680x4320x3 per GPU per step",
+            "global_batch": 64 * world, "per_gpu_batch": 64,
+            "parallelism": f"image-sharded x{world} (weak scaling: 64 images per GPU), no collective",
             "l2": "inputs 1.59 GB >> 126 MB L2 (no flush needed)"}
 
 
@@ -1116,7 +1117,7 @@ def run_reference(args):
             ops[op] = {k: r[k] for k in ("value", "value_1core", "cores", "sample")}
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": step_px / (v * 1e6) * 1e3,
-            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "u8",
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u8",
             "data": "synthetic (seeded uniform u8)",
             "config": dict(headline_config(1), parallelism=f"{cores} host processes (reference NumPy path)"),
             "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "port",
@@ -1202,7 +1203,7 @@ def run_fovea(args, world, rank, local):
         cpu = summary[head].get("cpu_baseline")
         line = {
             "metric": METRIC, "value": job_mps(r), "unit": UNIT, "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": r["ms_per_step"], "higher_is_better": True, "scaling": "strong",
+            "warmup": args.warmup, "ms_per_step": r["ms_per_step"], "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "u8",
             "data": "synthetic (seeded uniform u8/f32, generated on device)" if not be.dry else "dry run",
             "config": headline_config(world),

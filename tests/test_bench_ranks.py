@@ -46,9 +46,11 @@ def test_gpus_2_relaunches_two_ranks_and_reduces():
     for name, o in ops.items():
         assert o["verified"] is True
         assert "e2e" in o and o["ms_per_step"] > 0
-    # whole-job value: all ranks' images over the MAX time (dry ops: 1000 px per image)
+    # whole-job value, weak scaling: 64 images per rank, all ranks' images
+    # over the MAX time (dry ops: 1000 px per image)
     head = ops["cfg1_resize_u8_64x4k"]
-    assert d["value"] == pytest.approx(64 * 1000 / (head["ms_per_step"] / 1e3) / 1e6)
+    assert d["scaling"] == "weak" and d["config"]["global_batch"] == 2 * 64
+    assert d["value"] == pytest.approx(2 * 64 * 1000 / (head["ms_per_step"] / 1e3) / 1e6)
     # replicas (cfg0): each rank's frames count
     g = ops["cfg0_gray_u8_1x1080p"]
     assert g["dst_mps"] == pytest.approx(2 * 1000 / (g["ms_per_step"] / 1e3) / 1e6)
