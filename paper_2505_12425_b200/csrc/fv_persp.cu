@@ -41,7 +41,8 @@
 //      (warp_tap, the exact kernel's). Bilinear sampling with a constant
 //      border is continuous in (sx, sy), so |out - oracle| <= 255 * 1e-3 +
 //      (blend roundings ~3e-4) < 1 LSB.
-//   4. Blend on the 0..255 scale (magic-word taps, FFMA2, floor(v + 0.5)),
+//   4. Blend on the 0..255 scale (magic-word taps; two horizontal lerps and a
+//      vertical one as FFMA2 on pixel pairs, floor(v + 0.5)),
 //      results stored as bytes into a per-warp SMEM row buffer; the warp then
 //      writes the row segment (384 B for C = 3) with 16-byte stores.
 #include "fv_warp.cuh"
@@ -65,6 +66,9 @@ constexpr int PT_RPW = PT_TH / PT_NW;  // rows per warp (rows warp, warp + PT_NW
 #endif
 constexpr int PT_WROWS = FV_PT_WROWS;  // SMEM window rows
 constexpr float PT_MAX_ERR = 5e-4f;
+#ifndef FV_PT_LERP
+#define FV_PT_LERP 1  // blend as two horizontal lerps and a vertical one (27 f32x2 ops per pixel pair, not 31)
+#endif
 #ifndef FV_PT_PF_MAX
 #define FV_PT_PF_MAX 196608  // DIRECT tiles: L2 prefetch of the box when it holds at most this many bytes (0 = off)
 #endif
@@ -391,6 +395,24 @@ __device__ __forceinline__ void pt_rows(const WarpArgs& a, const PtArgs& pa, con
         pt_taps<C>(w[k][0], sh[k], v00[k], v01[k]);
         pt_taps<C>(w[k][1], sh[k], v10[k], v11[k]);
       }
+#if FV_PT_LERP
+      // a = u00 + fx (u01 - u00) + 0.5, b likewise, v = a + fy (b - a): the
+      // tap differences are exact on the magic words, u + 0.5 = M - (2^23 -
+      // 0.5) exactly; each lerp rounds once (|error| < 2^-16 on the 0..256
+      // scale, far inside the <= 1 LSB gate)
+      const f2_t HM = f2(-8388607.5f, -8388607.5f);
+#pragma unroll
+      for (int c = 0; c < C; ++c) {
+        const f2_t M00 = f2u(v00[0][c], v00[1][c]), M01 = f2u(v01[0][c], v01[1][c]);
+        const f2_t M10 = f2u(v10[0][c], v10[1][c]), M11 = f2u(v11[0][c], v11[1][c]);
+        const f2_t A = ffma2(WX1, ffma2(M00, NEG1, M01), fadd2(M00, HM));
+        const f2_t B = ffma2(WX1, ffma2(M10, NEG1, M11), fadd2(M10, HM));
+        const f2_t v = ffma2(WY1, ffma2(A, NEG1, B), A);
+        uint32_t lo, hi;
+        f2split(fadd2_rd(v, MAG), lo, hi);  // floor(v) in the low byte (0 <= v < 256)
+        asm volatile("st.shared.u8 [%0], %1;" ::"r"(o0 + c), "r"(lo));
+        if (v1) asm volatile("st.shared.u8 [%0], %1;" ::"r"(o0 + 32 * C + c), "r"(hi));
+#else
       const f2_t WX0 = ffma2(WX1, NEG1, ONE), WY0 = ffma2(WY1, NEG1, ONE);
       const f2_t W00 = fmul2(WX0, WY0), W01 = fmul2(WX1, WY0), W10 = fmul2(WX0, WY1), W11 = fmul2(WX1, WY1);
       // first tap straight from its magic word M = 2^23 + u: C00 = 0.5 -
@@ -405,6 +427,7 @@ __device__ __forceinline__ void pt_rows(const WarpArgs& a, const PtArgs& pa, con
         f2split(fadd2_rd(v, MAG), lo, hi);  // floor(v) in the low byte (0 <= v < 256)
         asm volatile("st.shared.u8 [%0], %1;" ::"r"(o0 + c), "r"(lo));
         if (v1) asm volatile("st.shared.u8 [%0], %1;" ::"r"(o0 + 32 * C + c), "r"(hi));
+#endif
       }
     }
     __syncwarp();
