@@ -47,6 +47,42 @@ __device__ __forceinline__ uint32_t gray_u8_word(uint32_t v) {
   return q;
 }
 
+// Four pixels from their 12 bytes (three words) to one output word. Per pixel
+// the 64-bit product (S + 500) * M, M = ceil(2^32 / 1000) = 4294968, gives the
+// quotient in its high word (M * 1000 - 2^32 = 704, and 704 S / (1000 * 2^32) <
+// 1 / 1000 for S + 500 <= 255500) and the tie test in its low one: with S + 500 =
+// 1000 q + t the low word is 704 q + t M < 2^32, below M exactly when t = 0.
+// The four tie flags OR into one predicate, so the rare f64 re-run costs one
+// branch per output word instead of one per pixel (FV_GRAY_QUAD_TIE 0: the
+// per-pixel branch, the A/B baseline).
+#ifndef FV_GRAY_QUAD_TIE
+#define FV_GRAY_QUAD_TIE 1
+#endif
+__device__ __forceinline__ uint32_t gray_u8_quad(const uint32_t* wd) {
+  uint32_t w3[4] = {wd[0], __funnelshift_r(wd[0], wd[1], 24), __funnelshift_r(wd[1], wd[2], 16), wd[2] >> 8};
+  uint32_t q[4];
+#if FV_GRAY_QUAD_TIE
+  bool tie = false;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const uint32_t lo = __dp4a(w3[i], 0x00724B2Bu, 500u);  // 43 r + 75 g + 114 b + 500
+    const uint32_t hi = __dp4a(w3[i], 0x00000201u, 0u);    // r + 2 g
+    const uint64_t p = (uint64_t)((hi << 8) + lo) * 4294968u;
+    q[i] = (uint32_t)(p >> 32);
+    tie |= (uint32_t)p < 4294968u;
+  }
+  if (tie) {  // 12% of warps per word on uniform random input; re-running only the tie pixels from the kept low
+              // words measured slower (0.0477 vs 0.0456 ms for 32 frames), as did 2 or 4 rows per thread on top
+#pragma unroll
+    for (int i = 0; i < 4; ++i) q[i] = gray_u8_word(w3[i]);
+  }
+#else
+#pragma unroll
+  for (int i = 0; i < 4; ++i) q[i] = gray_u8_word(w3[i]);
+#endif
+  return pack4(q[0], q[1], q[2], q[3]);
+}
+
 // 16 pixels per thread; all of src/dst base, pitch and image stride are
 // 16-byte aligned (checked on the host). Luma by two IDP4A per pixel
 // (gray_u8_word): 0.058 -> 0.050 ms for 32 1080p frames in one launch (the
@@ -72,15 +108,8 @@ __global__ void __launch_bounds__(128) gray_u8_vec_kernel(const uint8_t* __restr
       const uint32_t* wd = reinterpret_cast<const uint32_t*>(v);
       uint32_t out[4] = {0, 0, 0, 0};
 #if FV_GRAY_DP4A
-      uint32_t q[16];
 #pragma unroll
-      for (int i = 0; i < 16; ++i) {
-        const int k = 3 * i;  // pixel i's bytes start at byte k of the 48
-        const uint32_t w3 = (k & 3) ? __funnelshift_r(wd[k >> 2], wd[(k >> 2) + 1], (k & 3) * 8) : wd[k >> 2];
-        q[i] = gray_u8_word(w3);
-      }
-#pragma unroll
-      for (int j = 0; j < 4; ++j) out[j] = pack4(q[4 * j], q[4 * j + 1], q[4 * j + 2], q[4 * j + 3]);
+      for (int j = 0; j < 4; ++j) out[j] = gray_u8_quad(wd + 3 * j);
 #else
 #pragma unroll
       for (int i = 0; i < 16; ++i) {
@@ -167,14 +196,8 @@ __global__ void __launch_bounds__(kFlatThreads) gray_u8_flat_kernel(const uint8_
     }
     uint32_t out[PX / 4];
 #if FV_GRAY_DP4A
-    uint32_t q[PX];
 #pragma unroll
-    for (int i = 0; i < PX; ++i) {
-      const int k = 3 * i;
-      q[i] = gray_u8_word((k & 3) ? __funnelshift_r(wd[k >> 2], wd[(k >> 2) + 1], (k & 3) * 8) : wd[k >> 2]);
-    }
-#pragma unroll
-    for (int j = 0; j < PX / 4; ++j) out[j] = pack4(q[4 * j], q[4 * j + 1], q[4 * j + 2], q[4 * j + 3]);
+    for (int j = 0; j < PX / 4; ++j) out[j] = gray_u8_quad(wd + 3 * j);
 #else
 #pragma unroll
     for (int i = 0; i < PX / 4; ++i) out[i] = 0;
