@@ -88,6 +88,7 @@ __device__ __forceinline__ uint32_t gray_u8_quad(const uint32_t* wd) {
 // (gray_u8_word): 0.058 -> 0.050 ms for 32 1080p frames in one launch (the
 // per-byte extraction made this kernel issue-bound); loading two or four
 // rows per thread before the arithmetic measured slower (0.060 / 0.064 ms).
+// One tie branch per output word (gray_u8_quad): 0.050 -> 0.0456 ms.
 __global__ void __launch_bounds__(128) gray_u8_vec_kernel(const uint8_t* __restrict__ src, int64_t s_is,
                                                           int64_t s_rp, uint8_t* __restrict__ dst,
                                                           int64_t d_is, int64_t d_rp, int h, int w) {
