@@ -41,3 +41,21 @@ def test_tiny_inputs_round_to_zero():
         assert (ref == 0).all()
         fused = np.floor((x.astype(np.float64) * K + 0.5).astype(np.float32))
         assert (fused == 0).all()
+
+
+def test_gray_quotient_and_tie_from_one_product():
+    """fv_gray.cu:gray_u8_quad: for every S + 500 the kernel can form
+    (500 .. 255 * 1000 + 500) the high word of (S + 500) * M, M = ceil(2^32 /
+    1000), is (S + 500) // 1000 and the low word is below M exactly when
+    (S + 500) % 1000 == 0 (the decimal ties that re-run the f64 path); and
+    S + 500 = 256 (r + 2 g) + (43 r + 75 g + 114 b + 500), the two byte dot
+    products, for the extreme triples."""
+    M = np.uint64(4294968)
+    assert int(M) == -(-(1 << 32) // 1000)
+    s = np.arange(500, 255 * 1000 + 501, dtype=np.uint64)
+    p = s * M
+    hi, lo = p >> np.uint64(32), p & np.uint64(0xFFFFFFFF)
+    assert np.array_equal(hi, s // np.uint64(1000))
+    assert np.array_equal(lo < M, s % np.uint64(1000) == 0)
+    for r, g, b in [(0, 0, 0), (255, 255, 255), (255, 0, 0), (0, 255, 0), (0, 0, 255), (1, 2, 3)]:
+        assert 256 * (r + 2 * g) + (43 * r + 75 * g + 114 * b + 500) == 299 * r + 587 * g + 114 * b + 500
