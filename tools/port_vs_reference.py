@@ -22,3 +22,10 @@ img2 = Image(Tensor.from_shape_slice(a2.shape, a2.reshape(-1), dtype=np.uint8), 
 tr, r = t(lambda: _resize_u8(img2, ImageSize(1920,1080), 'bilinear'))
 to, o = t(lambda: O.resize_u8(a2, 1920, 1080))
 print('up2   ref %.3fs port %.3fs  equal %s' % (tr, to, np.array_equal(r.as_array().reshape(o.shape), o)))
+from fovea import imgproc
+g = O.seeded_u8_image(1920, 1080, 3, 2)
+gsrc = Image(Tensor.from_shape_slice(g.shape, g.reshape(-1), dtype=np.uint8), 3)
+gdst = Image(Tensor.from_shape_slice((1080, 1920, 1), np.zeros(1080 * 1920, np.uint8), dtype=np.uint8), 1)
+tr, _ = t(lambda: imgproc.gray_from_rgb(gsrc, gdst))
+to, o = t(lambda: O.gray_from_rgb(g))
+print('gray  ref %.3fs port %.3fs  equal %s' % (tr, to, np.array_equal(gdst.as_array().reshape(o.shape), o)))
