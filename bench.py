@@ -1119,8 +1119,9 @@ def run_reference(args):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": step_px / (v * 1e6) * 1e3,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u8",
             "data": "synthetic (seeded uniform u8)",
-            "config": dict(headline_config(1), parallelism=f"{cores} host processes (reference NumPy path)"),
+            "config": headline_config(1),  # the fovea arm's own N=1 config, key for key (the driver compares them)
             "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "port",
+                             "host_parallelism": f"{cores} host processes (reference NumPy path)",
                              "value_1core": vals[0]["value_1core"],
                              "sample": CPU_SAMPLE["resize"] + "; oracle/ NumPy port of the reference"},
             "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
